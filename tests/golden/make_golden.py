@@ -1,0 +1,146 @@
+"""Generates the golden vectors in this directory from the REFERENCE ITSELF.
+
+Run in a container that has /root/reference (the reference headers compiled behind
+oracle/ref_shim.cpp by `make -C oracle ref`):
+
+    python tests/golden/make_golden.py
+
+The vectors pin the C restatement (oracle/ffdp_oracle.c) through
+tests/test_oracle_golden.py, which runs anywhere (no /root/reference needed). Inputs
+are regenerated from seeds with the reference's own splitmix64 Rng (rng.hpp), mirroring
+the fixture patterns of the reference tests (test_sampler.cpp:30-61 margin fixture,
+test_lncc.cpp, test_mi.cpp:56-69, test_distops.cpp).
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import Oracle, Reference, step_inputs  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def margin_fixture(orc, seed, img_shape, out_shape, perturb):
+    """test_sampler.cpp:30-61: fractional source indices in [0.15, 0.85]."""
+    r = orc.rng(seed)
+    L = orc.lib
+    import ctypes as C
+    img = orc.random_volume(r, img_shape)
+    S = np.array([1.25, 0.8, 1.1])
+    A = np.eye(3)
+    t = np.zeros(3)
+    if perturb:
+        for i in range(3):
+            for j in range(3):
+                A[i, j] = (1.0 if i == j else 0.0) + (-0.05 + 0.1 * L.or_rng_uniform(C.byref(r)))
+        t = np.array([-0.05 + 0.1 * L.or_rng_uniform(C.byref(r)) for _ in range(3)])
+    onz, ony, onx = out_shape
+    inz, iny, inx = img_shape
+    n_img = (inx, iny, inz)
+    u = np.zeros(tuple(out_shape) + (3,))
+    ax = lambda i, n: -1.0 + 2.0 * (i / (n - 1))
+    for z in range(onz):
+        for y in range(ony):
+            for x in range(onx):
+                X = np.array([ax(x, onx), ax(y, ony), ax(z, onz)])
+                base = A @ X + t
+                for c in range(3):
+                    n = n_img[c]
+                    cell = L.or_rng_uniform_int(C.byref(r), -1, n - 1)
+                    frac = 0.15 + 0.7 * L.or_rng_uniform(C.byref(r))
+                    target = 2.0 * (cell + frac) / (n - 1) - 1.0
+                    u[z, y, x, c] = (target - base[c]) / S[c]
+    return img, u, A, t, S
+
+
+def main():
+    orc, ref = Oracle(), Reference()
+    g = {}
+    # --- sampler: margin fixtures (fwd + every gradient), distinct in/out lattices
+    for i, (ish, osh, pert) in enumerate([((8, 8, 8), (8, 8, 8), True), ((7, 7, 7), (6, 6, 6), True),
+                                          ((6, 9, 5), (5, 4, 7), False)]):
+        img, u, A, t, S = margin_fixture(orc, 107 + i, ish, osh, pert)
+        up = orc.random_volume(orc.rng(500 + i), osh, -1.0, 1.0)
+        fw = ref.sample(img, u, A, t, S)
+        bw = ref.sample(img, u, A, t, S, upstream=up, want=("image", "warp", "affine", "translation"))
+        g.update({f"smp{i}_img": img, f"smp{i}_u": u, f"smp{i}_A": A, f"smp{i}_t": t, f"smp{i}_S": S,
+                  f"smp{i}_up": up, f"smp{i}_out": fw["out"], f"smp{i}_gimg": bw["image"],
+                  f"smp{i}_gu": bw["warp"], f"smp{i}_gA": bw["affine"], f"smp{i}_gt": bw["translation"]})
+    # sampler on a face (test_sampler.cpp:225-241) and with sharded output bounds
+    r = orc.rng(137)
+    img = orc.random_volume(r, (6, 6, 6))
+    u = np.zeros((6, 6, 6, 3))
+    u[2, 2, 2, 0] = (2.0 * 3.0 / 5.0 - 1.0) - (-1.0 + 2.0 * 2 / 5)
+    up = np.zeros((6, 6, 6))
+    up[2, 2, 2] = 1.0
+    bw = ref.sample(img, u, upstream=up, want=("warp",))
+    g.update({"face_img": img, "face_u": u, "face_up": up, "face_gu": bw["warp"]})
+    bounds = np.array([-1, -1, -0.2, 1, 1, 0.6])
+    img = orc.random_volume(orc.rng(141), (9, 8, 7))
+    u = orc.random_volume(orc.rng(142), (4, 8, 7, 3), -0.05, 0.05)
+    fw = ref.sample(img, u, bounds=bounds)
+    g.update({"bnd_img": img, "bnd_u": u, "bnd_bounds": bounds, "bnd_out": fw["out"]})
+
+    # --- LNCC: fwd (loss, state, map) + bwd ANTs / exact, odd lattice, windows 7 and 3
+    for i, (sh, w) in enumerate([((12, 11, 10), 7), ((9, 10, 13), 3), ((5, 6, 7), 7)]):
+        r = orc.rng(211 + i)
+        f = orc.random_volume(r, sh)
+        m = orc.random_volume(r, sh)
+        for ants in (True, False):
+            res = ref.lncc(f, m, window=w, eps=1e-5, ants=ants, upstream=1.3, want_map=True)
+            k = f"lncc{i}_{'ants' if ants else 'exact'}"
+            g.update({f"{k}_loss": np.array(res["loss"]), f"{k}_gf": res["grad_f"], f"{k}_gm": res["grad_m"]})
+        g.update({f"lncc{i}_f": f, f"lncc{i}_m": m, f"lncc{i}_w": np.array(w), f"lncc{i}_state": res["state"],
+                  f"lncc{i}_map": res["map"]})
+
+    # --- MI: exact / approx, three kernels, B = 8 and 32, margin-filled intensities
+    r = orc.rng(311)
+    vi = orc.random_volume(r, (6, 7, 8), 0.0, 1.0)
+    vj = np.clip(0.6 * vi + 0.4 * orc.random_volume(r, (6, 7, 8)), 0, 1)
+    g.update({"mi_i": vi, "mi_j": vj})
+    for kind in ("gaussian", "bspline3", "delta"):
+        for bins in (8, 32):
+            for approx in (False, True):
+                res = ref.mi(vi, vj, bins=bins, kind=kind, approx=approx, upstream=-1.0)
+                k = f"mi_{kind}_{bins}_{int(approx)}"
+                g.update({f"{k}_mi": np.array(res["mi"]), f"{k}_raw": res["raw"], f"{k}_pij": res["pij"],
+                          f"{k}_stats": np.array(res["stats"], dtype=np.uint64), f"{k}_gi": res["grad_i"],
+                          f"{k}_gj": res["grad_j"]})
+    xs = np.linspace(-0.2, 0.2, 401)
+    for kind in ("gaussian", "bspline3", "delta"):
+        kap, om = ref.parzen_eval(kind, 32, xs)
+        g.update({f"parzen_{kind}_kappa": kap, f"parzen_{kind}_omega": om})
+    g["parzen_x"] = xs
+
+    # --- synth pair + the full step at H = 1 and H = 2 / 3 (ring + halo + allreduce)
+    f, m, w = ref.synth_pair(4242, (16, 17, 18), 5, 0.12)
+    g.update({"synth_f": f, "synth_m": m, "synth_w": w})
+    for loss in ("lncc", "mi"):
+        si = step_inputs(orc, (18, 17, 16), seed=4242, loss=loss)
+        g.update({f"step_{loss}_f": si.f, f"step_{loss}_m": si.m, f"step_{loss}_u": si.u, f"step_{loss}_A": si.A,
+                  f"step_{loss}_t": si.t})
+        for world in (1, 2, 3):
+            res = ref.step(loss, si.f, si.m, si.u, si.A, si.t, world=world)
+            g.update({f"step_{loss}_H{world}_loss": np.array(res["loss"]), f"step_{loss}_H{world}_gu": res["g_u"],
+                      f"step_{loss}_H{world}_moved": res["moved"]})
+
+    # --- gp_convolve across shards (distops.hpp:54-101)
+    v = orc.random_volume(orc.rng(601), (11, 6, 5))
+    for world in (1, 2, 3):
+        for sync in (True, False):
+            g[f"gp_box_H{world}_s{int(sync)}"] = ref.gp_convolve(v, np.full(7, 1 / 7), world, False, sync)
+    g["gp_v"] = v
+    wv = orc.random_volume(orc.rng(602), (9, 5, 4, 3))
+    g["gp_w"] = wv
+    g["gp_gauss_H3"] = ref.gp_convolve(wv, orc.gaussian_taps(1.0), 3, True, True)
+
+    path = os.path.join(OUT, "voxreg_golden.npz")
+    np.savez_compressed(path, **g)
+    print(f"wrote {path}: {len(g)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,127 @@
+"""Pins the C restatement (oracle/ffdp_oracle.c) against golden vectors produced by the
+reference itself (tests/golden/make_golden.py over oracle/_ref). CPU only."""
+import numpy as np
+import pytest
+
+from oracle import step_inputs
+
+
+def close(a, b, tol=1e-12):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape
+    assert np.max(np.abs(a - b), initial=0.0) <= tol * max(1.0, np.max(np.abs(b), initial=0.0))
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_sampler_margin_fixtures(orc, golden, i):
+    g = lambda k: golden[f"smp{i}_{k}"]
+    fw = orc.sample(g("img"), g("u"), g("A"), g("t"), g("S"))
+    close(fw["out"], g("out"))
+    bw = orc.sample(g("img"), g("u"), g("A"), g("t"), g("S"), upstream=g("up"),
+                    want=("image", "warp", "affine", "translation"))
+    close(bw["image"], g("gimg"))
+    close(bw["warp"], g("gu"))
+    close(bw["affine"], g("gA"))
+    close(bw["translation"], g("gt"))
+
+
+def test_sampler_face_and_bounds(orc, golden):
+    bw = orc.sample(golden["face_img"], golden["face_u"], upstream=golden["face_up"], want=("warp",))
+    close(bw["warp"], golden["face_gu"])
+    img = golden["face_img"]
+    # floor cell at a face: one-sided slope (test_sampler.cpp:225-241)
+    assert bw["warp"][2, 2, 2, 0] == pytest.approx((img[2, 2, 4] - img[2, 2, 3]) * 2.5, abs=1e-12)
+    fw = orc.sample(golden["bnd_img"], golden["bnd_u"], bounds=golden["bnd_bounds"])
+    close(fw["out"], golden["bnd_out"])
+
+
+def test_sampler_rejects_bad_args(orc):
+    with pytest.raises(ValueError):
+        orc.sample(np.zeros((4, 4, 4)), np.zeros((4, 4, 4, 3)), S=[0.0, 1, 1])
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_lncc(orc, golden, i):
+    g = lambda k: golden[f"lncc{i}_{k}"]
+    w = int(g("w"))
+    loss, state, mp = orc.lncc_forward(g("f"), g("m"), window=w, eps=1e-5, want_map=True)
+    close(state, g("state"))
+    close(mp, g("map"))
+    for mode in ("ants", "exact"):
+        assert loss == pytest.approx(float(golden[f"lncc{i}_{mode}_loss"]), rel=1e-12)
+        gf, gm, _ = orc.lncc_backward(1.3, state, g("f"), g("m"), window=w, eps=1e-5, ants=(mode == "ants"))
+        close(gf, golden[f"lncc{i}_{mode}_gf"])
+        close(gm, golden[f"lncc{i}_{mode}_gm"])
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "bspline3", "delta"])
+@pytest.mark.parametrize("bins", [8, 32])
+@pytest.mark.parametrize("approx", [False, True])
+def test_mi(orc, golden, kind, bins, approx):
+    k = orc.parzen(kind, bins)
+    key = f"mi_{kind}_{bins}_{int(approx)}"
+    h = orc.mi_forward(golden["mi_i"], golden["mi_j"], k, approx=approx)
+    assert h["mi"] == pytest.approx(float(golden[f"{key}_mi"]), rel=1e-12, abs=1e-15)
+    close(h["raw"], golden[f"{key}_raw"])
+    b = bins
+    close(np.concatenate([h["p_ij"].ravel(), h["p_i"], h["p_j"]]), golden[f"{key}_pij"])
+    assert tuple(int(s) for s in h["stats"]) == tuple(int(s) for s in golden[f"{key}_stats"])
+    if not approx:
+        gi, gj, _ = orc.mi_backward(-1.0, golden["mi_i"], golden["mi_j"], k, h)
+        close(gi, golden[f"{key}_gi"])
+        close(gj, golden[f"{key}_gj"])
+    assert b == bins
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "bspline3", "delta"])
+def test_parzen(orc, golden, kind):
+    k = orc.parzen(kind, 32)
+    xs = golden["parzen_x"]
+    kap = np.array([orc.lib.or_parzen_kappa(k, float(x)) for x in xs])
+    om = np.array([orc.lib.or_parzen_omega(k, float(x)) for x in xs])
+    close(kap, golden[f"parzen_{kind}_kappa"])
+    close(om, golden[f"parzen_{kind}_omega"])
+
+
+def test_synth_pair_bit_identical(orc, golden):
+    f, m, w = orc.synth_pair(4242, (16, 17, 18), 5, 0.12)
+    assert np.array_equal(f, golden["synth_f"])
+    assert np.array_equal(m, golden["synth_m"])
+    assert np.array_equal(w, golden["synth_w"])
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_step_h1_and_shard_invariance(orc, golden, loss):
+    si = step_inputs(orc, (18, 17, 16), seed=4242, loss=loss)
+    for k in ("f", "m", "u", "A", "t"):
+        assert np.array_equal(getattr(si, k), golden[f"step_{loss}_{k}"])
+    if loss == "lncc":
+        res = orc.step_lncc(si.f, si.m, si.u, si.A, si.t)
+    else:
+        res = orc.step_mi(si.f, si.m, si.u, orc.parzen("bspline3", 32), si.A, si.t)
+    for world in (1, 2, 3):
+        ref_loss = float(golden[f"step_{loss}_H{world}_loss"])
+        assert res["loss"] == pytest.approx(ref_loss, rel=1e-10)
+        close(res["g_u"], golden[f"step_{loss}_H{world}_gu"], tol=1e-8)
+        close(res["moved"], golden[f"step_{loss}_H{world}_moved"], tol=1e-9)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_ring_sample_partials_sum_to_global(orc, golden, world):
+    """distops.hpp:144-248: per-shard zero-padded partial interpolations sum to the
+    global interpolation (restated single-process)."""
+    si = step_inputs(orc, (18, 17, 16), seed=4242, loss="lncc")
+    nz = si.f.shape[0]
+    out = []
+    for r in range(world):
+        lo, hi = orc.shard_range(nz, world, r)
+        ax = lambda i: -1.0 + 2.0 * (i / (nz - 1))
+        bounds = [-1, -1, ax(lo), 1, 1, ax(hi - 1)]
+        out.append(orc.ring_sample(si.m, world, si.u[lo:hi], bounds, si.A, si.t))
+    close(np.concatenate(out, axis=0), golden[f"step_lncc_H{world}_moved"], tol=1e-9)
+
+
+def test_shard_ranges(orc):
+    assert [orc.shard_range(10, 3, r) for r in range(3)] == [(0, 4), (4, 7), (7, 10)]
+    with pytest.raises(ValueError):
+        orc.shard_range(2, 3, 0)
