@@ -1,0 +1,257 @@
+/*
+ * ffdp.h -- C ABI of the B200-native fused warp + loss step (libffdp.so, sm_100a).
+ *
+ * Drop-in boundary for the hot path of the voxreg reference engine
+ * (/root/reference/proj/include/voxreg). Every entry point names the reference
+ * interface it replaces (file:line). Conventions:
+ *
+ *  - all array arguments are DEVICE pointers (cudaMalloc'd, fp32 unless stated);
+ *    scalars are host values; `stream` is a cudaStream_t (NULL = legacy default);
+ *  - volumes are x-fastest, index (z*ny + y)*nx + x (volume.hpp:3-7,41-43);
+ *    warp fields interleave xyz per voxel, index 3*voxel + c (volume.hpp:57,69-71);
+ *  - outputs are caller-owned buffers; nothing is allocated on the caller's behalf
+ *    except stream-ordered scratch that is released before the call returns;
+ *  - every call returns an ffdp_status; on failure ffdp_last_error() (thread-local)
+ *    holds the message. Status codes map onto the reference's exception types:
+ *    FFDP_INVALID_ARGUMENT <-> std::invalid_argument, FFDP_RUNTIME <-> std::runtime_error,
+ *    FFDP_LOGIC <-> std::logic_error (mi.hpp:132), FFDP_CUDA for device failures.
+ *  - there is no CPU fallback: without a usable sm_100a device every call fails
+ *    with FFDP_CUDA.
+ */
+#ifndef FFDP_H
+#define FFDP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFDP_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FFDP_API __attribute__((visibility("default")))
+#else
+#define FFDP_API
+#endif
+
+typedef enum {
+    FFDP_OK = 0,
+    FFDP_INVALID_ARGUMENT = 1,
+    FFDP_RUNTIME = 2,
+    FFDP_LOGIC = 3,
+    FFDP_CUDA = 4
+} ffdp_status;
+
+/* Dims3 (geometry.hpp:88-95). */
+typedef struct {
+    int64_t nx, ny, nz;
+} ffdp_dims;
+
+/* SamplerArgs (sampler.hpp:25-37) with DomainBounds (geometry.hpp:74-86) flattened. */
+typedef struct {
+    double A[9];     /* row-major affine, normalized coordinates */
+    double t[3];     /* translation */
+    double S[3];     /* diagonal rescale of the displacement */
+    double x_min[3]; /* normalized coordinates of the first output voxel centre */
+    double x_max[3]; /* ... and of the last */
+} ffdp_sampler_args;
+
+/* SamplerGradWant (sampler.hpp:39-44) as a bit mask. */
+enum {
+    FFDP_WANT_IMAGE = 1,
+    FFDP_WANT_WARP = 2,
+    FFDP_WANT_AFFINE = 4,
+    FFDP_WANT_TRANSLATION = 8
+};
+
+/* ParzenKernel (mi.hpp:28-140). Build with ffdp_parzen_make. */
+typedef enum { FFDP_PARZEN_GAUSSIAN = 0, FFDP_PARZEN_BSPLINE3 = 1, FFDP_PARZEN_DELTA = 2 } ffdp_parzen_kind;
+typedef struct {
+    int32_t kind;
+    int32_t bins;
+    double sigma;  /* gaussian: sigma in intensity units */
+    double radius; /* support half-width in intensity units */
+    double norm;   /* gaussian normaliser */
+} ffdp_parzen;
+
+/*
+ * Moving-image window: planes [z_begin, z_end) of a volume whose full lattice is
+ * `dims` (its own normalized frame spans [-1,1]^3). `data` points at plane z_begin.
+ * Single-GPU callers pass the whole volume (z_begin 0, z_end dims.nz). Sharded callers
+ * pass the resident planes; a sample whose interpolation corner falls inside the
+ * volume but outside the window increments *miss (if given) and reads as zero, so the
+ * caller can widen the window and repeat (exact).
+ */
+typedef struct {
+    const float* data;
+    ffdp_dims dims;
+    int64_t z_begin, z_end;
+} ffdp_image_window;
+
+/*
+ * Z-slab of a lattice that is sharded along z (fabric.hpp:31-70). A buffer described
+ * by a slab holds global planes [buf_z0, buf_z0 + buf_nz) of a lattice with nz_global
+ * planes; compute covers global planes [z_begin, z_end) of it. Single GPU:
+ * {0, nz, 0, nz, nz}.
+ */
+typedef struct {
+    int64_t buf_z0, buf_nz;
+    int64_t z_begin, z_end;
+    int64_t nz_global;
+} ffdp_slab;
+
+FFDP_API const char* ffdp_last_error(void);
+FFDP_API int ffdp_abi_version(void);
+/* Fails with FFDP_CUDA unless an sm_100 device is current. */
+FFDP_API int ffdp_device_check(void);
+
+/* ---------------------------------------------------------------------- sampler */
+
+/*
+ * fused_sample / fused_sample_accumulate (sampler.hpp:254-276):
+ * out[v] (+)= I(A*X_v + t + S*u(X_v)), trilinear, zero padding, no grid materialised.
+ * u may be NULL (identity warp; the output lattice is out_dims). accumulate != 0 adds
+ * into out. abs_contrib (device double, may be NULL) += sum |value| (RingSampleStats).
+ */
+FFDP_API int ffdp_sampler_fwd(ffdp_image_window img, const float* u, ffdp_dims out_dims, const ffdp_sampler_args* args,
+                     float* out, int accumulate, double* abs_contrib, int32_t* miss, void* stream);
+
+/*
+ * fused_sample_backward (sampler.hpp:279-300) / composite_sample_core backward sweep
+ * (sampler.hpp:200-239). want: FFDP_WANT_* mask. g_img (image lattice, zeroed by the
+ * caller, accumulated with atomics), g_u (3 per output voxel, overwritten), gAt
+ * (device double[12] = gA row-major then gt, overwritten; fp64 reduction in a fixed
+ * order, deterministic). Outputs not wanted may be NULL.
+ */
+FFDP_API int ffdp_sampler_bwd(const float* upstream, ffdp_image_window img, const float* u, ffdp_dims out_dims,
+                     const ffdp_sampler_args* args, int want, float* g_img, float* g_u, double* gAt,
+                     int32_t* miss, void* stream);
+
+/* --------------------------------------------------------------------- smoothing */
+
+/*
+ * convolve_axis (smoothing.hpp:52-94): 1-D convolution of a channel-interleaved block
+ * along `axis` (0 x, 1 y, 2 z) with host taps (odd count <= 63). mode 0 = zero_pad,
+ * 1 = renormalize. lo_global/n_global place the block on the global axis so sharded
+ * (halo-padded) blocks match the unsharded result exactly (smoothing.hpp:10-13).
+ */
+FFDP_API int ffdp_convolve_axis(const float* in, float* out, ffdp_dims dims, int channels, int axis, const double* taps,
+                       int ntaps, int mode, int64_t lo_global, int64_t n_global, void* stream);
+
+/* -------------------------------------------------------------------------- LNCC */
+
+/*
+ * lncc_forward_fused (lncc.hpp:144-205) on a z-slab. f, m: buffers described by `slab`
+ * (halo planes included). state: 5 channels x interior voxels, channel-major
+ * (mean_f, mean_m, mean_ff, mean_mm, mean_fm -- LnccState, lncc.hpp:30-35), fp64 so the
+ * cancellation in mean_fm - mean_f*mean_m stays exact-product accurate.
+ * ncc_map (interior voxels, may be NULL). sum_n: device double, += sum of n_i over the
+ * interior (loss = 1 - allreduce(sum_n)/N_total, distops.hpp:309-318).
+ * Moments accumulate in fp64 from exact products.
+ */
+FFDP_API int ffdp_lncc_fwd(const float* f, const float* m, ffdp_dims buf_dims, ffdp_slab slab, int window, double eps,
+                  double* state, float* ncc_map, double* sum_n, void* stream);
+
+/*
+ * First half of lncc_backward_fused (lncc.hpp:359-374): rewrites state in place as the
+ * gamma family (gamma, gamma_AB, gamma_AC, gamma_FM, gamma_MF) with gi = dL/dn_i
+ * (= -upstream/N, lncc.hpp:361; -1/N_total in dist_lncc, distops.hpp:320).
+ */
+FFDP_API int ffdp_lncc_gamma(double* state, int64_t voxels, double eps, double gi, void* stream);
+
+/*
+ * Second half (lncc.hpp:376-406): exact mode (ants == 0) box-filters the gamma family
+ * (gamma buffer described by `slab`, halo planes included) before the combination;
+ * ANTs mode uses it as is. grad_f may be NULL. f, m, grad_f, grad_m cover the interior.
+ */
+FFDP_API int ffdp_lncc_combine(const double* gamma, ffdp_dims buf_dims, ffdp_slab slab, int window, int ants,
+                      const float* f, const float* m, float* grad_f, float* grad_m, void* stream);
+
+/* ---------------------------------------------------------------------------- MI */
+
+/* ParzenKernel::gaussian/bspline3/delta (mi.hpp:33-63) incl. the normalisation check
+ * (mi.hpp:120-133, FFDP_LOGIC on failure). Host-only. */
+FFDP_API int ffdp_parzen_make(int kind, int bins, double sigma_bins, ffdp_parzen* out);
+
+/*
+ * mi_forward_exact (mi.hpp:235-272) / mi_forward_approx (mi.hpp:285-354) histogram
+ * accumulation. raw: device double[B*B + 2B] (raw_joint, raw_marg_i, raw_marg_j),
+ * ACCUMULATED (zero it first). Accumulation is order-independent fixed point
+ * (2^-24 per contribution), so results are deterministic. bad_input (device int32,
+ * may be NULL) is set when an intensity lies outside [0,1] (mi.hpp:170-179).
+ * stats (host uint64[2], may be NULL) += the MiStats counters (mi.hpp:156-159).
+ */
+FFDP_API int ffdp_mi_hist(const float* vi, const float* vj, int64_t n, const ffdp_parzen* kernel, int approx, double* raw,
+                 int32_t* bad_input, uint64_t* stats, void* stream);
+
+/*
+ * finalize_histogram + histogram_mi + the ghat table of mi_backward_impl
+ * (mi.hpp:181-209, 369-390). table (device double[2*B*B + 2B + 4]):
+ *   p_ij[B*B], p_i[B], p_j[B], ghat[B*B], {z, mi, dot, 0}. upstream = dL/dMI.
+ */
+FFDP_API int ffdp_mi_finalize(const double* raw, int bins, double upstream, double* table, void* stream);
+
+/* Per-voxel part of mi_backward_impl (mi.hpp:392-421). grad_i may be NULL. */
+FFDP_API int ffdp_mi_bwd(const float* vi, const float* vj, int64_t n, const ffdp_parzen* kernel, const double* table,
+                float* grad_i, float* grad_j, void* stream);
+
+/* ------------------------------------------------------------- fused step (★) */
+
+/*
+ * The deformable step's hot path (registration.hpp:277-312) for LNCC in ANTs mode, as
+ * ONE pass: Mw = fused_sample(M, u) for the slab + 3 halo planes, the five LNCC
+ * moments, dL/dMw (lncc.hpp:226-280 with ants_approx), and g_u =
+ * fused_sample_backward(dL/dMw) (sampler.hpp:221-230). Nothing but g_u is written.
+ *   f, u: buffers described by `slab` (halo planes of radius window/2 included);
+ *   g_u: interior planes only (3 floats per voxel);
+ *   args: the sampler arguments of the GLOBAL output lattice (buf_dims.nx, buf_dims.ny,
+ *     slab.nz_global); voxels are addressed by global lattice index, which is the
+ *     ring sampler's per-shard rescale (distops.hpp:120-133) folded into one frame;
+ *   gi: dL/dn_i (-1/N_total for the deformable step);
+ *   shift_f, shift_m: intensity shifts for the moment accumulation (any value is exact
+ *     up to rounding; the mid-range of the data is most accurate);
+ *   sum_n: device double, += sum of n_i over the slab interior.
+ */
+FFDP_API int ffdp_step_lncc(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
+                   const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f, float shift_m,
+                   float* g_u, double* sum_n, int32_t* miss, void* stream);
+
+/*
+ * Fused MI step, pass 1 (registration.hpp:278-299 with dist_mi, distops.hpp:355-373):
+ * samples Mw and accumulates the joint Parzen histogram of (f, Mw) into raw
+ * (device double[B*B + 2B]; the marginals are accumulated too). Then allreduce raw
+ * (if sharded), ffdp_mi_finalize(raw, B, -1, table), and pass 2. f, u as for
+ * ffdp_step_lncc (halo planes allowed, not needed); interior planes are processed.
+ */
+FFDP_API int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
+                      const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, int32_t* miss,
+                      void* stream);
+
+/* Pass 2: re-samples Mw, dL/dMw from the ghat table (mi.hpp:392-421), g_u (3N). */
+FFDP_API int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
+                      const ffdp_sampler_args* args, const ffdp_parzen* kernel, const double* table, float* g_u,
+                      int32_t* miss, void* stream);
+
+/* ----------------------------------------------------------------- utilities */
+
+/* Sum of `n` doubles into *out (device), fixed order (deterministic). */
+FFDP_API int ffdp_reduce_sum_f64(const double* in, int64_t n, double* out, void* stream);
+
+/* Min and max of a float array into out[2] (device float), for intensity ranges. */
+FFDP_API int ffdp_minmax(const float* in, int64_t n, float* out, void* stream);
+
+/*
+ * z-extent of the moving planes a sampler pass over `out_dims` needs
+ * (ring-sampler plan, distops.hpp:144-168): out[0] = min, out[1] = max global plane
+ * index of any interpolation corner that lies inside the moving volume (device int64[2];
+ * out[0] > out[1] when none). Reads u once.
+ */
+FFDP_API int ffdp_sampler_z_extent(const float* u, ffdp_dims out_dims, ffdp_dims m_dims, const ffdp_sampler_args* args,
+                          int64_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFDP_H */

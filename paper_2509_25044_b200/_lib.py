@@ -1,0 +1,137 @@
+"""ctypes binding of libffdp.so (the C ABI declared in include/ffdp.h).
+
+The library is built in-tree (``paper_2509_25044_b200/libffdp.so``) by
+``paper_2509_25044_b200.build`` / ``__graft_entry__.build()``. There is no fallback:
+if the library is missing or no sm_100 device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libffdp.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "ffdp.h")
+
+OK, INVALID_ARGUMENT, RUNTIME, LOGIC, CUDA = 0, 1, 2, 3, 4
+WANT_IMAGE, WANT_WARP, WANT_AFFINE, WANT_TRANSLATION = 1, 2, 4, 8
+PARZEN_GAUSSIAN, PARZEN_BSPLINE3, PARZEN_DELTA = 0, 1, 2
+
+
+class FfdpError(RuntimeError):
+    """Base class of errors raised by libffdp."""
+
+
+class InvalidArgument(FfdpError, ValueError):
+    """std::invalid_argument in the reference (shape / argument errors)."""
+
+
+class FabricError(FfdpError):
+    """std::runtime_error in the reference (transport / size mismatch)."""
+
+
+class LogicError(FfdpError):
+    """std::logic_error in the reference (ParzenKernel normalisation, mi.hpp:132)."""
+
+
+class CudaError(FfdpError):
+    """Device failure (no sm_100 device, launch error, out of memory)."""
+
+
+_EXC = {INVALID_ARGUMENT: InvalidArgument, RUNTIME: FabricError, LOGIC: LogicError, CUDA: CudaError}
+
+
+class Dims(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64)]
+
+
+class SamplerArgsC(C.Structure):
+    _fields_ = [("A", C.c_double * 9), ("t", C.c_double * 3), ("S", C.c_double * 3), ("x_min", C.c_double * 3),
+                ("x_max", C.c_double * 3)]
+
+
+class ImageWindow(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("dims", Dims), ("z_begin", C.c_int64), ("z_end", C.c_int64)]
+
+
+class Slab(C.Structure):
+    _fields_ = [("buf_z0", C.c_int64), ("buf_nz", C.c_int64), ("z_begin", C.c_int64), ("z_end", C.c_int64),
+                ("nz_global", C.c_int64)]
+
+
+class ParzenC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("bins", C.c_int32), ("sigma", C.c_double), ("radius", C.c_double),
+                ("norm", C.c_double)]
+
+
+_vp, _dp = C.c_void_p, C.POINTER(C.c_double)
+_SIGS = {
+    "ffdp_last_error": (C.c_char_p, []),
+    "ffdp_abi_version": (C.c_int, []),
+    "ffdp_device_check": (C.c_int, []),
+    "ffdp_sampler_fwd": (C.c_int, [ImageWindow, _vp, Dims, C.POINTER(SamplerArgsC), _vp, C.c_int, _vp, _vp, _vp]),
+    "ffdp_sampler_bwd": (C.c_int, [_vp, ImageWindow, _vp, Dims, C.POINTER(SamplerArgsC), C.c_int, _vp, _vp, _vp, _vp,
+                                   _vp]),
+    "ffdp_convolve_axis": (C.c_int, [_vp, _vp, Dims, C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                     _vp]),
+    "ffdp_lncc_fwd": (C.c_int, [_vp, _vp, Dims, Slab, C.c_int, C.c_double, _vp, _vp, _vp, _vp]),
+    "ffdp_lncc_gamma": (C.c_int, [_vp, C.c_int64, C.c_double, C.c_double, _vp]),
+    "ffdp_lncc_combine": (C.c_int, [_vp, Dims, Slab, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]),
+    "ffdp_parzen_make": (C.c_int, [C.c_int, C.c_int, C.c_double, C.POINTER(ParzenC)]),
+    "ffdp_mi_hist": (C.c_int, [_vp, _vp, C.c_int64, C.POINTER(ParzenC), C.c_int, _vp, _vp,
+                               C.POINTER(C.c_uint64), _vp]),
+    "ffdp_mi_finalize": (C.c_int, [_vp, C.c_int, C.c_double, _vp, _vp]),
+    "ffdp_mi_bwd": (C.c_int, [_vp, _vp, C.c_int64, C.POINTER(ParzenC), _vp, _vp, _vp, _vp]),
+    "ffdp_step_lncc": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.c_int, C.c_double,
+                                 C.c_double, C.c_float, C.c_float, _vp, _vp, _vp, _vp]),
+    "ffdp_step_mi_hist": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
+                                    _vp, _vp, _vp]),
+    "ffdp_step_mi_grad": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
+                                    _vp, _vp, _vp, _vp]),
+    "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
+    "ffdp_minmax": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
+    "ffdp_sampler_z_extent": (C.c_int, [_vp, Dims, Dims, C.POINTER(SamplerArgsC), _vp, _vp]),
+}
+
+
+def header_symbols(path: str = HEADER):
+    """Every entry point declared by include/ffdp.h."""
+    with open(path) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^FFDP_API\s+[\w\s\*]+?\b(ffdp_\w+)\(", text, flags=re.M)))
+
+
+class _Lib:
+    def __init__(self):
+        self._lib = None
+
+    def load(self):
+        if self._lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise CudaError(f"libffdp.so is not built ({LIB_PATH}); run __graft_entry__.build()")
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            self._lib = lib
+        return self._lib
+
+    def __getattr__(self, name):
+        lib = self.load()
+        fn = getattr(lib, name)
+        if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check"):
+            return fn
+
+        def call(*args):
+            rc = fn(*args)
+            if rc != OK:
+                msg = lib.ffdp_last_error().decode(errors="replace")
+                raise _EXC.get(rc, FfdpError)(f"{name}: {msg}")
+            return rc
+
+        return call
+
+
+lib = _Lib()

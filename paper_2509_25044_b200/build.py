@@ -1,0 +1,65 @@
+"""Build recipe for libffdp.so (sm_100a) and the test oracle libraries.
+
+    python -m paper_2509_25044_b200.build          # libffdp.so (+ oracle, + oracle/_ref if possible)
+
+nvcc cross-compiles without a GPU. The .so files are written in-tree so they travel
+with the gpurun snapshot; they are git-ignored.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = ["capi.cu", "sampler.cu", "lncc.cu", "mi.cu", "step_lncc.cu"]
+LIB = os.path.join(HERE, "libffdp.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared"]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> str:
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    deps = srcs + [os.path.join(CSRC, "ffdp_common.cuh"), os.path.join(ROOT, "include", "ffdp.h")]
+    if force or _stale(LIB, deps):
+        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + srcs
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """The parity checker (test infrastructure): C restatement always, reference shim
+    when /root/reference is present (prebuilt copies travel to the GPU box)."""
+    od = os.path.join(ROOT, "oracle")
+    subprocess.run(["make", "-s", "-C", od, "all"], check=True)
+    if os.path.isdir("/root/reference/proj/include"):
+        subprocess.run(["make", "-s", "-C", od, "ref"], check=True)
+
+
+def build_all(verbose: bool = False) -> None:
+    build_lib(verbose=verbose)
+    build_oracle(verbose=verbose)
+
+
+if __name__ == "__main__":
+    build_all(verbose="-v" in sys.argv)
+    print("built", LIB)

@@ -1,0 +1,266 @@
+// ffdp_common.cuh -- shared device/host helpers for the sm_100a kernels of libffdp.
+//
+// Geometry: the composite transform x -> A*X + t + S*u(X) of the reference sampler
+// (sampler.hpp:165-243) is folded on the host, in fp64, into the image's fractional
+// index space:  f_a = K_a + sum_c P[a][c] * i_c + Q_a * u_a   (i = output lattice index).
+// The per-voxel evaluation stays fp64 so that the floor-based cell choice and the
+// 1e-9 face snap (resample.hpp:17-43) agree with the fp64 reference everywhere; the
+// trilinear weights and the gather run in fp32.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ffdp.h"
+
+#define FFDP_FACE_SNAP 1e-9
+
+namespace ffdp {
+
+// Host-folded sampler geometry (kernel parameter, ~300 B).
+struct Geom {
+    double K[3];
+    double P[9];  // row a = image axis, column c = output axis
+    double Q[3];
+    float dscale[3];  // S_a * 0.5 * (N_a - 1): dL/du_a = dscale_a * dfrac_a * g
+    float hn[3];      // 0.5 * (N_a - 1): d(value)/d(xsrc_a) = dfrac_a * hn_a
+    int32_t n[3];     // image lattice (global)
+    int32_t wz0, wz1; // resident image planes [wz0, wz1)
+    const float* img; // points at plane wz0
+    int64_t sy, sz;   // image strides in elements
+    double Xlo[3], Xstep[3];  // output lattice normalized coordinates (for gA)
+    int32_t on[3];            // output lattice (global)
+};
+
+// Result of resolving one source coordinate (resolve_cell, sampler.hpp:100-113).
+struct Cell {
+    int32_t i0[3];
+    float frac[3];
+};
+
+__device__ __forceinline__ void cell_assign(double f, int32_t n, int32_t& i0, float& frac) {
+    // resample.hpp:32-43: floor, then snap fractions within 1e-9 of a face onto it.
+    double fl = floor(f);
+    double a = f - fl;
+    if (a < FFDP_FACE_SNAP) {
+        a = 0.0;
+    } else if (1.0 - a < FFDP_FACE_SNAP) {
+        fl += 1.0;
+        a = 0.0;
+    }
+    // anything beyond the lattice by more than a cell is fully zero padded
+    fl = fmin(fmax(fl, -2.0), (double)n + 1.0);
+    i0 = (int32_t)fl;
+    frac = (float)a;
+}
+
+__device__ __forceinline__ Cell resolve(const Geom& g, int32_t ix, int32_t iy, int32_t iz, float u0, float u1,
+                                        float u2) {
+    Cell c;
+    const double x = ix, y = iy, z = iz;
+    const double f0 = fma(g.Q[0], (double)u0, fma(g.P[2], z, fma(g.P[1], y, fma(g.P[0], x, g.K[0]))));
+    const double f1 = fma(g.Q[1], (double)u1, fma(g.P[5], z, fma(g.P[4], y, fma(g.P[3], x, g.K[1]))));
+    const double f2 = fma(g.Q[2], (double)u2, fma(g.P[8], z, fma(g.P[7], y, fma(g.P[6], x, g.K[2]))));
+    cell_assign(f0, g.n[0], c.i0[0], c.frac[0]);
+    cell_assign(f1, g.n[1], c.i0[1], c.frac[1]);
+    cell_assign(f2, g.n[2], c.i0[2], c.frac[2]);
+    return c;
+}
+
+// The 8 corner values (zero padded); counts window misses.
+struct Corners {
+    float v[8];  // index bx + 2*by + 4*bz
+};
+
+__device__ __forceinline__ Corners gather(const Geom& g, const Cell& c, int& miss) {
+    Corners k;
+    const bool vx0 = c.i0[0] >= 0 && c.i0[0] < g.n[0];
+    const bool vx1 = c.i0[0] + 1 >= 0 && c.i0[0] + 1 < g.n[0];
+    const bool vy0 = c.i0[1] >= 0 && c.i0[1] < g.n[1];
+    const bool vy1 = c.i0[1] + 1 >= 0 && c.i0[1] + 1 < g.n[1];
+#pragma unroll
+    for (int bz = 0; bz < 2; ++bz) {
+        const int32_t iz = c.i0[2] + bz;
+        bool vz = iz >= 0 && iz < g.n[2];
+        if (vz && (iz < g.wz0 || iz >= g.wz1)) {
+            miss = 1;
+            vz = false;
+        }
+        const float* plane = g.img + (int64_t)(iz - g.wz0) * g.sz;
+#pragma unroll
+        for (int by = 0; by < 2; ++by) {
+            const bool vy = by ? vy1 : vy0;
+            const float* row = plane + (int64_t)(c.i0[1] + by) * g.sy + c.i0[0];
+            k.v[4 * bz + 2 * by + 0] = (vz && vy && vx0) ? __ldg(row) : 0.0f;
+            k.v[4 * bz + 2 * by + 1] = (vz && vy && vx1) ? __ldg(row + 1) : 0.0f;
+        }
+    }
+    return k;
+}
+
+// Trilinear value (sample_cell, sampler.hpp:116-134).
+__device__ __forceinline__ float interp(const Corners& k, const Cell& c) {
+    const float ax = c.frac[0], ay = c.frac[1], az = c.frac[2];
+    const float e00 = fmaf(ax, k.v[1] - k.v[0], k.v[0]);
+    const float e10 = fmaf(ax, k.v[3] - k.v[2], k.v[2]);
+    const float e01 = fmaf(ax, k.v[5] - k.v[4], k.v[4]);
+    const float e11 = fmaf(ax, k.v[7] - k.v[6], k.v[6]);
+    const float g0 = fmaf(ay, e10 - e00, e00);
+    const float g1 = fmaf(ay, e11 - e01, e01);
+    return fmaf(az, g1 - g0, g0);
+}
+
+// Value and d(value)/d(fractional index) (sample_cell_dfrac, sampler.hpp:138-161).
+__device__ __forceinline__ float interp_grad(const Corners& k, const Cell& c, float d[3]) {
+    const float ax = c.frac[0], ay = c.frac[1], az = c.frac[2];
+    const float dx00 = k.v[1] - k.v[0], dx10 = k.v[3] - k.v[2];
+    const float dx01 = k.v[5] - k.v[4], dx11 = k.v[7] - k.v[6];
+    const float e00 = fmaf(ax, dx00, k.v[0]);
+    const float e10 = fmaf(ax, dx10, k.v[2]);
+    const float e01 = fmaf(ax, dx01, k.v[4]);
+    const float e11 = fmaf(ax, dx11, k.v[6]);
+    const float dy0 = e10 - e00, dy1 = e11 - e01;
+    const float g0 = fmaf(ay, dy0, e00);
+    const float g1 = fmaf(ay, dy1, e01);
+    const float h0 = fmaf(ay, dx10 - dx00, dx00);
+    const float h1 = fmaf(ay, dx11 - dx01, dx01);
+    d[0] = fmaf(az, h1 - h0, h0);
+    d[1] = fmaf(az, dy1 - dy0, dy0);
+    d[2] = g1 - g0;
+    return fmaf(az, g1 - g0, g0);
+}
+
+// fp64 trilinear value, for losses whose kernels are discontinuous in the sampled value
+// (Gaussian truncation, delta / hard binning): keeps bin decisions equal to fp64.
+__device__ __forceinline__ double interp_f64(const Corners& k, const Cell& c) {
+    const double ax = c.frac[0], ay = c.frac[1], az = c.frac[2];
+    double acc = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double w = ((q & 1) ? ax : 1.0 - ax) * ((q & 2) ? ay : 1.0 - ay) * ((q & 4) ? az : 1.0 - az);
+        acc = fma(w, (double)k.v[q], acc);
+    }
+    return acc;
+}
+
+// ------------------------------------------------------------------ Parzen kernels
+// Up to four bins m_lo..m_lo+3 carry weight for one intensity (mi.hpp:28-140):
+// bspline3 support 4 bins, gaussian 3-4 bins (radius 1.5 bins), delta 1 bin.
+struct ParzenDev {
+    int32_t kind, bins;
+    double sigma, radius, norm;
+    float inv_sigma2_f, norm_f, inv_sigma_f;
+};
+
+struct Bins4 {
+    int32_t m_lo;
+    float k[4];  // kappa(b_m - v)
+    float w[4];  // omega(b_m - v) (only when requested)
+};
+
+__device__ __forceinline__ float bspline3(float t) {
+    const float a = fabsf(t);
+    if (a < 1.0f) return (4.0f - 6.0f * a * a + 3.0f * a * a * a) * (1.0f / 6.0f);
+    if (a < 2.0f) {
+        const float q = 2.0f - a;
+        return q * q * q * (1.0f / 6.0f);
+    }
+    return 0.0f;
+}
+__device__ __forceinline__ float bspline3_deriv(float t) {
+    const float a = fabsf(t);
+    const float s = t < 0.0f ? -1.0f : 1.0f;
+    if (a < 1.0f) return s * (-2.0f * a + 1.5f * a * a);
+    if (a < 2.0f) {
+        const float q = 2.0f - a;
+        return s * (-0.5f * q * q);
+    }
+    return 0.0f;
+}
+
+// v may be supplied in fp64 (exact truncation decisions for discontinuous kernels).
+template <bool WANT_OMEGA>
+__device__ __forceinline__ Bins4 parzen_bins(const ParzenDev& p, double v) {
+    Bins4 r;
+    const int B = p.bins;
+    if (p.kind == FFDP_PARZEN_BSPLINE3) {
+        const double s = v * B - 0.5;
+        const double fl = floor(s);
+        r.m_lo = (int32_t)fl - 1;
+        const float phi = (float)(s - fl);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // x*B for bin m_lo+q: (m_lo + q + 0.5) - v*B = q - 1 - phi
+            const float tq = (float)(q - 1) - phi;
+            const bool ok = (r.m_lo + q) >= 0 && (r.m_lo + q) < B;
+            r.k[q] = ok ? bspline3(tq) : 0.0f;
+            if (WANT_OMEGA) r.w[q] = ok ? -(float)B * bspline3_deriv(tq) : 0.0f;
+        }
+    } else if (p.kind == FFDP_PARZEN_GAUSSIAN) {
+        const double s = v * B - 0.5;
+        r.m_lo = (int32_t)floor(s - 1.5);  // bins with |m - s| <= 1.5 lie in m_lo .. m_lo+3
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int m = r.m_lo + q;
+            const double x = ((double)m + 0.5) / (double)B - v;  // bin_center(m) - v, fp64 (mi.hpp:142-144)
+            const bool ok = m >= 0 && m < B && !(fabs(x) > p.radius);
+            const float xf = (float)x;
+            const float kap = ok ? p.norm_f * expf(-0.5f * xf * xf * p.inv_sigma2_f) : 0.0f;
+            r.k[q] = kap;
+            if (WANT_OMEGA) r.w[q] = xf * p.inv_sigma2_f * kap;
+        }
+    } else {  // delta (mi.hpp:55-63): indicator |x| < radius
+        r.m_lo = (int32_t)floor(v * B);
+        const int m = r.m_lo;
+        const double x = ((double)m + 0.5) / (double)B - v;
+        const bool ok = m >= 0 && m < B && fabs(x) < p.radius;
+        r.k[0] = ok ? 1.0f : 0.0f;
+        r.k[1] = r.k[2] = r.k[3] = 0.0f;
+        if (WANT_OMEGA) r.w[0] = r.w[1] = r.w[2] = r.w[3] = 0.0f;
+    }
+    return r;
+}
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block sum of a double (all threads participate); result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* smem /* NT/32 */) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) smem[w] = v;
+    __syncthreads();
+    double r = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NT / 32; ++i) r += smem[i];
+    return r;
+}
+
+}  // namespace ffdp
+
+// ------------------------------------------------------------------ host helpers
+namespace ffdp {
+
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+Geom make_geom(const ffdp_image_window& img, const ffdp_dims& out_dims, const ffdp_sampler_args& a);
+bool valid_args(const ffdp_sampler_args& a, const char** why);
+ParzenDev make_parzen_dev(const ffdp_parzen& k);
+int num_sms();
+// Stream-ordered scratch (cudaMallocAsync); freed with scratch_free on the same stream.
+void* scratch_alloc(size_t bytes, cudaStream_t s);
+void scratch_free(void* p, cudaStream_t s);
+
+}  // namespace ffdp
+
+#define FFDP_CHECK_CUDA(expr)                                                                         \
+    do {                                                                                              \
+        cudaError_t e_ = (expr);                                                                      \
+        if (e_ != cudaSuccess) return ffdp::set_error(FFDP_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
