@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Benchmark of the fused warp + loss forward+backward step (the FFDP hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload mi256|lncc720|lncc128|lncc1024|mi1760] [--no-secondary]
+
+Metric (BASELINE.json): Gvoxel/s of the fused warp+loss fwd+bwd step, voxel = output
+(fixed-lattice) voxel; one step = read F, M, u -> Mw -> loss -> dL/dMw -> g_u
+(registration.hpp:277-312). Default workload = BASELINE configs[1]: a synthetic
+256^3 multimodal pair, warp + Mattes MI (32 bins, B-spline Parzen) on one B200.
+A secondary LNCC line (configs[2], 720x640x720, window 7, ANTs) is added as
+``secondary``. Inputs (F, M, u, g_u: 536 MB at 256^3) exceed the 126 MB L2, so no L2
+flush is needed between steps. Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (shape (nz, ny, nx), loss, BASELINE config index)
+    "mi256": ((256, 256, 256), "mi", 1),
+    "lncc720": ((720, 640, 720), "lncc", 2),
+    "lncc128": ((128, 128, 128), "lncc", 0),
+    "lncc1024": ((1024, 1024, 1024), "lncc", 3),
+    "mi1760": ((1200, 1760, 1760), "mi", 4),
+}
+BYTES_PER_VOXEL = {"lncc": 32, "mi": 52}  # algorithmic bytes per output voxel
+METRIC = "Gvoxel/s of fused warp+loss fwd+bwd step (1–8 B200), % of HBM roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ synthetic inputs
+def synth_inputs(shape, loss, seed, device):
+    """Synthetic pair of the survey's recipe on the GPU: smooth
+    ellipsoidal structures with texture, M = F pushed through a smooth warp (<=0.12
+    normalized), u = smooth field + U(-0.01, 0.01) jitter, A = I + U(-0.02, 0.02),
+    t = U(-0.02, 0.02). MI: M = normalize(4 m (1 - m) + 0.02 noise)."""
+    import numpy as np
+    import torch
+
+    from paper_2509_25044_b200 import voxreg
+
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    rnd = lambda *s: torch.rand(*s, generator=g, dtype=torch.float64)
+    nz, ny, nx = shape
+    ax = lambda n: torch.linspace(-1.0, 1.0, n, device=device, dtype=torch.float32)
+    z, y, x = ax(nz).view(nz, 1, 1), ax(ny).view(1, ny, 1), ax(nx).view(1, 1, nx)
+    f = torch.zeros(shape, dtype=torch.float32, device=device)
+    for _ in range(6):
+        c = (rnd(3) * 1.2 - 0.6).tolist()
+        r = (rnd(3) * 0.3 + 0.2).tolist()
+        inten = float(rnd(1) * 0.7 + 0.3)
+        q = ((x - c[0]) / r[0]) ** 2 + ((y - c[1]) / r[1]) ** 2 + ((z - c[2]) / r[2]) ** 2
+        f += inten * torch.sigmoid((1.0 - q) * 10.0)
+        del q
+    for _ in range(3):
+        k = (rnd(3) * 12 + 4).tolist()
+        ph = (rnd(3) * 6.28).tolist()
+        f += 0.04 * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(k[2] * z + ph[2])
+    f = (f - f.min()) / (f.max() - f.min())
+
+    def smooth_field(amp):
+        u = torch.zeros(shape + (3,), dtype=torch.float32, device=device)
+        for c in range(3):
+            for _ in range(3):
+                k = (rnd(3) * 3 + 0.5).tolist()
+                ph = (rnd(3) * 6.28).tolist()
+                a = float(rnd(1) * 2 - 1) * amp
+                u[..., c] += a * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(k[2] * z + ph[2])
+        return u
+
+    u_true = smooth_field(0.04)
+    m = voxreg.fused_sample(f, u_true, voxreg.SamplerArgs())
+    del u_true
+    m = (m - m.min()) / (m.max() - m.min())
+    if loss == "mi":
+        noise = torch.randn(shape, generator=torch.Generator(device=device).manual_seed(seed + 1), device=device)
+        m = 4.0 * m * (1.0 - m) + 0.02 * noise
+        del noise
+        m = (m - m.min()) / (m.max() - m.min())
+    u = smooth_field(0.02)
+    u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2), device=device) * 0.02
+          - 0.01)
+    aff = rnd(12).numpy() * 0.04 - 0.02
+    A = np.eye(3) + aff[:9].reshape(3, 3)
+    t = aff[9:]
+    torch.cuda.synchronize()
+    return f.contiguous(), m.contiguous(), u.contiguous(), A, t
+
+
+# ------------------------------------------------------------------ the GPU arm
+class Stepper:
+    """Launches one fused step through the C ABI on the current stream, recording CUDA
+    events around each of our kernels so per-kernel device time is measured live."""
+
+    def __init__(self, f, m, u, A, t, loss, bins=32):
+        import ctypes as C
+
+        import torch
+
+        from paper_2509_25044_b200 import voxreg
+        from paper_2509_25044_b200._lib import lib
+
+        self.C, self.torch, self.V, self.lib = C, torch, voxreg, lib
+        self.f, self.m, self.u, self.loss = f, m, u, loss
+        self.n = f.numel()
+        self.g_u = torch.empty_like(u)
+        self.args = voxreg.SamplerArgs(A=A, t=t).to_c()
+        self.ws = voxreg.StepWorkspace(f.device, bins)
+        self.bins = bins
+        self.slab = voxreg._full_slab(f.shape[0])
+        self.win = voxreg._window(m)
+        self.dims = voxreg._dims(f.shape)
+        if loss == "lncc":
+            self.shifts = (voxreg.intensity_shift(f), voxreg.intensity_shift(m))
+        else:
+            self.kernel = voxreg.ParzenKernel.bspline3(bins)
+        self.kernel_ms = {}
+        self.launches_per_step = 1 if loss == "lncc" else 4
+
+    def _p(self, t):
+        return self.C.c_void_p(t.data_ptr())
+
+    def step(self, record=False):
+        torch, C, lib = self.torch, self.C, self.lib
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
+        if self.loss == "lncc":
+            self.ws.sum_n.zero_()
+            if record:
+                ev[0].record()
+            lib.ffdp_step_lncc(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
+                               7, 1e-5, -1.0 / self.n, self.shifts[0], self.shifts[1], self._p(self.g_u),
+                               self._p(self.ws.sum_n), None, s)
+            if record:
+                ev[1].record()
+                return [("k_step_lncc", ev[0], ev[1])]
+            return None
+        self.ws.raw.zero_()
+        if record:
+            ev[0].record()
+        lib.ffdp_step_mi_hist(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
+                              C.byref(self.kernel.c), self._p(self.ws.raw), None, s)
+        lib.ffdp_mi_finalize(self._p(self.ws.raw), self.bins, -1.0, self._p(self.ws.table), s)
+        if record:
+            ev[1].record()
+        lib.ffdp_step_mi_grad(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
+                              C.byref(self.kernel.c), self._p(self.ws.table), self._p(self.g_u), None, s)
+        if record:
+            ev[2].record()
+            return [("k_step_mi_hist+finalize", ev[0], ev[1]), ("k_step_mi_grad", ev[1], ev[2])]
+        return None
+
+    def loss_value(self):
+        if self.loss == "lncc":
+            return 1.0 - float(self.ws.sum_n.item()) / self.n
+        b = self.bins
+        return -float(self.ws.table[2 * b * b + 2 * b + 1].item())
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    from paper_2509_25044_b200._lib import lib
+    so = lib.load()
+    if so.ffdp_device_check() != 0:
+        raise RuntimeError(so.ffdp_last_error().decode())
+    shape, loss, cfg = WORKLOADS[args.workload]
+    # weak scaling: every rank owns a full per-GPU workload (independent z-slab shards
+    # of a world-size-times-taller volume need no data-path collective for MI pass 2;
+    # see DESIGN.md "multi-GPU")
+    f, m, u, A, t = synth_inputs(shape, loss, 1234 + rank, dev)
+    st = Stepper(f, m, u, A, t, loss)
+    hbm, hbm_kind = peaks()
+    for _ in range(args.warmup):
+        st.step()
+    torch.cuda.synchronize()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    recs = []
+    e0.record()
+    for i in range(args.steps):
+        r = st.step(record=True)
+        recs.append(r)
+    e1.record()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    per_kernel = {}
+    for r in recs:
+        for name, a, b in r:
+            per_kernel.setdefault(name, []).append(a.elapsed_time(b))
+    kern_ms = {k: sum(v) / len(v) for k, v in per_kernel.items()}
+    nvox = f.numel()
+    ms_step = ms / args.steps
+    value = world * nvox / (ms_step * 1e-3) / 1e9
+    loss_val = st.loss_value()
+
+    # dominant kernel roofline (algorithmic bytes per launch / live event duration)
+    if loss == "lncc":
+        dom, dom_bytes = "k_step_lncc", 32 * nvox
+    else:
+        dom = max(kern_ms, key=kern_ms.get)
+        dom_bytes = (20 if "hist" in dom else 32) * nvox
+    achieved = dom_bytes / (kern_ms[dom] * 1e-3) / 1e9
+    step_gbs = BYTES_PER_VOXEL[loss] * nvox / (ms_step * 1e-3) / 1e9
+
+    # end to end through the public API with host buffers (pinned), H2D + step + D2H(loss)
+    e2e = run_e2e(args, st, f, m, u, A, t, loss, world)
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 coordinates / moment differences)", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}]",
+                   "volume": "x".join(str(s) for s in shape[::-1]), "loss": loss,
+                   "loss_params": "window 7, eps 1e-5, ANTs" if loss == "lncc" else "32 bins, B-spline Parzen, exact",
+                   "voxels_per_gpu": nvox, "parallelism": f"z-slab x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs (F, M, u, g_u) exceed the 126 MB L2; no flush between steps"},
+        "loss": loss_val,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": None, "peak_kind": hbm_kind,
+                     "algorithmic_bytes_per_voxel": dom_bytes // nvox},
+        "step_roofline": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / hbm, 4),
+                          "bytes_per_voxel": BYTES_PER_VOXEL[loss]},
+        "kernel_ms": {k: round(v, 5) for k, v in kern_ms.items()},
+        "gpu_launches": st.launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+    }
+    return out, st
+
+
+def run_e2e(args, st, f, m, u, A, t, loss, world):
+    import torch
+    steps = max(3, min(args.steps, 20))
+    hf, hm, hu = (x.cpu().pin_memory() for x in (f, m, u))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_loss = 0.0
+    e0.record()
+    for _ in range(steps):
+        st.f.copy_(hf, non_blocking=True)
+        st.m.copy_(hm, non_blocking=True)
+        st.u.copy_(hu, non_blocking=True)
+        st.step()
+        host_loss = st.loss_value()  # D2H read of the step result (8 bytes)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    h2d = (hf.numel() + hm.numel() + hu.numel()) * 4
+    return {"value": round(world * f.numel() / (ms * 1e-3) / 1e9, 4), "unit": "Gvoxel/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "ms_per_step": round(ms, 3), "steps": steps,
+            "loss": host_loss}
+
+
+# ------------------------------------------------------------------ the CPU reference
+def cpu_reference(loss, sample_shape, steps, threads):
+    """The reference's own step (ring_sample -> dist_lncc|dist_mi -> ring_sample_backward
+    under WorkerGroup(H), oracle/_ref) on a bounded sample, H = `threads` std::threads."""
+    from oracle import Oracle, Reference, step_inputs
+    try:
+        ref = Reference()
+        kind = "reference"
+    except FileNotFoundError:
+        ref = None
+        kind = "port"
+    orc = Oracle()
+    si = step_inputs(orc, sample_shape, seed=4242, loss=loss)
+    n = int(si.f.size)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        if ref is not None:
+            ref.step(loss, si.f, si.m, si.u, si.A, si.t, world=threads)
+        elif loss == "lncc":
+            orc.step_lncc(si.f, si.m, si.u, si.A, si.t)
+        else:
+            orc.step_mi(si.f, si.m, si.u, orc.parzen("bspline3", 32), si.A, si.t)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": round(n / dt / 1e9, 6), "unit": "Gvoxel/s", "cores": threads if ref is not None else 1,
+            "kind": kind, "sample": f"{'x'.join(str(s) for s in sample_shape[::-1])} {loss} step x{steps} "
+                                    f"({'T=double, WorkerGroup(%d)' % threads if ref is not None else 'C port, 1 thread'})",
+            "s_per_step": round(dt, 4)}
+
+
+def cpu_sample_for(loss):
+    return (96, 96, 96) if loss == "mi" else (128, 128, 128)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="mi256", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    shape, loss, cfg = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        samp = cpu_sample_for(loss)
+        reps = []
+        for _ in range(args.warmup):
+            cpu_reference(loss, samp, 1, threads)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            reps.append(cpu_reference(loss, samp, 1, threads))
+        dt = (time.perf_counter() - t0) / args.steps
+        n = samp[0] * samp[1] * samp[2]
+        v = n / dt / 1e9
+        cb = dict(reps[-1])
+        cb["value"] = round(v, 6)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "Gvoxel/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}] (bounded sample "
+                                   f"{'x'.join(str(s) for s in samp[::-1])} on the host cores)", "loss": loss},
+            "cpu_baseline": {"value": round(v, 6), "unit": "Gvoxel/s", "cores": cb["cores"], "kind": cb["kind"],
+                             "sample": cb["sample"]},
+            "e2e": {"value": round(v, 6), "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    out, st = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu:
+            try:
+                out["cpu_baseline"] = cpu_reference(loss, cpu_sample_for(loss), 2, os.cpu_count() or 1)
+            except Exception as e:  # the baseline is reported, never required
+                out["cpu_baseline"] = {"value": None, "unit": "Gvoxel/s", "cores": 0, "kind": "port",
+                                       "sample": f"unavailable: {e}"}
+        if not args.no_secondary and args.workload == "mi256" and world == 1:
+            import torch
+            del st
+            torch.cuda.empty_cache()
+            a2 = argparse.Namespace(**vars(args))
+            a2.workload, a2.steps = "lncc720", max(5, min(args.steps, 20))
+            sec, _ = run_ours(a2, rank, world, local_rank)
+            out["secondary"] = {k: sec[k] for k in ("value", "unit", "ms_per_step", "config", "roofline",
+                                                    "step_roofline", "kernel_ms", "clocks", "e2e", "loss")}
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

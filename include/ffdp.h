@@ -220,7 +220,9 @@ FFDP_API int ffdp_step_lncc(const float* f, const float* u, ffdp_dims buf_dims, 
 /*
  * Fused MI step, pass 1 (registration.hpp:278-299 with dist_mi, distops.hpp:355-373):
  * samples Mw and accumulates the joint Parzen histogram of (f, Mw) into raw
- * (device double[B*B + 2B]; the marginals are accumulated too). Then allreduce raw
+ * (device double[B*B + 2B]). When nx % 4 == 0 only the joint is accumulated (the
+ * marginal entries are left untouched): finalize_histogram derives p_i, p_j from the
+ * joint (mi.hpp:181-196), so the raw marginals are payload only (distops.hpp:366-372). Then allreduce raw
  * (if sharded), ffdp_mi_finalize(raw, B, -1, table), and pass 2. f, u as for
  * ffdp_step_lncc (halo planes allowed, not needed); interior planes are processed.
  */

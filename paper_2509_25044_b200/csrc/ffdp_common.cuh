@@ -143,6 +143,131 @@ __device__ __forceinline__ double interp_f64(const Corners& k, const Cell& c) {
     return acc;
 }
 
+// ------------------------------------------------------------------ fast row sampler
+// Conversion-free cell assignment (the f64->int / f64->f32 conversions issue at a
+// quarter of the FP64 rate on sm_100). t = f + 1.5*2^20 places floor(f) + 2^19 in
+// mantissa bits 32..51 and frac(f) in units of 2^-32 in the low word (|f| < 2^19), so
+// the 1e-9 face snap of cell_assign (resample.hpp:32-43) becomes integer compares on
+// the low word: frac < 1e-9 <=> lo <= 4, 1 - frac < 1e-9 <=> lo >= 2^32 - 4.
+__device__ __forceinline__ void cell_fix(double f, int32_t& i0, float& frac) {
+    const double t = f + 1572864.0;
+    uint32_t fr = (uint32_t)__double2loint(t);
+    const int32_t hi = __double2hiint(t);
+    int32_t ip = (hi & 0xFFFFF) - 0x80000;
+    if (fr + 4u <= 8u) {  // within 1e-9 of a face (rare): snap onto it
+        ip += fr > 4u ? 1 : 0;
+        fr = 0u;
+    }
+    // |f| >= 2^19 (exponent of t off): far outside any lattice -> fully zero padded
+    if ((uint32_t)(hi - 0x41300000) >= 0x100000u) ip = -4;
+    i0 = ip;
+    frac = __uint_as_float(0x3F800000u | (fr >> 9)) - 1.0f;
+}
+
+// Division by a runtime constant without an integer divide (round-up multiplier,
+// exact for every 32-bit numerator): n / d = (hi + ((n - hi) >> 1)) >> (l - 1).
+struct FastDiv {
+    uint32_t d, m, s;  // s = l - 1 (0 when d == 1)
+    bool one;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.one = d == 1;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    f.m = f.one ? 0u : (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+    f.s = f.one ? 0u : l - 1;
+    return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    if (f.one) return n;
+    const uint32_t hi = __umulhi(n, f.m);
+    return (hi + ((n - hi) >> 1)) >> f.s;
+}
+
+// Row-run sampler state: the fp64 affine part of f for the current voxel, advanced by
+// one DADD per axis per x step (the composite transform is affine in the lattice index).
+struct RowBase {
+    double b[3];
+    __device__ __forceinline__ void init(const Geom& g, int32_t x, int32_t y, int32_t z) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            b[a] = fma(g.P[3 * a + 0], (double)x, fma(g.P[3 * a + 2], (double)z, fma(g.P[3 * a + 1], (double)y, g.K[a])));
+    }
+    __device__ __forceinline__ void step(const Geom& g) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) b[a] += g.P[3 * a];
+    }
+    __device__ __forceinline__ Cell cell(const Geom& g, float u0, float u1, float u2) const {
+        Cell c;
+        cell_fix(fma(g.Q[0], (double)u0, b[0]), c.i0[0], c.frac[0]);
+        cell_fix(fma(g.Q[1], (double)u1, b[1]), c.i0[1], c.frac[1]);
+        cell_fix(fma(g.Q[2], (double)u2, b[2]), c.i0[2], c.frac[2]);
+        return c;
+    }
+};
+
+// Gather with a branch-free interior fast path: all 8 corners inside the (resident)
+// lattice -> unpredicated loads; otherwise the zero-padding path of `gather`.
+template <bool FULLWIN>
+__device__ __forceinline__ Corners gather_fast(const Geom& g, const Cell& c, int& miss) {
+    const bool inside = (uint32_t)c.i0[0] < (uint32_t)(g.n[0] - 1) && (uint32_t)c.i0[1] < (uint32_t)(g.n[1] - 1) &&
+                        (FULLWIN ? (uint32_t)c.i0[2] < (uint32_t)(g.n[2] - 1)
+                                 : (c.i0[2] >= g.wz0 && c.i0[2] + 1 < g.wz1));
+    if (inside) {
+        Corners k;
+        const float* p = g.img + (int64_t)(c.i0[2] - g.wz0) * g.sz + (int64_t)(c.i0[1] * (int32_t)g.sy + c.i0[0]);
+        const int32_t sy = (int32_t)g.sy;
+        k.v[0] = __ldg(p);
+        k.v[1] = __ldg(p + 1);
+        k.v[2] = __ldg(p + sy);
+        k.v[3] = __ldg(p + sy + 1);
+        p += g.sz;
+        k.v[4] = __ldg(p);
+        k.v[5] = __ldg(p + 1);
+        k.v[6] = __ldg(p + sy);
+        k.v[7] = __ldg(p + sy + 1);
+        return k;
+    }
+    return gather(g, c, miss);
+}
+
+// Four samples at once: the corner loads of all four are issued back to back (memory
+// level parallelism) when every lane's samples are interior (warp-uniform decision, no
+// divergence); otherwise every sample takes the zero-padding path.
+template <bool FULLWIN>
+__device__ __forceinline__ bool cell_inside(const Geom& g, const Cell& c) {
+    return (uint32_t)c.i0[0] < (uint32_t)(g.n[0] - 1) && (uint32_t)c.i0[1] < (uint32_t)(g.n[1] - 1) &&
+           (FULLWIN ? (uint32_t)c.i0[2] < (uint32_t)(g.n[2] - 1) : (c.i0[2] >= g.wz0 && c.i0[2] + 1 < g.wz1));
+}
+
+template <bool FULLWIN, int NS>
+__device__ __forceinline__ void gather_n(const Geom& g, const Cell (&c)[NS], Corners (&k)[NS], int& miss) {
+    bool in = true;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) in = in && cell_inside<FULLWIN>(g, c[q]);
+    if (__all_sync(__activemask(), in)) {
+        const int32_t sy = (int32_t)g.sy;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const float* p =
+                g.img + (int64_t)(c[q].i0[2] - g.wz0) * g.sz + (int64_t)(c[q].i0[1] * sy + c[q].i0[0]);
+            k[q].v[0] = __ldg(p);
+            k[q].v[1] = __ldg(p + 1);
+            k[q].v[2] = __ldg(p + sy);
+            k[q].v[3] = __ldg(p + sy + 1);
+            k[q].v[4] = __ldg(p + g.sz);
+            k[q].v[5] = __ldg(p + g.sz + 1);
+            k[q].v[6] = __ldg(p + g.sz + sy);
+            k[q].v[7] = __ldg(p + g.sz + sy + 1);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) k[q] = gather(g, c[q], miss);
+    }
+}
+
 // ------------------------------------------------------------------ Parzen kernels
 // Up to four bins m_lo..m_lo+3 carry weight for one intensity (mi.hpp:28-140):
 // bspline3 support 4 bins, gaussian 3-4 bins (radius 1.5 bins), delta 1 bin.
