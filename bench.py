@@ -149,8 +149,12 @@ def synth_inputs(shape, loss, seed, device):
         del noise
         m = (m - m.min()) / (m.max() - m.min())
     u = smooth_field(0.02)
-    u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2), device=device) * 0.02
-          - 0.01)
+    # sub-voxel jitter (+-0.02 voxel) keeps samples off cell faces; a registration warp is
+    # smooth (it is Gaussian-smoothed every iteration, registration.hpp:316), so the
+    # parity tests' U(-0.01, 0.01)-normalized jitter (+-1.3 voxels at 256^3) would be an
+    # unrealistically rough field for a throughput benchmark
+    jit = torch.tensor([0.04 / (nx - 1), 0.04 / (ny - 1), 0.04 / (nz - 1)], device=device)
+    u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2), device=device) - 0.5) * jit
     aff = rnd(12).numpy() * 0.04 - 0.02
     A = np.eye(3) + aff[:9].reshape(3, 3)
     t = aff[9:]
@@ -179,7 +183,8 @@ class Stepper:
         self.ws = voxreg.StepWorkspace(f.device, bins)
         self.bins = bins
         self.slab = voxreg._full_slab(f.shape[0])
-        self.win = voxreg._window(m)
+        self.mimg = voxreg.MovingImage(m)  # zero-bordered layout, made once per scale
+        self.win = self.mimg.window()
         self.dims = voxreg._dims(f.shape)
         if loss == "lncc":
             self.shifts = (voxreg.intensity_shift(f), voxreg.intensity_shift(m))
@@ -327,7 +332,7 @@ def run_e2e(args, st, f, m, u, A, t, loss, world):
     e0.record()
     for _ in range(steps):
         st.f.copy_(hf, non_blocking=True)
-        st.m.copy_(hm, non_blocking=True)
+        st.mimg.interior.copy_(hm, non_blocking=True)  # H2D straight into the bordered layout
         st.u.copy_(hu, non_blocking=True)
         st.step()
         host_loss = st.loss_value()  # D2H read of the step result (8 bytes)

@@ -77,16 +77,22 @@ typedef struct {
 
 /*
  * Moving-image window: planes [z_begin, z_end) of a volume whose full lattice is
- * `dims` (its own normalized frame spans [-1,1]^3). `data` points at plane z_begin.
- * Single-GPU callers pass the whole volume (z_begin 0, z_end dims.nz). Sharded callers
- * pass the resident planes; a sample whose interpolation corner falls inside the
- * volume but outside the window increments *miss (if given) and reads as zero, so the
- * caller can widen the window and repeat (exact).
+ * `dims` (its own normalized frame spans [-1,1]^3). Single-GPU callers pass the whole
+ * volume (z_begin 0, z_end dims.nz). Sharded callers pass the resident planes; a sample
+ * whose interpolation corner falls inside the volume but outside the window increments
+ * *miss (if given) and reads as zero, so the caller can widen the window and repeat
+ * (exact).
+ * pad = 0: `data` points at plane z_begin of a dense nx*ny*(z_end-z_begin) block.
+ * pad = 2: `data` points at a zero-bordered block of (nx+4)*(ny+4)*(z_end-z_begin+4)
+ *   floats (ffdp_pad_window), voxel (x,y,z) at ((z-z_begin+2)*(ny+4) + y+2)*(nx+4) + x+2.
+ *   The fused step kernels then gather all eight corners without bounds checks: the
+ *   border holds the reference's zero padding (sampler.hpp:106-110).
  */
 typedef struct {
     const float* data;
     ffdp_dims dims;
     int64_t z_begin, z_end;
+    int64_t pad;
 } ffdp_image_window;
 
 /*
@@ -239,6 +245,12 @@ FFDP_API int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims buf_dim
 
 /* Sum of `n` doubles into *out (device), fixed order (deterministic). */
 FFDP_API int ffdp_reduce_sum_f64(const double* in, int64_t n, double* out, void* stream);
+
+/* Copies planes [z_begin, z_end) of a dense volume (src points at plane z_begin) into
+ * the zero-bordered pad = 2 layout of ffdp_image_window (dst sized
+ * (nx+4)*(ny+4)*(z_end-z_begin+4), border written as zero). */
+FFDP_API int ffdp_pad_window(const float* src, ffdp_dims dims, int64_t z_begin, int64_t z_end, float* dst,
+                             void* stream);
 
 /* Min and max of a float array into out[2] (device float), for intensity ranges. */
 FFDP_API int ffdp_minmax(const float* in, int64_t n, float* out, void* stream);

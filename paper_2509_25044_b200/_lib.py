@@ -11,7 +11,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libffdp.so")
+LIB_PATH = os.environ.get("FFDP_LIB") or os.path.join(HERE, "libffdp.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ffdp.h")
 
 OK, INVALID_ARGUMENT, RUNTIME, LOGIC, CUDA = 0, 1, 2, 3, 4
@@ -52,7 +52,8 @@ class SamplerArgsC(C.Structure):
 
 
 class ImageWindow(C.Structure):
-    _fields_ = [("data", C.c_void_p), ("dims", Dims), ("z_begin", C.c_int64), ("z_end", C.c_int64)]
+    _fields_ = [("data", C.c_void_p), ("dims", Dims), ("z_begin", C.c_int64), ("z_end", C.c_int64),
+                ("pad", C.c_int64)]
 
 
 class Slab(C.Structure):
@@ -91,6 +92,7 @@ _SIGS = {
                                     _vp, _vp, _vp, _vp]),
     "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_minmax": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
+    "ffdp_pad_window": (C.c_int, [_vp, Dims, C.c_int64, C.c_int64, _vp, _vp]),
     "ffdp_sampler_z_extent": (C.c_int, [_vp, Dims, Dims, C.POINTER(SamplerArgsC), _vp, _vp]),
 }
 

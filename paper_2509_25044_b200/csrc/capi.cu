@@ -72,9 +72,16 @@ Geom make_geom(const ffdp_image_window& img, const ffdp_dims& out, const ffdp_sa
     }
     g.wz0 = (int32_t)img.z_begin;
     g.wz1 = (int32_t)img.z_end;
-    g.img = img.data;
-    g.sy = img.dims.nx;
-    g.sz = img.dims.nx * img.dims.ny;
+    g.pad = (int32_t)img.pad;
+    if (img.pad == 2) {
+        g.sy = img.dims.nx + 4;
+        g.sz = (img.dims.nx + 4) * (img.dims.ny + 4);
+        g.img = img.data ? img.data + 2 * g.sz + 2 * g.sy + 2 : nullptr;
+    } else {
+        g.sy = img.dims.nx;
+        g.sz = img.dims.nx * img.dims.ny;
+        g.img = img.data;
+    }
     return g;
 }
 
@@ -198,6 +205,15 @@ __global__ void __launch_bounds__(NT) k_z_extent(Geom g, const float* u, int64_t
     }
 }
 
+__global__ void k_pad_window(const float* __restrict__ src, int64_t nx, int64_t ny, int64_t nzw,
+                             float* __restrict__ dst) {
+    const int64_t px = nx + 4, py = ny + 4, n = px * py * (nzw + 4);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = i % px - 2, y = (i / px) % py - 2, z = i / (px * py) - 2;
+        dst[i] = (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nzw) ? src[(z * ny + y) * nx + x] : 0.0f;
+    }
+}
+
 __global__ void k_init_extent(int64_t* out) {
     out[0] = INT64_MAX;
     out[1] = INT64_MIN;
@@ -249,7 +265,7 @@ int ffdp_sampler_z_extent(const float* u, ffdp_dims out_dims, ffdp_dims m_dims, 
     const char* why = nullptr;
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!out) return set_error(FFDP_INVALID_ARGUMENT, "z_extent: null output");
-    ffdp_image_window w{nullptr, m_dims, 0, m_dims.nz};
+    ffdp_image_window w{nullptr, m_dims, 0, m_dims.nz, 0};
     const Geom g = make_geom(w, out_dims, *args);
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = out_dims.nx * out_dims.ny * out_dims.nz;
@@ -257,6 +273,15 @@ int ffdp_sampler_z_extent(const float* u, ffdp_dims out_dims, ffdp_dims m_dims, 
     const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(8 * num_sms(), (n + 255) / 256));
     k_z_extent<256><<<nb, 256, 0, s>>>(g, u, n, out);
     return check_launch("z_extent");
+}
+
+int ffdp_pad_window(const float* src, ffdp_dims d, int64_t z_begin, int64_t z_end, float* dst, void* stream) {
+    if (!src || !dst || d.nx < 1 || d.ny < 1 || z_begin < 0 || z_end > d.nz || z_begin >= z_end)
+        return set_error(FFDP_INVALID_ARGUMENT, "pad_window: bad arguments");
+    const int64_t n = (d.nx + 4) * (d.ny + 4) * (z_end - z_begin + 4);
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, 16LL * num_sms());
+    k_pad_window<<<nb, 256, 0, (cudaStream_t)stream>>>(src, d.nx, d.ny, z_end - z_begin, dst);
+    return check_launch("pad_window");
 }
 
 int ffdp_parzen_make(int kind, int bins, double sigma_bins, ffdp_parzen* k) {

@@ -26,8 +26,9 @@ struct Geom {
     float hn[3];      // 0.5 * (N_a - 1): d(value)/d(xsrc_a) = dfrac_a * hn_a
     int32_t n[3];     // image lattice (global)
     int32_t wz0, wz1; // resident image planes [wz0, wz1)
-    const float* img; // points at plane wz0
-    int64_t sy, sz;   // image strides in elements
+    const float* img; // points at voxel (0, 0, wz0) (inside the border when padded)
+    int64_t sy, sz;   // image strides in elements (of the padded layout when padded)
+    int32_t pad;      // 0 or 2 (zero-bordered layout, ffdp_pad_window)
     double Xlo[3], Xstep[3];  // output lattice normalized coordinates (for gA)
     int32_t on[3];            // output lattice (global)
 };
@@ -199,6 +200,10 @@ struct RowBase {
 #pragma unroll
         for (int a = 0; a < 3; ++a) b[a] += g.P[3 * a];
     }
+    __device__ __forceinline__ void step_y(const Geom& g) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) b[a] += g.P[3 * a + 1];
+    }
     __device__ __forceinline__ Cell cell(const Geom& g, float u0, float u1, float u2) const {
         Cell c;
         cell_fix(fma(g.Q[0], (double)u0, b[0]), c.i0[0], c.frac[0]);
@@ -266,6 +271,38 @@ __device__ __forceinline__ void gather_n(const Geom& g, const Cell (&c)[NS], Cor
 #pragma unroll
         for (int q = 0; q < NS; ++q) k[q] = gather(g, c[q], miss);
     }
+}
+
+// Zero-bordered moving image (pad = 2): clamp each cell index into [-2, n] (a cell at
+// -2 or n reads two border zeros, like the reference's fully zero-padded samples) and
+// load the 8 corners unconditionally. With a z window, corners on non-resident planes
+// inside the volume are window misses (they read the zero border).
+template <bool FULLWIN>
+__device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int& miss) {
+    const int32_t ix = min(max(c.i0[0], -2), g.n[0]);
+    const int32_t iy = min(max(c.i0[1], -2), g.n[1]);
+    int32_t iz;
+    if (FULLWIN) {
+        iz = min(max(c.i0[2], -2), g.n[2]);
+    } else {
+        const int32_t z0 = c.i0[2];
+        const bool in0 = z0 >= 0 && z0 < g.n[2], in1 = z0 + 1 >= 0 && z0 + 1 < g.n[2];
+        if ((in0 && (z0 < g.wz0 || z0 >= g.wz1)) || (in1 && (z0 + 1 < g.wz0 || z0 + 1 >= g.wz1))) miss = 1;
+        iz = min(max(z0, g.wz0 - 2), g.wz1);
+    }
+    const int32_t sy = (int32_t)g.sy;
+    const float* p = g.img + (int64_t)(iz - g.wz0) * g.sz + (int64_t)(iy * sy + ix);
+    Corners k;
+    k.v[0] = __ldg(p);
+    k.v[1] = __ldg(p + 1);
+    k.v[2] = __ldg(p + sy);
+    k.v[3] = __ldg(p + sy + 1);
+    p += g.sz;
+    k.v[4] = __ldg(p);
+    k.v[5] = __ldg(p + 1);
+    k.v[6] = __ldg(p + sy);
+    k.v[7] = __ldg(p + sy + 1);
+    return k;
 }
 
 // ------------------------------------------------------------------ Parzen kernels

@@ -445,7 +445,8 @@ static SlabIdx make_slab_idx(const ffdp_dims& d, const ffdp_slab& s) {
     return r;
 }
 
-bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_parzen& k);
+bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
+                          const ffdp_parzen& k);
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, int32_t* miss, cudaStream_t st);
 int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
@@ -518,7 +519,7 @@ int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims d, ffdp_slab s, 
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!f || !u || !raw || !m.data) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    if (mi_quad_path_applies(d, s, *kernel)) return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, miss, st);
+    if (mi_quad_path_applies(d, s, m, *kernel)) return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, miss, st);
     const int B = kernel->bins;
     const int nh = B * B + 2 * B;
     const ffdp_dims out{d.nx, d.ny, s.nz_global};
@@ -548,7 +549,7 @@ int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims d, ffdp_slab s, 
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!f || !u || !table || !g_u || !m.data) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    if (mi_quad_path_applies(d, s, *kernel))
+    if (mi_quad_path_applies(d, s, m, *kernel))
         return mi_quad_grad(f, u, d, s, m, *args, *kernel, table, g_u, miss, st);
     const int B = kernel->bins;
     const ffdp_dims out{d.nx, d.ny, s.nz_global};

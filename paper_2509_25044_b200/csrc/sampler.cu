@@ -155,6 +155,7 @@ static int check_window(const ffdp_image_window& img) {
     if (!img.data) return set_error(FFDP_INVALID_ARGUMENT, "sampler: null image");
     if (img.dims.nx < 1 || img.dims.ny < 1 || img.dims.nz < 1)
         return set_error(FFDP_INVALID_ARGUMENT, "Volume3: dims must be positive");
+    if (img.pad != 0 && img.pad != 2) return set_error(FFDP_INVALID_ARGUMENT, "sampler: pad must be 0 or 2");
     if (img.z_begin < 0 || img.z_end > img.dims.nz || img.z_begin >= img.z_end)
         return set_error(FFDP_INVALID_ARGUMENT, "sampler: bad image window [%lld,%lld) of %lld planes",
                          (long long)img.z_begin, (long long)img.z_end, (long long)img.dims.nz);

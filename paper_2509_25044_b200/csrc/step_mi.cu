@@ -8,8 +8,8 @@
 //   pass 2  Mw and dMw/du again, dL/dMw = sum_m kappa_i sum_n ghat omega_j
 //           (mi.hpp:392-421), g_u = S dxsrc dL/dMw -- reads F, u, M, writes g_u: 32 B.
 //
-// Work unit: a quad of 4 consecutive x voxels of one row (float4 loads of F and u,
-// float4 stores of g_u; needs nx % 4 == 0, other lattices use mi.cu's scalar path).
+// Work unit: a warp covers 32 consecutive x voxels of 4 consecutive rows (needs the
+// zero-bordered moving image, ffdp_pad_window; dense images use mi.cu's scalar path).
 // Histogram: 16 joint products per voxel rounded to fixed point by one FFMA against
 // the 1.5*2^23 magic constant and added with native shared u32 atomics; every 1024
 // voxels the CTA folds the u32 counters into a u64 shared copy (no overflow), and at
@@ -23,8 +23,7 @@
 namespace ffdp {
 namespace mstep {
 
-constexpr int NT = 256;
-constexpr int CHUNK_QUADS = NT;  // one quad per thread per chunk -> 1024 voxels per fold
+constexpr int NT = 256;  // 8 warps x 128 voxels -> 1024 voxels per histogram fold
 
 struct Params {
     Geom g;
@@ -35,10 +34,10 @@ struct Params {
     const double* table;
     unsigned long long* hist;  // global u64 [B*B]
     int32_t* miss;
-    int32_t nx, ny, qpr;       // quads per row
-    FastDiv div_qpr, div_ny;
+    int32_t nx, ny, nxb, nyq;  // lattice, 32-wide x blocks, 4-row groups
+    FastDiv div_nxb, div_nyq;
     int64_t plane, z_begin, buf_z0;
-    int64_t nquads;
+    int64_t nunits;
     float fix_scale;           // 2^23 (bspline) / 2^22 (gaussian) / 2^21 (delta)
 };
 
@@ -88,14 +87,28 @@ __device__ __forceinline__ BS4 generic_bins(const ParzenDev& p, double v) {
     return r;
 }
 
-__device__ __forceinline__ void quad_coords(const Params& P, int64_t q, int32_t& x0, int32_t& y, int32_t& z,
-                                            int64_t& bi) {
-    const uint32_t row = fdiv((uint32_t)q, P.div_qpr);
-    x0 = ((int32_t)q - (int32_t)row * P.qpr) * 4;
-    const uint32_t zz = fdiv(row, P.div_ny);
-    y = (int32_t)row - (int32_t)zz * P.ny;
-    z = (int32_t)zz + (int32_t)P.z_begin;
-    bi = ((int64_t)zz + P.z_begin - P.buf_z0) * P.plane + (int64_t)(y * P.nx + x0);
+// Work unit of a warp: 32 consecutive x voxels (lane = x offset) of 4 consecutive rows.
+// Consecutive lanes sample neighbouring source positions, so each corner load of the
+// warp touches one or two 128-B lines (coalesced gather); a thread's 4 voxels are
+// y-neighbours, so their Parzen footprints usually share bins (histogram aggregation).
+struct Unit {
+    int32_t x, y0, z;   // lattice coordinates (z global)
+    int64_t bi;         // buffer index of (x, y0, z)
+    bool vx;            // x inside the lattice
+};
+
+__device__ __forceinline__ Unit unit_coords(const Params& P, uint32_t unit, int lane) {
+    Unit w;
+    const uint32_t r1 = fdiv(unit, P.div_nxb);
+    const int32_t xb = (int32_t)(unit - r1 * P.nxb);
+    const uint32_t zz = fdiv(r1, P.div_nyq);
+    const int32_t yq = (int32_t)(r1 - zz * P.nyq);
+    w.x = xb * 32 + lane;
+    w.y0 = yq * 4;
+    w.z = (int32_t)zz + (int32_t)P.z_begin;
+    w.vx = w.x < P.nx;
+    w.bi = ((int64_t)zz + P.z_begin - P.buf_z0) * P.plane + (int64_t)w.y0 * P.nx + (w.vx ? w.x : 0);
+    return w;
 }
 
 // Padded bin tables: bin m lives at row m + PAD of a (B + 2 PAD)^2 table, so the
@@ -104,24 +117,25 @@ __device__ __forceinline__ void quad_coords(const Params& P, int64_t q, int32_t&
 // back (histogram) or hold zeros (ghat).
 constexpr int PAD = 2;
 
-__device__ __forceinline__ void load_quad(const Params& P, int64_t bi, float (&ff)[4], float (&uu)[12]) {
-    const float4 fv = __ldg(reinterpret_cast<const float4*>(P.f + bi));
-    const float4 ua = __ldg(reinterpret_cast<const float4*>(P.u + 3 * bi));
-    const float4 ub = __ldg(reinterpret_cast<const float4*>(P.u + 3 * bi + 4));
-    const float4 uc = __ldg(reinterpret_cast<const float4*>(P.u + 3 * bi + 8));
-    ff[0] = fv.x; ff[1] = fv.y; ff[2] = fv.z; ff[3] = fv.w;
-    uu[0] = ua.x; uu[1] = ua.y; uu[2] = ua.z; uu[3] = ua.w;
-    uu[4] = ub.x; uu[5] = ub.y; uu[6] = ub.z; uu[7] = ub.w;
-    uu[8] = uc.x; uu[9] = uc.y; uu[10] = uc.z; uu[11] = uc.w;
-}
-
-__device__ __forceinline__ void quad_cells(const Params& P, int32_t x0, int32_t y, int32_t z, const float (&uu)[12],
-                                           Cell (&c)[4]) {
-    RowBase rb;
-    rb.init(P.g, x0, y, z);
+__device__ __forceinline__ void load_unit(const Params& P, const Unit& w, float (&ff)[4], float (&uu)[12],
+                                          bool (&ok)[4]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        if (k) rb.step(P.g);
+        ok[k] = w.vx && (w.y0 + k) < P.ny;
+        const int64_t i = w.bi + (int64_t)k * P.nx;
+        ff[k] = ok[k] ? __ldg(P.f + i) : 0.0f;
+        uu[3 * k] = ok[k] ? __ldg(P.u + 3 * i) : 0.0f;
+        uu[3 * k + 1] = ok[k] ? __ldg(P.u + 3 * i + 1) : 0.0f;
+        uu[3 * k + 2] = ok[k] ? __ldg(P.u + 3 * i + 2) : 0.0f;
+    }
+}
+
+__device__ __forceinline__ void unit_cells(const Params& P, const Unit& w, const float (&uu)[12], Cell (&c)[4]) {
+    RowBase rb;
+    rb.init(P.g, w.x, w.y0, w.z);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k) rb.step_y(P.g);
         c[k] = rb.cell(P.g, uu[3 * k], uu[3 * k + 1], uu[3 * k + 2]);
     }
 }
@@ -141,41 +155,78 @@ __global__ void __launch_bounds__(NT) k_step_mi_hist(const Params P) {
     }
     __syncthreads();
     int miss = 0;
-    const int64_t stride = (int64_t)gridDim.x * CHUNK_QUADS;
-    for (int64_t base = (int64_t)blockIdx.x * CHUNK_QUADS; base < P.nquads; base += stride) {
-        const int64_t q = base + threadIdx.x;
-        if (q < P.nquads) {
-            int32_t x0, y, z;
-            int64_t bi;
-            quad_coords(P, q, x0, y, z, bi);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t stride = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t base = (int64_t)blockIdx.x * (NT / 32); base < P.nunits; base += stride) {
+        const int64_t unit = base + warp;
+        if (unit < P.nunits) {
+            const Unit w = unit_coords(P, (uint32_t)unit, lane);
             float ff[4], uu[12];
-            load_quad(P, bi, ff, uu);
+            bool ok[4];
+            load_unit(P, w, ff, uu, ok);
             Cell c[4];
-            quad_cells(P, x0, y, z, uu, c);
+            unit_cells(P, w, uu, c);
             Corners cr[4];
-            gather_n<FULLWIN, 4>(P.g, c, cr, miss);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
+            BS4 bI[4], bJ[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                BS4 bi_, bj_;
                 if (BSPLINE) {
-                    bi_ = bspline_bins<false>(ff[k], B);
-                    bj_ = bspline_bins<false>(interp(cr[k], c[k]), B);
+                    bI[k] = bspline_bins<false>(ff[k], B);
+                    bJ[k] = bspline_bins<false>(interp(cr[k], c[k]), B);
                 } else {
-                    bi_ = generic_bins<false>(P.p, (double)ff[k]);
-                    bj_ = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
+                    bI[k] = generic_bins<false>(P.p, (double)ff[k]);
+                    bJ[k] = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
                 }
-                float kj[4];
+                const float sc = ok[k] ? P.fix_scale : 0.0f;  // voxels outside the lattice add nothing
 #pragma unroll
-                for (int b = 0; b < 4; ++b) kj[b] = bj_.k[b] * P.fix_scale;
-                uint32_t* h = s32 + (bi_.m_lo + PAD) * LD + (bj_.m_lo + PAD);
+                for (int b = 0; b < 4; ++b) bJ[k].k[b] *= sc;
+            }
+            const int mlo = min(min(bI[0].m_lo, bI[1].m_lo), min(bI[2].m_lo, bI[3].m_lo));
+            const int mhi = max(max(bI[0].m_lo, bI[1].m_lo), max(bI[2].m_lo, bI[3].m_lo));
+            const int nlo = min(min(bJ[0].m_lo, bJ[1].m_lo), min(bJ[2].m_lo, bJ[3].m_lo));
+            const int nhi = max(max(bJ[0].m_lo, bJ[1].m_lo), max(bJ[2].m_lo, bJ[3].m_lo));
+            if (mhi - mlo <= 1 && nhi - nlo <= 1) {
+                // the four footprints fit one 5 x 5 window: aggregate in registers, then 25
+                // atomics instead of 64 (neighbouring voxels share bins)
+                float wv[25];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
+                for (int i = 0; i < 25; ++i) wv[i] = 0.0f;
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        // round-to-nearest fixed point without a conversion instruction
-                        atomicAdd(h + a * LD + b,
-                                  (uint32_t)(__float_as_int(fmaf(bi_.k[a], kj[b], 12582912.0f)) - 0x4B400000));
-                    }
+                for (int k = 0; k < 4; ++k) {
+                    const bool dm = bI[k].m_lo != mlo, dn = bJ[k].m_lo != nlo;
+                    const float a5[5] = {dm ? 0.0f : bI[k].k[0], dm ? bI[k].k[0] : bI[k].k[1],
+                                         dm ? bI[k].k[1] : bI[k].k[2], dm ? bI[k].k[2] : bI[k].k[3],
+                                         dm ? bI[k].k[3] : 0.0f};
+                    const float b5[5] = {dn ? 0.0f : bJ[k].k[0], dn ? bJ[k].k[0] : bJ[k].k[1],
+                                         dn ? bJ[k].k[1] : bJ[k].k[2], dn ? bJ[k].k[2] : bJ[k].k[3],
+                                         dn ? bJ[k].k[3] : 0.0f};
+#pragma unroll
+                    for (int r = 0; r < 5; ++r)
+#pragma unroll
+                        for (int cc = 0; cc < 5; ++cc) wv[5 * r + cc] = fmaf(a5[r], b5[cc], wv[5 * r + cc]);
+                }
+                uint32_t* h = s32 + (mlo + PAD) * LD + (nlo + PAD);
+#pragma unroll
+                for (int r = 0; r < 5; ++r)
+#pragma unroll
+                    for (int cc = 0; cc < 5; ++cc)
+                        // round-to-nearest through the fp64 magic constant (sums of 4 voxels exceed
+                        // the fp32 magic range); no conversion-pipe instruction
+                        atomicAdd(h + r * LD + cc,
+                                  (uint32_t)__double2loint((double)wv[5 * r + cc] + 6755399441055744.0));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t* h = s32 + (bI[k].m_lo + PAD) * LD + (bJ[k].m_lo + PAD);
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            // one voxel stays below 2^22 at the chosen scale: fp32 magic rounding
+                            atomicAdd(h + a * LD + b, (uint32_t)(__float_as_int(fmaf(bI[k].k[a], bJ[k].k[b],
+                                                                                     12582912.0f)) - 0x4B400000));
                 }
             }
         }
@@ -209,18 +260,18 @@ __global__ void __launch_bounds__(NT, 3) k_step_mi_grad(const Params P) {
         __syncthreads();
     }
     int miss = 0;
-    const int64_t stride = (int64_t)gridDim.x * NT;
-    for (int64_t q = (int64_t)blockIdx.x * NT + threadIdx.x; q < P.nquads; q += stride) {
-        int32_t x0, y, z;
-        int64_t bi;
-        quad_coords(P, q, x0, y, z, bi);
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t unit = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); unit < P.nunits; unit += stride) {
+        const Unit w = unit_coords(P, (uint32_t)unit, lane);
         float ff[4], uu[12];
-        load_quad(P, bi, ff, uu);
+        bool ok[4];
+        load_unit(P, w, ff, uu, ok);
         Cell c[4];
-        quad_cells(P, x0, y, z, uu, c);
+        unit_cells(P, w, uu, c);
         Corners cr[4];
-        gather_n<FULLWIN, 4>(P.g, c, cr, miss);
-        float go[12];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             float d[3];
@@ -244,14 +295,13 @@ __global__ void __launch_bounds__(NT, 3) k_step_mi_grad(const Params P) {
                 acc = fmaf(gr[a * LD + 3], bj_.w[3], acc);
                 gj = fmaf(bi_.k[a], acc, gj);
             }
-            go[3 * k] = P.g.dscale[0] * d[0] * gj;
-            go[3 * k + 1] = P.g.dscale[1] * d[1] * gj;
-            go[3 * k + 2] = P.g.dscale[2] * d[2] * gj;
+            if (ok[k]) {
+                float* o = P.g_u + 3 * (w.bi + (int64_t)k * P.nx - (P.z_begin - P.buf_z0) * P.plane);
+                o[0] = P.g.dscale[0] * d[0] * gj;
+                o[1] = P.g.dscale[1] * d[1] * gj;
+                o[2] = P.g.dscale[2] * d[2] * gj;
+            }
         }
-        float4* out = reinterpret_cast<float4*>(P.g_u + 3 * ((bi - (P.z_begin - P.buf_z0) * P.plane)));
-        out[0] = make_float4(go[0], go[1], go[2], go[3]);
-        out[1] = make_float4(go[4], go[5], go[6], go[7]);
-        out[2] = make_float4(go[8], go[9], go[10], go[11]);
     }
     const unsigned anym = __ballot_sync(0xffffffffu, miss);
     if (anym && P.miss && (threadIdx.x & 31) == 0) atomicAdd(P.miss, __popc(anym));
@@ -266,10 +316,11 @@ __global__ void k_hist_to_raw(const unsigned long long* h, int n, double inv_sca
 
 // Returns FFDP_OK and launches, or a non-zero code when the quad path does not apply
 // (the caller then uses the scalar kernels of mi.cu).
-bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_parzen& k) {
-    // 32-bit quad indices and in-plane offsets
-    return d.nx % 4 == 0 && k.bins <= 64 && (int64_t)d.nx * d.ny < (1LL << 31) &&
-           (d.nx / 4) * d.ny * (s.z_end - s.z_begin) < (1LL << 31);
+bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
+                          const ffdp_parzen& k) {
+    // zero-bordered moving image, 32-bit unit indices and in-plane offsets
+    return m.pad == 2 && k.bins <= 64 && (int64_t)d.nx * d.ny < (1LL << 31) &&
+           ((d.nx + 31) / 32) * ((d.ny + 3) / 4) * (s.z_end - s.z_begin) < (1LL << 31);
 }
 
 static mstep::Params make_params(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s,
@@ -286,13 +337,14 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
     P.miss = nullptr;
     P.nx = (int32_t)d.nx;
     P.ny = (int32_t)d.ny;
-    P.qpr = (int32_t)(d.nx / 4);
-    P.div_qpr = make_fastdiv((uint32_t)P.qpr);
-    P.div_ny = make_fastdiv((uint32_t)d.ny);
+    P.nxb = (int32_t)((d.nx + 31) / 32);
+    P.nyq = (int32_t)((d.ny + 3) / 4);
+    P.div_nxb = make_fastdiv((uint32_t)P.nxb);
+    P.div_nyq = make_fastdiv((uint32_t)P.nyq);
     P.plane = d.nx * d.ny;
     P.z_begin = s.z_begin;
     P.buf_z0 = s.buf_z0;
-    P.nquads = (int64_t)P.qpr * d.ny * (s.z_end - s.z_begin);
+    P.nunits = (int64_t)P.nxb * P.nyq * (s.z_end - s.z_begin);
     P.fix_scale = k.kind == FFDP_PARZEN_BSPLINE3 ? 8388608.0f : k.kind == FFDP_PARZEN_GAUSSIAN ? 4194304.0f
                                                                                                  : 2097152.0f;
     return P;
@@ -309,7 +361,7 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     P.hist = h;
     P.miss = miss;
     const size_t smem = (sizeof(unsigned long long) + sizeof(uint32_t)) * (B + 2 * PAD) * (B + 2 * PAD);
-    const int64_t chunks = (P.nquads + CHUNK_QUADS - 1) / CHUNK_QUADS;
+    const int64_t chunks = (P.nunits + NT / 32 - 1) / (NT / 32);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, 6LL * num_sms()));
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool bs = k.kind == FFDP_PARZEN_BSPLINE3;
@@ -336,7 +388,8 @@ int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     P.miss = miss;
     const int B = k.bins;
     const size_t smem = sizeof(float) * (B + 2 * PAD) * (B + 2 * PAD);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.nquads + NT - 1) / NT, 6LL * num_sms()));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((P.nunits + NT / 32 - 1) / (NT / 32),
+                                                                 6LL * num_sms()));
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool bs = k.kind == FFDP_PARZEN_BSPLINE3;
     if (bs && full)

@@ -64,7 +64,30 @@ def _dims(shape) -> Dims:
 
 def _window(img: torch.Tensor) -> ImageWindow:
     nz = img.shape[0]
-    return ImageWindow(img.data_ptr(), _dims(img.shape), 0, nz)
+    return ImageWindow(img.data_ptr(), _dims(img.shape), 0, nz, 0)
+
+
+class MovingImage:
+    """A moving image in the zero-bordered layout (2 voxels of zeros on every side) that
+    the fused step kernels gather from without bounds checks (ffdp_pad_window). The
+    border realises the reference's zero padding (sampler.hpp:106-110). The moving image
+    is static within a scale (registration.hpp:249,270), so the padded copy is made once
+    per scale and reused by every iteration."""
+
+    def __init__(self, m: torch.Tensor):
+        m = _vol(m, "MovingImage")
+        self.shape = tuple(m.shape)
+        nz, ny, nx = self.shape
+        self.padded = torch.empty((nz + 4, ny + 4, nx + 4), dtype=torch.float32, device=m.device)
+        lib.ffdp_pad_window(_ptr(m), _dims(m.shape), 0, nz, _ptr(self.padded), _stream())
+
+    @property
+    def interior(self) -> torch.Tensor:
+        """View of the volume inside the border (copy new data into it in place)."""
+        return self.padded[2:-2, 2:-2, 2:-2]
+
+    def window(self) -> ImageWindow:
+        return ImageWindow(self.padded.data_ptr(), _dims(self.shape), 0, self.shape[0], 2)
 
 
 def _full_slab(nz: int) -> Slab:
@@ -495,7 +518,8 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
     distops.hpp:320) or upstream -1 on MI (distops.hpp:392). F and M share a lattice
     (the driver extracts both with F's ShardSpec, registration.hpp:268-270)."""
     params = params or LossParams()
-    f, m = _vol(f, "warp_loss_step"), _vol(m, "warp_loss_step")
+    f = _vol(f, "warp_loss_step")
+    mi = m if isinstance(m, MovingImage) else MovingImage(m)
     u = _warp(u, "warp_loss_step")
     if tuple(u.shape[:3]) != tuple(f.shape):
         raise InvalidArgument("sampler: warp lattice mismatch")
@@ -508,14 +532,16 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
     n = f.numel()
     nz = f.shape[0]
     slab = _full_slab(nz)
-    win = _window(m)
+    if mi.shape != tuple(f.shape):
+        raise InvalidArgument("warp_loss_step: F and M must share a lattice (registration.hpp:268-270)")
+    win = mi.window()
     ws.miss.zero_()
     if params.kind == "lncc":
         if not params.ants_approx:
             raise InvalidArgument("warp_loss_step: the fused LNCC step implements the ANTs backward "
                                   "(use lncc_forward_fused / lncc_backward_fused for exact mode)")
         if shifts is None:
-            shifts = (intensity_shift(f), intensity_shift(m))
+            shifts = (intensity_shift(f), intensity_shift(mi.interior.contiguous()))
         ws.sum_n.zero_()
         lib.ffdp_step_lncc(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), params.window, params.epsilon,
                            -1.0 / n, shifts[0], shifts[1], _ptr(g_u), _ptr(ws.sum_n), _ptr(ws.miss), _stream())
