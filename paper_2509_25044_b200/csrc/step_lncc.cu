@@ -8,15 +8,18 @@
 // 32 algorithmic bytes per output voxel.
 //
 // CTA = TX x TY output columns marching along z. Per plane p:
-//   S1  sample Mw (and F) on the (TX+6) x (TY+6) haloed plane into shared memory
-//       (shifted by the intensity mid-range); the thread that owns an output column
-//       also keeps F, Mw and dL/du-per-dL/dMw of its own voxel in a 4-plane register
-//       ring (the voxel's moments are complete 3 planes later);
-//   S2  x box sums of the five moment channels (runs of 4, sliding, fp32);
-//   S3  y box sums -> P(p) (fp32), z box by sliding Z += P(p) - P(p-7) in fp64 (exact:
-//       P(p-7) is the identical fp32 value, kept in a 7-plane shared ring); then the
-//       voxel of plane p-3 is finished: A, B, C in fp64 (cancellation), gamma family,
-//       dL/dMw, g_u = S * dxsrc * dL/dMw (sampler.hpp:221-230).
+//   S1  sample Mw (and F) on the (TX+6) x (TY+6) haloed plane into an 8-plane shared
+//       ring of shifted (F, Mw) pairs; F and u of the next plane are already in flight
+//       (register prefetch); the owner of an output column keeps S*dMw/df of its voxel
+//       in a 4-plane register ring (its moments complete 3 planes later);
+//   S2  x box sums of the five moment-channel DIFFERENCES v(p) - v(p-7) (runs of 4,
+//       sliding, fp32), read from ring slots p and p-7;
+//   S3  y box sums of the differences, Z += box in fp64 -- Z is the 7x7x7 window sum of
+//       every channel by telescoping, with no ring of per-plane sums; then the voxel of
+//       plane p-3 is finished: A, B, C from Z in fp64 (the cancellation-prone part),
+//       gamma family, dL/dMw, g_u = S * dxsrc * dL/dMw (sampler.hpp:221-230).
+// Intensities are shifted by their mid-range before the moments (exact up to rounding;
+// the zero-padded border is corrected with the in-volume window weight W).
 #include <algorithm>
 
 #include "ffdp_common.cuh"
@@ -27,15 +30,15 @@ namespace lstep {
 constexpr int R = 3, WIN = 7;
 constexpr int TX = 64, TY = 8, NT = 256;
 constexpr int HX = TX + 2 * R, HY = TY + 2 * R;  // 70 x 14
-constexpr int HXP = 72;                          // raw row pitch
+constexpr int HXP = 72;                          // ring row pitch (float2)
 constexpr int NOUT = TX * TY;                    // 512 outputs per plane, 2 per thread
 constexpr int NHALO = HX * HY - NOUT;            // 468
 constexpr int XJOBS = HY * (TX / 4);             // 224 x-pass runs of 4
+constexpr int NSLOT = 8;                         // planes p-7 .. p
 
 struct Smem {
-    float raw[2][HY][HXP];   // shifted F, Mw of the current plane
-    float X[5][HY][TX];      // x box sums
-    float P[WIN][5][NOUT];   // 7-plane ring of xy box sums
+    float2 raw[NSLOT][HY][HXP];  // shifted (F, Mw), zero outside the volume
+    float X[5][HY][TX];          // x box sums of the channel differences
 };
 
 struct Params {
@@ -72,131 +75,140 @@ __device__ __forceinline__ float win_count(int64_t g, int64_t n) {
     return (float)(hi - lo + 1);
 }
 
-struct Own {
-    float fp, mp, gu0, gu1, gu2;  // shifted F, shifted Mw, dscale * dfrac
+// Exact int -> double without the (quarter-rate) conversion pipe.
+__device__ __forceinline__ double i2d(int32_t i) {
+    return __hiloint2double(0x43300000, (int32_t)((uint32_t)i ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+// Cell of the sample at lattice (x, y, plane of kz): the fp64 affine part plus Q u, then
+// the conversion-free cell assignment (ffdp_common.cuh cell_fix).
+__device__ __forceinline__ Cell cell_at(const Geom& g, const double (&kz)[3], int x, int y, float u0, float u1,
+                                        float u2) {
+    const double xd = i2d(x), yd = i2d(y);
+    Cell c;
+    cell_fix(fma(g.Q[0], (double)u0, fma(g.P[0], xd, fma(g.P[1], yd, kz[0]))), c.i0[0], c.frac[0]);
+    cell_fix(fma(g.Q[1], (double)u1, fma(g.P[3], xd, fma(g.P[4], yd, kz[1]))), c.i0[1], c.frac[1]);
+    cell_fix(fma(g.Q[2], (double)u2, fma(g.P[6], xd, fma(g.P[7], yd, kz[2]))), c.i0[2], c.frac[2]);
+    return c;
+}
+
+// The thread's four sample positions (2 owned outputs, up to 2 halo positions); their
+// (x, y) is fixed for the whole z march.
+struct Pos {
+    int gx[4], gy[4];   // lattice coordinates
+    int hx[4], hy[4];   // haloed tile coordinates
+    bool inxy[4];       // inside the lattice in x, y (and a valid slot)
 };
 
-template <int SLOT>
-__device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Own (&ring)[4][2], double (&Z)[2][5],
-                                           double& nsum, int& miss, int64_t p, int64_t pstart, int64_t pend,
-                                           int x0, int y0, int64_t zc0) {
+struct Pref {
+    float f[4], u[4][3];
+};
+
+__device__ __forceinline__ void prefetch(const Params& P, const Pos& ps, int64_t p, Pref& pf) {
+    const bool plane_in = p >= 0 && p < P.nz_global;
+    const int64_t zoff = (p - P.buf_z0) * P.plane;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool ok = plane_in && ps.inxy[k];
+        const int64_t bi = zoff + (int64_t)ps.gy[k] * P.nx + ps.gx[k];
+        pf.f[k] = ok ? __ldg(P.f + bi) : 0.0f;
+        pf.u[k][0] = ok ? __ldg(P.u + 3 * bi) : 0.0f;
+        pf.u[k][1] = ok ? __ldg(P.u + 3 * bi + 1) : 0.0f;
+        pf.u[k][2] = ok ? __ldg(P.u + 3 * bi + 2) : 0.0f;
+    }
+}
+
+template <int SLOT, bool FULLWIN>
+__device__ __forceinline__ void plane_step(const Params& P, Smem& sm, const Pos& ps, Pref& pf, float (&gur)[4][2][3],
+                                           double (&Z)[2][5], double& nsum, int& miss, int64_t p, int64_t pstart,
+                                           int64_t pend, int x0, int y0, int64_t zc0) {
     if (p >= pend) return;  // uniform across the CTA
     const int t = threadIdx.x;
     const bool plane_in = p >= 0 && p < P.nz_global;
-    const int64_t zoff = (p - P.buf_z0) * P.plane;
+    const int slot = (int)((p - pstart) & (NSLOT - 1));
+    const int slot_old = (slot + 1) & (NSLOT - 1);  // plane p-7
 
     // ---- S1: sampling ------------------------------------------------------------
+    Pref cur = pf;
+    if (p + 1 < pend) prefetch(P, ps, p + 1, pf);  // next plane's F, u in flight during this plane
+    const double zd = i2d((int32_t)p);
+    double kz[3];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int o = t + NT * j;
-        const int ox = o & (TX - 1), oy = o / TX;
-        const int gx = x0 + ox, gy = y0 + oy;
-        Own w{0.f, 0.f, 0.f, 0.f, 0.f};
-        if (plane_in && gx < P.nx && gy < P.ny) {
-            const int64_t bi = zoff + (int64_t)gy * P.nx + gx;
-            const float fv = __ldg(P.f + bi);
-            const float u0 = __ldg(P.u + 3 * bi), u1 = __ldg(P.u + 3 * bi + 1), u2 = __ldg(P.u + 3 * bi + 2);
-            const Cell c = resolve(P.g, gx, gy, (int32_t)p, u0, u1, u2);
-            const Corners k = gather(P.g, c, miss);
+    for (int a = 0; a < 3; ++a) kz[a] = fma(P.g.P[3 * a + 2], zd, P.g.K[a]);
+    Cell c[4];
+    Corners cr[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = cell_at(P.g, kz, ps.gx[k], ps.gy[k], cur.u[k][0], cur.u[k][1], cur.u[k][2]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool ok = plane_in && ps.inxy[k];
+        float2 v = make_float2(0.f, 0.f);
+        if (k < 2) {
             float d[3];
-            const float mw = interp_grad(k, c, d);
-            w.fp = fv - P.sf;
-            w.mp = mw - P.sm;
-            w.gu0 = P.g.dscale[0] * d[0];
-            w.gu1 = P.g.dscale[1] * d[1];
-            w.gu2 = P.g.dscale[2] * d[2];
-        }
-        sm.raw[0][oy + R][ox + R] = w.fp;
-        sm.raw[1][oy + R][ox + R] = w.mp;
-        ring[SLOT][j] = w;
-    }
+            const float mw = interp_grad(cr[k], c[k], d);
+            if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int h = t + NT * j;
-        if (h < NHALO) {
-            int hx, hy;
-            halo_pos(h, hx, hy);
-            const int gx = x0 + hx - R, gy = y0 + hy - R;
-            float fp = 0.f, mp = 0.f;
-            if (plane_in && gx >= 0 && gx < P.nx && gy >= 0 && gy < P.ny) {
-                const int64_t bi = zoff + (int64_t)gy * P.nx + gx;
-                const float fv = __ldg(P.f + bi);
-                const float u0 = __ldg(P.u + 3 * bi), u1 = __ldg(P.u + 3 * bi + 1), u2 = __ldg(P.u + 3 * bi + 2);
-                const Cell c = resolve(P.g, gx, gy, (int32_t)p, u0, u1, u2);
-                const Corners k = gather(P.g, c, miss);
-                fp = fv - P.sf;
-                mp = interp(k, c) - P.sm;
-            }
-            sm.raw[0][hy][hx] = fp;
-            sm.raw[1][hy][hx] = mp;
+            for (int a = 0; a < 3; ++a) gur[SLOT][k][a] = ok ? P.g.dscale[a] * d[a] : 0.0f;
+        } else {
+            const float mw = interp(cr[k], c[k]);
+            if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
         }
+        if (k < 2 || t + NT * (k - 2) < NHALO) sm.raw[slot][ps.hy[k]][ps.hx[k]] = v;
     }
     __syncthreads();
 
-    // ---- S2: x box sums, runs of 4 -------------------------------------------------
+    // ---- S2: x box sums of v(p) - v(p-7), runs of 4 --------------------------------
     if (t < XJOBS) {
         const int r = t >> 4, xs = (t & 15) * 4;
-        float F[10], M[10];
+        float dv[5][10];
 #pragma unroll
         for (int k = 0; k < 10; ++k) {
-            F[k] = sm.raw[0][r][xs + k];
-            M[k] = sm.raw[1][r][xs + k];
-        }
-        float s[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int k = 0; k < WIN; ++k) {
-            s[0] += F[k];
-            s[1] += M[k];
-            s[2] = fmaf(F[k], F[k], s[2]);
-            s[3] = fmaf(M[k], M[k], s[3]);
-            s[4] = fmaf(F[k], M[k], s[4]);
-        }
-        float o[5][4];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) o[c][0] = s[c];
-#pragma unroll
-        for (int i = 1; i < 4; ++i) {
-            const float fa = F[i + 6], ma = M[i + 6], fr = F[i - 1], mr = M[i - 1];
-            s[0] += fa - fr;
-            s[1] += ma - mr;
-            s[2] += fmaf(fa, fa, -fr * fr);
-            s[3] += fmaf(ma, ma, -mr * mr);
-            s[4] += fmaf(fa, ma, -fr * mr);
-#pragma unroll
-            for (int c = 0; c < 5; ++c) o[c][i] = s[c];
+            const float2 n = sm.raw[slot][r][xs + k], o = sm.raw[slot_old][r][xs + k];
+            dv[0][k] = n.x - o.x;
+            dv[1][k] = n.y - o.y;
+            dv[2][k] = fmaf(n.x, n.x, -o.x * o.x);
+            dv[3][k] = fmaf(n.y, n.y, -o.y * o.y);
+            dv[4][k] = fmaf(n.x, n.y, -o.x * o.y);
         }
 #pragma unroll
-        for (int c = 0; c < 5; ++c)
-            *reinterpret_cast<float4*>(&sm.X[c][r][xs]) = make_float4(o[c][0], o[c][1], o[c][2], o[c][3]);
+        for (int ch = 0; ch < 5; ++ch) {
+            float s = dv[ch][0] + dv[ch][1] + dv[ch][2] + dv[ch][3] + dv[ch][4] + dv[ch][5] + dv[ch][6];
+            float o0 = s;
+            s += dv[ch][7] - dv[ch][0];
+            const float o1 = s;
+            s += dv[ch][8] - dv[ch][1];
+            const float o2 = s;
+            s += dv[ch][9] - dv[ch][2];
+            *reinterpret_cast<float4*>(&sm.X[ch][r][xs]) = make_float4(o0, o1, o2, s);
+        }
     }
     __syncthreads();
 
-    // ---- S3: y box sums, z slide, finish plane p-3 ---------------------------------
-    const int slot = (int)((p - pstart) % WIN);
+    // ---- S3: y box sums, Z += box, finish plane p-3 --------------------------------
     const bool emit = p >= zc0 + R;
     const int64_t q = p - R;
+    const int slot_q = (slot + NSLOT - R) & (NSLOT - 1);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int o = t + NT * j;
         const int ox = o & (TX - 1), oy = o / TX;
 #pragma unroll
-        for (int c = 0; c < 5; ++c) {
+        for (int ch = 0; ch < 5; ++ch) {
             float s = 0.f;
 #pragma unroll
-            for (int k = 0; k < WIN; ++k) s += sm.X[c][oy + k][ox];
-            const float old = sm.P[slot][c][o];
-            sm.P[slot][c][o] = s;
-            Z[j][c] += (double)s - (double)old;
+            for (int k = 0; k < WIN; ++k) s += sm.X[ch][oy + k][ox];
+            Z[j][ch] += (double)s;
         }
         const int gx = x0 + ox, gy = y0 + oy;
         if (emit && gx < P.nx && gy < P.ny) {
-            const Own w = ring[(SLOT + 1) & 3][j];
+            const float2 fm = sm.raw[slot_q][oy + R][ox + R];
             const float cw = win_count(gx, P.nx) * win_count(gy, P.ny) * win_count(q, P.nz_global);
             const double inv = 1.0 / (double)(WIN * WIN * WIN);
             const double W = (double)cw * inv;
             const double Sf = Z[j][0], Sm = Z[j][1];
-            // window sums of the shifted channels; moments scaled by 343^2 (exact
-            // power-free fold), cancellation-prone differences in fp64
+            // moments scaled by 343^2; the cancellation-prone differences in fp64
             const double N = WIN * WIN * WIN;
             double A = N * Z[j][4] - Sf * Sm;
             double Bv = N * Z[j][2] - Sf * Sf;
@@ -216,17 +228,19 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Own (&ring
             const float rab = a * b * invD;
             const float mf = (float)(Sf * inv), mm = (float)(Sm * inv);
             const float omwf = (float)(1.0 - W);
-            const float df = (w.fp - mf) + P.sf * omwf;  // F - mean_F
-            const float dm = (w.mp - mm) + P.sm * omwf;  // Mw - mean_M
+            const float df = (fm.x - mf) + P.sf * omwf;    // F - mean_F
+            const float dm = (fm.y - mm) + P.sm * omwf;    // Mw - mean_M
             const float gmw = gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:404, ANTs)
+            const int sq = (SLOT + 1) & 3;                 // gu of plane p-3
             const int64_t ov = 3 * ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx);
-            P.g_u[ov] = w.gu0 * gmw;
-            P.g_u[ov + 1] = w.gu1 * gmw;
-            P.g_u[ov + 2] = w.gu2 * gmw;
+            P.g_u[ov] = gur[sq][j][0] * gmw;
+            P.g_u[ov + 1] = gur[sq][j][1] * gmw;
+            P.g_u[ov + 2] = gur[sq][j][2] * gmw;
         }
     }
 }
 
+template <bool FULLWIN>
 __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -234,22 +248,45 @@ __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
     const int64_t zc0 = P.z_begin + (int64_t)blockIdx.z * P.zchunk;
     const int64_t zc1 = min(P.z_end, zc0 + P.zchunk);
     if (zc0 >= zc1) return;
-    for (int i = threadIdx.x; i < WIN * 5 * NOUT; i += NT) (&sm.P[0][0][0])[i] = 0.f;
-    __syncthreads();
-    Own ring[4][2];
+    for (int i = threadIdx.x; i < NSLOT * HY * HXP; i += NT) (&sm.raw[0][0][0])[i] = make_float2(0.f, 0.f);
+    const int t = threadIdx.x;
+    Pos ps;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int hx, hy;
+        bool slot_ok = true;
+        if (k < 2) {
+            const int o = t + NT * k;
+            hx = (o & (TX - 1)) + R;
+            hy = o / TX + R;
+        } else {
+            const int h = t + NT * (k - 2);
+            slot_ok = h < NHALO;
+            halo_pos(slot_ok ? h : 0, hx, hy);
+        }
+        ps.hx[k] = hx;
+        ps.hy[k] = hy;
+        ps.gx[k] = x0 + hx - R;
+        ps.gy[k] = y0 + hy - R;
+        ps.inxy[k] = slot_ok && ps.gx[k] >= 0 && ps.gx[k] < P.nx && ps.gy[k] >= 0 && ps.gy[k] < P.ny;
+    }
+    float gur[4][2][3];
     double Z[2][5];
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int c = 0; c < 5; ++c) Z[j][c] = 0.0;
+        for (int ch = 0; ch < 5; ++ch) Z[j][ch] = 0.0;
     double nsum = 0.0;
     int miss = 0;
     const int64_t pstart = zc0 - R, pend = zc1 + R;
+    Pref pf;
+    prefetch(P, ps, pstart, pf);
+    __syncthreads();
     for (int64_t p = pstart; p < pend; p += 4) {
-        plane_step<0>(P, sm, ring, Z, nsum, miss, p, pstart, pend, x0, y0, zc0);
-        plane_step<1>(P, sm, ring, Z, nsum, miss, p + 1, pstart, pend, x0, y0, zc0);
-        plane_step<2>(P, sm, ring, Z, nsum, miss, p + 2, pstart, pend, x0, y0, zc0);
-        plane_step<3>(P, sm, ring, Z, nsum, miss, p + 3, pstart, pend, x0, y0, zc0);
+        plane_step<0, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p, pstart, pend, x0, y0, zc0);
+        plane_step<1, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p + 1, pstart, pend, x0, y0, zc0);
+        plane_step<2, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p + 2, pstart, pend, x0, y0, zc0);
+        plane_step<3, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p + 3, pstart, pend, x0, y0, zc0);
     }
     // loss partial and window misses
     nsum = warp_sum(nsum);
@@ -281,6 +318,9 @@ extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_
         return set_error(FFDP_INVALID_ARGUMENT, "halo_exchange: buffer lacks the %d halo planes the window needs", R);
     if (m.z_begin < 0 || m.z_end > m.dims.nz || m.z_begin >= m.z_end)
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: bad moving window");
+    if (m.pad != 2)
+        return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: the moving image must be zero-bordered (pad = 2, "
+                                                "ffdp_pad_window)");
     if (d.nx >= (1 << 30) || d.ny >= (1 << 30) || s.nz_global >= (1 << 30))
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: lattice too large");
     Params P;
@@ -313,10 +353,14 @@ extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_
     if (ty > 65535 || chunks > 65535) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: grid too large");
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_step_lncc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        cudaFuncSetAttribute(k_step_lncc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+        cudaFuncSetAttribute(k_step_lncc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
         attr_set = true;
     }
     const dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)chunks);
-    k_step_lncc<<<grid, NT, sizeof(Smem), (cudaStream_t)stream>>>(P);
+    if (m.z_begin == 0 && m.z_end == m.dims.nz)
+        k_step_lncc<true><<<grid, NT, sizeof(Smem), (cudaStream_t)stream>>>(P);
+    else
+        k_step_lncc<false><<<grid, NT, sizeof(Smem), (cudaStream_t)stream>>>(P);
     return check_launch("step_lncc");
 }
