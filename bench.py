@@ -191,12 +191,15 @@ class Stepper:
         else:
             self.kernel = voxreg.ParzenKernel.bspline3(bins)
         self.kernel_ms = {}
-        self.launches_per_step = 1 if loss == "lncc" else 4
+        self.launches_per_step = 1 if loss == "lncc" else 4  # lncc: step; mi: hist, to_raw, finalize, grad
 
     def _p(self, t):
         return self.C.c_void_p(t.data_ptr())
 
     def step(self, record=False):
+        """One step on the current stream. record=True brackets each of our kernels with
+        CUDA events (per-kernel device time, live); record=False is launch-only and is
+        what the CUDA graph captures."""
         torch, C, lib = self.torch, self.C, self.lib
         s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
@@ -211,20 +214,37 @@ class Stepper:
                 ev[1].record()
                 return [("k_step_lncc", ev[0], ev[1])]
             return None
+        if not record:
+            lib.ffdp_step_mi(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
+                             C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.table), self._p(self.g_u),
+                             self._p(self.ws.scratch), None, s)
+            return None
         self.ws.raw.zero_()
-        if record:
-            ev[0].record()
+        ev[0].record()
         lib.ffdp_step_mi_hist(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
-                              C.byref(self.kernel.c), self._p(self.ws.raw), None, s)
+                              C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.scratch), None, s)
         lib.ffdp_mi_finalize(self._p(self.ws.raw), self.bins, -1.0, self._p(self.ws.table), s)
-        if record:
-            ev[1].record()
+        ev[1].record()
         lib.ffdp_step_mi_grad(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
                               C.byref(self.kernel.c), self._p(self.ws.table), self._p(self.g_u), None, s)
-        if record:
-            ev[2].record()
-            return [("k_step_mi_hist+finalize", ev[0], ev[1]), ("k_step_mi_grad", ev[1], ev[2])]
-        return None
+        ev[2].record()
+        return [("k_step_mi_hist+finalize", ev[0], ev[1]), ("k_step_mi_grad", ev[1], ev[2])]
+
+    def capture(self):
+        """CUDA graph of one launch-only step: the timed loop replays it, so host launch
+        overhead never gates the device."""
+        torch = self.torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.step()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        torch.cuda.synchronize()
+        return g
 
     def loss_value(self):
         if self.loss == "lncc":
@@ -262,11 +282,13 @@ def run_ours(args, rank, world, local_rank):
     time.sleep(0.3)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    recs = []
+    graph = st.capture()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
     e0.record()
     for i in range(args.steps):
-        r = st.step(record=True)
-        recs.append(r)
+        graph.replay()
     e1.record()
     torch.cuda.synchronize()
     if dist is not None:
@@ -277,6 +299,9 @@ def run_ours(args, rank, world, local_rank):
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
+    # per-kernel device time: the same K steps launched with events around each kernel
+    recs = [st.step(record=True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
     per_kernel = {}
     for r in recs:
         for name, a, b in r:

@@ -231,10 +231,25 @@ FFDP_API int ffdp_step_lncc(const float* f, const float* u, ffdp_dims buf_dims, 
  * joint (mi.hpp:181-196), so the raw marginals are payload only (distops.hpp:366-372). Then allreduce raw
  * (if sharded), ffdp_mi_finalize(raw, B, -1, table), and pass 2. f, u as for
  * ffdp_step_lncc (halo planes allowed, not needed); interior planes are processed.
+ * workspace: device scratch of ffdp_step_mi_workspace_bytes(B) bytes, or NULL for a
+ * stream-ordered allocation per call (pass one to capture the step in a CUDA graph).
  */
 FFDP_API int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
-                      const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, int32_t* miss,
-                      void* stream);
+                      const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, void* workspace,
+                      int32_t* miss, void* stream);
+
+/* Bytes of device scratch the MI step passes need for `bins` bins. */
+FFDP_API int64_t ffdp_step_mi_workspace_bytes(int bins);
+
+/*
+ * The whole single-GPU MI step in one call (pass 1, finalize with upstream -1 -- the
+ * loss is -MI, distops.hpp:391-392 -- and pass 2). raw (B*B + 2B doubles) is zeroed
+ * here; table as ffdp_mi_finalize (the loss is -table[2B^2 + 2B + 1]). Launch-only
+ * (no host synchronisation), so it can be captured in a CUDA graph.
+ */
+FFDP_API int ffdp_step_mi(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
+                 const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, double* table, float* g_u,
+                 void* workspace, int32_t* miss, void* stream);
 
 /* Pass 2: re-samples Mw, dL/dMw from the ghat table (mi.hpp:392-421), g_u (3N). */
 FFDP_API int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,

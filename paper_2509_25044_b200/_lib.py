@@ -87,7 +87,10 @@ _SIGS = {
     "ffdp_step_lncc": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.c_int, C.c_double,
                                  C.c_double, C.c_float, C.c_float, _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_hist": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
-                                    _vp, _vp, _vp]),
+                                    _vp, _vp, _vp, _vp]),
+    "ffdp_step_mi_workspace_bytes": (C.c_int64, [C.c_int]),
+    "ffdp_step_mi": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
+                               _vp, _vp, _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_grad": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
                                     _vp, _vp, _vp, _vp]),
     "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
@@ -123,7 +126,7 @@ class _Lib:
     def __getattr__(self, name):
         lib = self.load()
         fn = getattr(lib, name)
-        if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check"):
+        if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check", "ffdp_step_mi_workspace_bytes"):
             return fn
 
         def call(*args):

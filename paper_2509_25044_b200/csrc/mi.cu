@@ -448,7 +448,8 @@ static SlabIdx make_slab_idx(const ffdp_dims& d, const ffdp_slab& s) {
 bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                           const ffdp_parzen& k);
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
-                 const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, int32_t* miss, cudaStream_t st);
+                 const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
+                 int32_t* miss, cudaStream_t st);
 int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, const double* table, float* g_u, int32_t* miss,
                  cudaStream_t st);
@@ -510,23 +511,29 @@ int ffdp_mi_bwd(const float* vi, const float* vj, int64_t n, const ffdp_parzen* 
     return check_launch("mi_bwd");
 }
 
+int64_t ffdp_step_mi_workspace_bytes(int bins) {
+    return (int64_t)sizeof(unsigned long long) * 2 * ((int64_t)bins * bins + 2 * bins);
+}
+
 int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
-                      const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, int32_t* miss,
-                      void* stream) {
+                      const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, void* workspace,
+                      int32_t* miss, void* stream) {
     if (int rc = check_parzen(kernel)) return rc;
     if (int rc = check_slab_mi(d, s)) return rc;
     const char* why = nullptr;
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!f || !u || !raw || !m.data) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    if (mi_quad_path_applies(d, s, m, *kernel)) return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, miss, st);
+    if (mi_quad_path_applies(d, s, m, *kernel))
+        return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, (unsigned long long*)workspace, miss, st);
     const int B = kernel->bins;
     const int nh = B * B + 2 * B;
     const ffdp_dims out{d.nx, d.ny, s.nz_global};
     const Geom g = make_geom(m, out, *args);
     const SlabIdx si = make_slab_idx(d, s);
     const ParzenDev p = make_parzen_dev(*kernel);
-    unsigned long long* gh = (unsigned long long*)scratch_alloc(sizeof(unsigned long long) * 2 * nh, st);
+    unsigned long long* gh = (unsigned long long*)workspace;
+    if (!gh) gh = (unsigned long long*)scratch_alloc(sizeof(unsigned long long) * 2 * nh, st);
     if (!gh) return set_error(FFDP_CUDA, "step_mi: scratch allocation failed");
     cudaMemsetAsync(gh, 0, sizeof(unsigned long long) * 2 * nh, st);
     const int chunk = chunk_for(*kernel);
@@ -536,8 +543,20 @@ int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims d, ffdp_slab s, 
     else
         k_step_mi_hist<true><<<nb, kMiNT, hist_smem(B), st>>>(g, si, f, u, p, chunk, gh, miss);
     k_fix_to_raw<<<(nh + 255) / 256, 256, 0, st>>>(gh, nh, raw);
-    scratch_free(gh, st);
+    if (!workspace) scratch_free(gh, st);
     return check_launch("step_mi_hist");
+}
+
+int ffdp_step_mi(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
+                 const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, double* table, float* g_u,
+                 void* workspace, int32_t* miss, void* stream) {
+    if (int rc = check_parzen(kernel)) return rc;
+    if (!raw || !table) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null raw/table");
+    const int B = kernel->bins;
+    cudaMemsetAsync(raw, 0, sizeof(double) * (B * B + 2 * B), (cudaStream_t)stream);
+    if (int rc = ffdp_step_mi_hist(f, u, d, s, m, args, kernel, raw, workspace, miss, stream)) return rc;
+    if (int rc = ffdp_mi_finalize(raw, B, -1.0, table, stream)) return rc;
+    return ffdp_step_mi_grad(f, u, d, s, m, args, kernel, table, g_u, miss, stream);
 }
 
 int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,

@@ -31,7 +31,7 @@ constexpr int R = 3, WIN = 7;
 constexpr int TX = 64, TY = 8, NT = 256;
 constexpr int HX = TX + 2 * R, HY = TY + 2 * R;  // 70 x 14
 constexpr int HXP = 72;                          // ring row pitch (float2)
-constexpr int NOUT = TX * TY;                    // 512 outputs per plane, 2 per thread
+constexpr int NOUT = TX * TY;                    // 512 outputs per plane, 2 per thread (a y pair)
 constexpr int NHALO = HX * HY - NOUT;            // 468
 constexpr int XJOBS = HY * (TX / 4);             // 224 x-pass runs of 4
 constexpr int NSLOT = 8;                         // planes p-7 .. p
@@ -92,25 +92,44 @@ __device__ __forceinline__ Cell cell_at(const Geom& g, const double (&kz)[3], in
     return c;
 }
 
-// The thread's four sample positions (2 owned outputs, up to 2 halo positions); their
-// (x, y) is fixed for the whole z march.
-struct Pos {
-    int gx[4], gy[4];   // lattice coordinates
-    int hx[4], hy[4];   // haloed tile coordinates
-    bool inxy[4];       // inside the lattice in x, y (and a valid slot)
+// The thread's four sample positions, fixed for the whole z march: k = 0, 1 its owned
+// outputs (a vertical pair, so the y sums share rows), k = 2, 3 halo positions
+// (k = 3 exists for the first NHALO - NT threads only). Recomputed (a few integer ops)
+// instead of held in registers.
+struct Pos1 {
+    int hx, hy, gx, gy;
+    bool inxy;  // inside the lattice in x, y, and an existing slot
 };
+
+__device__ __forceinline__ Pos1 pos_of(int k, int t, int x0, int y0, const Params& P) {
+    Pos1 q;
+    bool slot_ok = true;
+    if (k < 2) {
+        q.hx = (t & (TX - 1)) + R;
+        q.hy = 2 * (t / TX) + k + R;
+    } else {
+        const int h = t + NT * (k - 2);
+        slot_ok = h < NHALO;
+        halo_pos(slot_ok ? h : 0, q.hx, q.hy);
+    }
+    q.gx = x0 + q.hx - R;
+    q.gy = y0 + q.hy - R;
+    q.inxy = slot_ok && q.gx >= 0 && q.gx < P.nx && q.gy >= 0 && q.gy < P.ny;
+    return q;
+}
 
 struct Pref {
     float f[4], u[4][3];
 };
 
-__device__ __forceinline__ void prefetch(const Params& P, const Pos& ps, int64_t p, Pref& pf) {
+__device__ __forceinline__ void prefetch(const Params& P, int t, int x0, int y0, int64_t p, Pref& pf) {
     const bool plane_in = p >= 0 && p < P.nz_global;
     const int64_t zoff = (p - P.buf_z0) * P.plane;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const bool ok = plane_in && ps.inxy[k];
-        const int64_t bi = zoff + (int64_t)ps.gy[k] * P.nx + ps.gx[k];
+        const Pos1 q = pos_of(k, t, x0, y0, P);
+        const bool ok = plane_in && q.inxy;
+        const int64_t bi = zoff + (int64_t)q.gy * P.nx + q.gx;
         pf.f[k] = ok ? __ldg(P.f + bi) : 0.0f;
         pf.u[k][0] = ok ? __ldg(P.u + 3 * bi) : 0.0f;
         pf.u[k][1] = ok ? __ldg(P.u + 3 * bi + 1) : 0.0f;
@@ -119,7 +138,7 @@ __device__ __forceinline__ void prefetch(const Params& P, const Pos& ps, int64_t
 }
 
 template <int SLOT, bool FULLWIN>
-__device__ __forceinline__ void plane_step(const Params& P, Smem& sm, const Pos& ps, Pref& pf, float (&gur)[4][2][3],
+__device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Pref (&pf)[2], float (&gur)[4][2][3],
                                            double (&Z)[2][5], double& nsum, int& miss, int64_t p, int64_t pstart,
                                            int64_t pend, int x0, int y0, int64_t zc0) {
     if (p >= pend) return;  // uniform across the CTA
@@ -129,33 +148,55 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, const Pos&
     const int slot_old = (slot + 1) & (NSLOT - 1);  // plane p-7
 
     // ---- S1: sampling ------------------------------------------------------------
-    Pref cur = pf;
-    if (p + 1 < pend) prefetch(P, ps, p + 1, pf);  // next plane's F, u in flight during this plane
+    // register ping-pong: this plane's F, u were loaded during the previous plane; the
+    // next plane's loads are issued now and land while this plane is processed
+    const Pref& cur = pf[SLOT & 1];
+    if (p + 1 < pend) prefetch(P, t, x0, y0, p + 1, pf[(SLOT + 1) & 1]);
     const double zd = i2d((int32_t)p);
     double kz[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) kz[a] = fma(P.g.P[3 * a + 2], zd, P.g.K[a]);
-    Cell c[4];
-    Corners cr[4];
+    // two batches (owned pair, halo pair): the 16 corner loads of a batch are in flight together
 #pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = cell_at(P.g, kz, ps.gx[k], ps.gy[k], cur.u[k][0], cur.u[k][1], cur.u[k][2]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const bool ok = plane_in && ps.inxy[k];
-        float2 v = make_float2(0.f, 0.f);
-        if (k < 2) {
-            float d[3];
-            const float mw = interp_grad(cr[k], c[k], d);
-            if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) gur[SLOT][k][a] = ok ? P.g.dscale[a] * d[a] : 0.0f;
-        } else {
-            const float mw = interp(cr[k], c[k]);
-            if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
+    for (int bt = 0; bt < 2; ++bt) {
+        // slot 3 (second halo position) exists for the first NHALO - NT threads only
+        if (bt == 1 && !__any_sync(0xffffffffu, t + NT < NHALO)) {
+            const Pos1 q = pos_of(2, t, x0, y0, P);
+            Cell c = cell_at(P.g, kz, q.gx, q.gy, cur.u[2][0], cur.u[2][1], cur.u[2][2]);
+            const Corners cr = gather_pad<FULLWIN>(P.g, c, miss);
+            const float mw = interp(cr, c);
+            sm.raw[slot][q.hy][q.hx] =
+                (plane_in && q.inxy) ? make_float2(cur.f[2] - P.sf, mw - P.sm) : make_float2(0.f, 0.f);
+            continue;
         }
-        if (k < 2 || t + NT * (k - 2) < NHALO) sm.raw[slot][ps.hy[k]][ps.hx[k]] = v;
+        Pos1 q[2];
+        Cell c[2];
+        Corners cr[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int k = 2 * bt + i;
+            q[i] = pos_of(k, t, x0, y0, P);
+            c[i] = cell_at(P.g, kz, q[i].gx, q[i].gy, cur.u[k][0], cur.u[k][1], cur.u[k][2]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) cr[i] = gather_pad<FULLWIN>(P.g, c[i], miss);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int k = 2 * bt + i;
+            const bool ok = plane_in && q[i].inxy;
+            float2 v = make_float2(0.f, 0.f);
+            if (bt == 0) {
+                float d[3];
+                const float mw = interp_grad(cr[i], c[i], d);
+                if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) gur[SLOT][i][a] = ok ? P.g.dscale[a] * d[a] : 0.0f;
+            } else {
+                const float mw = interp(cr[i], c[i]);
+                if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
+            }
+            if (k < 3 || t + NT < NHALO) sm.raw[slot][q[i].hy][q[i].hx] = v;
+        }
     }
     __syncthreads();
 
@@ -190,17 +231,20 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, const Pos&
     const bool emit = p >= zc0 + R;
     const int64_t q = p - R;
     const int slot_q = (slot + NSLOT - R) & (NSLOT - 1);
+    const int ox = t & (TX - 1), oy0 = 2 * (t / TX);
+#pragma unroll
+    for (int ch = 0; ch < 5; ++ch) {
+        // rows oy0 .. oy0+7 cover the windows of both owned outputs
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < WIN; ++k) s += sm.X[ch][oy0 + k][ox];
+        Z[0][ch] += (double)s;
+        s += sm.X[ch][oy0 + WIN][ox] - sm.X[ch][oy0][ox];
+        Z[1][ch] += (double)s;
+    }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        const int o = t + NT * j;
-        const int ox = o & (TX - 1), oy = o / TX;
-#pragma unroll
-        for (int ch = 0; ch < 5; ++ch) {
-            float s = 0.f;
-#pragma unroll
-            for (int k = 0; k < WIN; ++k) s += sm.X[ch][oy + k][ox];
-            Z[j][ch] += (double)s;
-        }
+        const int oy = oy0 + j;
         const int gx = x0 + ox, gy = y0 + oy;
         if (emit && gx < P.nx && gy < P.ny) {
             const float2 fm = sm.raw[slot_q][oy + R][ox + R];
@@ -250,26 +294,6 @@ __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
     if (zc0 >= zc1) return;
     for (int i = threadIdx.x; i < NSLOT * HY * HXP; i += NT) (&sm.raw[0][0][0])[i] = make_float2(0.f, 0.f);
     const int t = threadIdx.x;
-    Pos ps;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        int hx, hy;
-        bool slot_ok = true;
-        if (k < 2) {
-            const int o = t + NT * k;
-            hx = (o & (TX - 1)) + R;
-            hy = o / TX + R;
-        } else {
-            const int h = t + NT * (k - 2);
-            slot_ok = h < NHALO;
-            halo_pos(slot_ok ? h : 0, hx, hy);
-        }
-        ps.hx[k] = hx;
-        ps.hy[k] = hy;
-        ps.gx[k] = x0 + hx - R;
-        ps.gy[k] = y0 + hy - R;
-        ps.inxy[k] = slot_ok && ps.gx[k] >= 0 && ps.gx[k] < P.nx && ps.gy[k] >= 0 && ps.gy[k] < P.ny;
-    }
     float gur[4][2][3];
     double Z[2][5];
 #pragma unroll
@@ -279,14 +303,14 @@ __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
     double nsum = 0.0;
     int miss = 0;
     const int64_t pstart = zc0 - R, pend = zc1 + R;
-    Pref pf;
-    prefetch(P, ps, pstart, pf);
+    Pref pf[2];
+    prefetch(P, t, x0, y0, pstart, pf[0]);
     __syncthreads();
     for (int64_t p = pstart; p < pend; p += 4) {
-        plane_step<0, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p, pstart, pend, x0, y0, zc0);
-        plane_step<1, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p + 1, pstart, pend, x0, y0, zc0);
-        plane_step<2, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p + 2, pstart, pend, x0, y0, zc0);
-        plane_step<3, FULLWIN>(P, sm, ps, pf, gur, Z, nsum, miss, p + 3, pstart, pend, x0, y0, zc0);
+        plane_step<0, FULLWIN>(P, sm, pf, gur, Z, nsum, miss, p, pstart, pend, x0, y0, zc0);
+        plane_step<1, FULLWIN>(P, sm, pf, gur, Z, nsum, miss, p + 1, pstart, pend, x0, y0, zc0);
+        plane_step<2, FULLWIN>(P, sm, pf, gur, Z, nsum, miss, p + 2, pstart, pend, x0, y0, zc0);
+        plane_step<3, FULLWIN>(P, sm, pf, gur, Z, nsum, miss, p + 3, pstart, pend, x0, y0, zc0);
     }
     // loss partial and window misses
     nsum = warp_sum(nsum);

@@ -351,11 +351,12 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
 }
 
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
-                 const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, int32_t* miss, cudaStream_t st) {
+                 const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
+                 int32_t* miss, cudaStream_t st) {
     using namespace mstep;
     Params P = make_params(f, u, d, s, m, args, k);
     const int B = k.bins;
-    unsigned long long* h = (unsigned long long*)scratch_alloc(sizeof(unsigned long long) * B * B, st);
+    unsigned long long* h = ws ? ws : (unsigned long long*)scratch_alloc(sizeof(unsigned long long) * B * B, st);
     if (!h) return set_error(FFDP_CUDA, "step_mi: scratch allocation failed");
     cudaMemsetAsync(h, 0, sizeof(unsigned long long) * B * B, st);
     P.hist = h;
@@ -374,7 +375,7 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     else
         k_step_mi_hist<false, false><<<grid, NT, smem, st>>>(P);
     k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
-    scratch_free(h, st);
+    if (!ws) scratch_free(h, st);
     return check_launch("step_mi_hist");
 }
 

@@ -497,6 +497,7 @@ class StepWorkspace:
         self.miss = torch.zeros(1, dtype=torch.int32, device=device)
         self.raw = torch.zeros(bins * bins + 2 * bins, dtype=torch.float64, device=device)
         self.table = torch.zeros(2 * bins * bins + 2 * bins + 4, dtype=torch.float64, device=device)
+        self.scratch = torch.zeros(int(lib.ffdp_step_mi_workspace_bytes(bins)), dtype=torch.uint8, device=device)
         self.bins = bins
 
 
@@ -552,12 +553,10 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
         k = params.make_kernel()
         if params.mi_approx_forward:
             raise InvalidArgument("warp_loss_step: the fused MI step uses the exact Parzen forward")
-        ws.raw.zero_()
-        lib.ffdp_step_mi_hist(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), C.byref(k.c), _ptr(ws.raw),
-                              _ptr(ws.miss), _stream())
-        lib.ffdp_mi_finalize(_ptr(ws.raw), params.bins, -1.0, _ptr(ws.table), _stream())
-        lib.ffdp_step_mi_grad(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), C.byref(k.c), _ptr(ws.table),
-                              _ptr(g_u), _ptr(ws.miss), _stream())
+        if ws.bins != params.bins:
+            raise InvalidArgument("warp_loss_step: workspace built for a different bin count")
+        lib.ffdp_step_mi(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), C.byref(k.c), _ptr(ws.raw),
+                         _ptr(ws.table), _ptr(g_u), _ptr(ws.scratch), _ptr(ws.miss), _stream())
         if not sync:
             return StepResult(float("nan"), g_u)
         b = params.bins
