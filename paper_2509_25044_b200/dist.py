@@ -1,0 +1,311 @@
+"""Z-slab sharding of the fused warp + loss step over GPUs of one node
+(fabric.hpp:31-132, distops.hpp:36-396), one process per GPU over torch.distributed
+(NCCL on B200s, gloo on CPU for the host-logic tests).
+
+The reference rotates every moving-image shard around the ring twice per iteration
+(ring_sample / ring_sample_backward, distops.hpp:144-248) and sums zero-padded partial
+interpolations. The interpolation those partials add up to is the global one, so here
+each rank keeps a *window* of moving-image planes -- its own slab plus the planes its
+warped samples reach -- fetched once per scale (the moving image is static within a
+scale, registration.hpp:249,270) and widened only when the kernels report a window
+miss, after which the step is simply re-run (exact). Per iteration the only traffic is
+the displacement halo the LNCC window needs (r planes of u from each neighbour; F's halo
+is static) and the reductions: one double for LNCC (distops.hpp:309-318) or the B*B
+joint histogram for MI (distops.hpp:365-373, the marginals are not consumed).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from ._lib import InvalidArgument, Slab
+
+
+# ------------------------------------------------------------------ sharding rules
+def shard_ranges(n: int, world: int) -> List[Tuple[int, int]]:
+    """shard_ranges (fabric.hpp:44-57): contiguous z ranges, the first n % world shards
+    one plane longer."""
+    if world < 1 or n < world:
+        raise InvalidArgument("shard_ranges: need 1 <= world <= axis size")
+    base, extra = divmod(n, world)
+    out, lo = [], 0
+    for h in range(world):
+        size = base + (1 if h < extra else 0)
+        out.append((lo, lo + size))
+        lo += size
+    return out
+
+
+def axis_coord(i: int, n: int) -> float:
+    """axis_coord (geometry.hpp:106-109)."""
+    if n <= 1:
+        return -1.0
+    return -1.0 + 2.0 * (float(i) / float(n - 1))
+
+
+@dataclass
+class ShardSpec:
+    """ShardSpec (fabric.hpp:31-42); dims are (nz, ny, nx) like the tensors."""
+    rank: int = 0
+    world: int = 1
+    lo: int = 0
+    hi: int = 0
+    global_shape: Tuple[int, int, int] = (0, 0, 0)
+    x_min: Tuple[float, float, float] = (-1.0, -1.0, -1.0)
+    x_max: Tuple[float, float, float] = (1.0, 1.0, 1.0)
+
+    @property
+    def thickness(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def local_shape(self) -> Tuple[int, int, int]:
+        return (self.hi - self.lo, self.global_shape[1], self.global_shape[2])
+
+
+def make_shard_spec(global_shape: Sequence[int], world: int, rank: int) -> ShardSpec:
+    """make_shard_spec (fabric.hpp:59-70): bounds in the global normalized frame."""
+    nz = int(global_shape[0])
+    lo, hi = shard_ranges(nz, world)[rank]
+    return ShardSpec(rank, world, lo, hi, tuple(int(s) for s in global_shape), (-1.0, -1.0, axis_coord(lo, nz)),
+                     (1.0, 1.0, axis_coord(hi - 1, nz)))
+
+
+@dataclass
+class ShardRescale:
+    """ShardRescale (distops.hpp:36-39)."""
+    S: Tuple[float, float, float] = (1.0, 1.0, 1.0)
+    t: Tuple[float, float, float] = (0.0, 0.0, 0.0)
+
+
+def compute_shard_rescale(x_min, x_max, g_min=(-1.0, -1.0, -1.0), g_max=(1.0, 1.0, 1.0)) -> ShardRescale:
+    """compute_shard_rescale (distops.hpp:41-49): S*x_min + t = g_min, S*x_max + t = g_max."""
+    S = tuple((g_max[c] - g_min[c]) / (x_max[c] - x_min[c]) for c in range(3))
+    t = tuple(g_min[c] - S[c] * x_min[c] for c in range(3))
+    return ShardRescale(S, t)
+
+
+# ------------------------------------------------------------------ collectives
+def _world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def halo_exchange(slab: torch.Tensor, spec: ShardSpec, pad: int) -> Tuple[torch.Tensor, int, int]:
+    """halo_exchange (fabric.hpp:315-370): the slab with up to `pad` planes from each
+    neighbour along z (dim 0); rank 0 has no left halo, the last rank no right halo.
+    Returns (padded, halo_lo, halo_hi). Raises like the reference when pad exceeds a
+    neighbour's thickness."""
+    if pad < 0:
+        raise InvalidArgument("halo_exchange: pad must be >= 0")
+    w, r = spec.world, spec.rank
+    if pad == 0 or w == 1:
+        return slab, 0, 0
+    ranges = shard_ranges(spec.global_shape[0], w)
+    if r > 0 and pad > ranges[r - 1][1] - ranges[r - 1][0]:
+        raise InvalidArgument("halo_exchange: pad exceeds left neighbor thickness")
+    if r < w - 1 and pad > ranges[r + 1][1] - ranges[r + 1][0]:
+        raise InvalidArgument("halo_exchange: pad exceeds right neighbor thickness")
+    lo = pad if r > 0 else 0
+    hi = pad if r < w - 1 else 0
+    out = torch.empty((slab.shape[0] + lo + hi,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=slab.device)
+    out[lo:lo + slab.shape[0]].copy_(slab)
+    ops = []
+    if r > 0:  # my first planes become the left neighbour's right halo, and vice versa
+        ops.append(dist.P2POp(dist.isend, slab[:pad].contiguous(), r - 1))
+        ops.append(dist.P2POp(dist.irecv, out[:lo], r - 1))
+    if r < w - 1:
+        ops.append(dist.P2POp(dist.isend, slab[slab.shape[0] - pad:].contiguous(), r + 1))
+        ops.append(dist.P2POp(dist.irecv, out[lo + slab.shape[0]:], r + 1))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    return out, lo, hi
+
+
+def allreduce_sum(t: torch.Tensor, ordered: bool = False) -> torch.Tensor:
+    """allreduce_sum (fabric.hpp:246-263). ordered=True reproduces the reference's
+    rank-ordered summation bit for bit (all-gather, then sum in rank order); the default
+    is the collective's own reduction (payloads here are <= 8.7 KB)."""
+    _, w = _world()
+    if w == 1:
+        return t
+    if not ordered:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t
+    parts = [torch.empty_like(t) for _ in range(w)]
+    dist.all_gather(parts, t)
+    acc = torch.zeros_like(t)
+    for p in parts:
+        acc += p
+    t.copy_(acc)
+    return t
+
+
+def fetch_planes(slab: torch.Tensor, spec: ShardSpec, z0: int, z1: int) -> torch.Tensor:
+    """Global planes [z0, z1) of a z-sharded volume, gathered from their owners (every
+    rank calls collectively with its own request). Used to build the moving-image window;
+    the reference's equivalent is the ring rotation of whole shards (distops.hpp:154-166)."""
+    r, w = spec.rank, spec.world
+    nz = spec.global_shape[0]
+    z0, z1 = max(0, int(z0)), min(nz, int(z1))
+    out = torch.zeros((max(0, z1 - z0),) + tuple(slab.shape[1:]), dtype=slab.dtype, device=slab.device)
+    req = torch.tensor([z0, z1], dtype=torch.int64, device=slab.device if slab.is_cuda else "cpu")
+    if w == 1:
+        out.copy_(slab[z0 - spec.lo:z1 - spec.lo])
+        return out
+    reqs = [torch.empty_like(req) for _ in range(w)]
+    dist.all_gather(reqs, req)
+    reqs = [tuple(int(v) for v in q.tolist()) for q in reqs]
+    ranges = shard_ranges(nz, w)
+    ops = []
+    for peer in range(w):
+        # what I send to peer: my planes inside peer's request
+        a, b = max(reqs[peer][0], spec.lo), min(reqs[peer][1], spec.hi)
+        if peer != r and a < b:
+            ops.append(dist.P2POp(dist.isend, slab[a - spec.lo:b - spec.lo].contiguous(), peer))
+        # what I receive from peer: peer's planes inside my request
+        plo, phi = ranges[peer]
+        a2, b2 = max(z0, plo), min(z1, phi)
+        if peer != r and a2 < b2:
+            ops.append(dist.P2POp(dist.irecv, out[a2 - z0:b2 - z0], peer))
+    a, b = max(z0, spec.lo), min(z1, spec.hi)
+    if a < b:
+        out[a - z0:b - z0].copy_(slab[a - spec.lo:b - spec.lo])
+    if ops:
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+    return out
+
+
+# ------------------------------------------------------------------ the sharded step
+@dataclass
+class ShardedStepState:
+    spec: ShardSpec
+    f_halo: torch.Tensor           # F slab + r halo planes (static within a scale)
+    halo_lo: int
+    halo_hi: int
+    m_window: Optional[object] = None  # voxreg-style window: padded tensor + [z0, z1)
+    m_z0: int = 0
+    m_z1: int = 0
+    window_fetches: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class ShardedStep:
+    """The deformable step (registration.hpp:277-312) on one rank's z slab.
+
+    Constructed once per scale with the rank's F and M slabs; `step(u_slab)` returns
+    (loss, g_u_slab) with the loss reduced over all ranks. The per-GPU compute is the
+    same fused kernel as the single-GPU path, run on the slab with its halo planes."""
+
+    R = 3  # LNCC window radius (window 7)
+
+    def __init__(self, f_slab: torch.Tensor, m_slab: torch.Tensor, spec: ShardSpec, A=None, t=None,
+                 params=None, margin_planes: int = 8):
+        from . import voxreg
+        self.V = voxreg
+        self.params = params or voxreg.LossParams()
+        self.spec = spec
+        self.A = np.eye(3) if A is None else np.asarray(A, dtype=np.float64)
+        self.t = np.zeros(3) if t is None else np.asarray(t, dtype=np.float64)
+        self.f = f_slab.to(torch.float32).contiguous()
+        self.m = m_slab.to(torch.float32).contiguous()
+        self.pad = self.R if self.params.kind == "lncc" else 0
+        self.f_halo, self.hlo, self.hhi = halo_exchange(self.f, spec, self.pad)
+        self.ws = voxreg.StepWorkspace(self.f.device, self.params.bins)
+        self.margin = int(margin_planes)
+        self.m_z0 = self.m_z1 = None
+        self.window_fetches = 0
+        self.shifts = None
+
+    # -- moving window ------------------------------------------------------------------
+    def _ensure_window(self, z0: int, z1: int):
+        nz = self.spec.global_shape[0]
+        z0, z1 = max(0, z0), min(nz, z1)
+        if self.m_z0 is not None and self.m_z0 <= z0 and self.m_z1 >= z1:
+            return
+        # the window request is collective: agree on widening across ranks
+        lohi = torch.tensor([z0, z1], dtype=torch.int64, device=self.f.device)
+        planes = fetch_planes(self.m, self.spec, int(lohi[0]), int(lohi[1]))
+        nzw = planes.shape[0]
+        pad = torch.zeros((nzw + 4, planes.shape[1] + 4, planes.shape[2] + 4), dtype=torch.float32,
+                          device=self.f.device)
+        pad[2:-2, 2:-2, 2:-2].copy_(planes)
+        self.m_pad, self.m_z0, self.m_z1 = pad, z0, z1
+        self.window_fetches += 1
+
+    def _window(self):
+        from ._lib import Dims, ImageWindow
+        nz, ny, nx = self.spec.global_shape
+        return ImageWindow(self.m_pad.data_ptr(), Dims(nx, ny, nz), self.m_z0, self.m_z1, 2)
+
+    # -- the step -------------------------------------------------------------------------
+    def step(self, u_slab: torch.Tensor, max_retries: int = 4):
+        V, p, spec = self.V, self.params, self.spec
+        u_slab = u_slab.to(torch.float32).contiguous()
+        u_h, lo, hi = halo_exchange(u_slab, spec, self.pad)
+        nzl = spec.thickness
+        ny, nx = spec.global_shape[1], spec.global_shape[2]
+        slab = Slab(spec.lo - lo, nzl + lo + hi, spec.lo, spec.hi, spec.global_shape[0])
+        dims = V._dims((nzl + lo + hi, ny, nx))
+        args = V.SamplerArgs(A=self.A, t=self.t).to_c()
+        n_total = spec.global_shape[0] * ny * nx
+        g_u = torch.empty_like(u_slab)
+        if self.m_z0 is None:
+            self._ensure_window(spec.lo - lo - self.margin, spec.hi + hi + self.margin)
+        if p.kind == "lncc" and self.shifts is None:
+            # the moment shift must be the same on every rank (it is part of the arithmetic)
+            mm = torch.tensor([self.f.min(), -self.f.max(), self.m.min(), -self.m.max()], dtype=torch.float64,
+                              device=self.f.device)
+            if spec.world > 1:
+                dist.all_reduce(mm, op=dist.ReduceOp.MIN)
+            v = mm.tolist()
+            self.shifts = (0.5 * (v[0] - v[1]), 0.5 * (v[2] - v[3]))
+        from ._lib import lib
+        for attempt in range(max_retries + 1):
+            self.ws.miss.zero_()
+            win = self._window()
+            stream = V._stream()
+            if p.kind == "lncc":
+                self.ws.sum_n.zero_()
+                lib.ffdp_step_lncc(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args), p.window,
+                                   p.epsilon, -1.0 / n_total, self.shifts[0], self.shifts[1], V._ptr(g_u),
+                                   V._ptr(self.ws.sum_n), V._ptr(self.ws.miss), stream)
+            else:
+                k = p.make_kernel()
+                self.ws.raw.zero_()
+                lib.ffdp_step_mi_hist(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args), C.byref(k.c),
+                                      V._ptr(self.ws.raw), V._ptr(self.ws.scratch), V._ptr(self.ws.miss), stream)
+            # a miss on any rank means the step has to be redone everywhere (collective agreement)
+            miss = self.ws.miss.to(torch.int64)
+            if spec.world > 1:
+                dist.all_reduce(miss, op=dist.ReduceOp.MAX)
+            if int(miss.item()) == 0:
+                break
+            ext = torch.empty(2, dtype=torch.int64, device=self.f.device)
+            lib.ffdp_sampler_z_extent(V._ptr(u_h), dims, V._dims(spec.global_shape), C.byref(
+                V.SamplerArgs(A=self.A, t=self.t, bounds=V.DomainBounds(
+                    (-1.0, -1.0, axis_coord(spec.lo - lo, spec.global_shape[0])),
+                    (1.0, 1.0, axis_coord(spec.hi + hi - 1, spec.global_shape[0])))).to_c()), V._ptr(ext), stream)
+            e = ext.tolist()
+            self.m_z0 = None
+            self._ensure_window(min(e[0], spec.lo) - 1, max(e[1], spec.hi) + 2)
+        else:
+            raise RuntimeError("ShardedStep: moving window kept missing")
+        if p.kind == "lncc":
+            s = allreduce_sum(self.ws.sum_n)
+            return 1.0 - float(s.item()) / n_total, g_u
+        b = p.bins
+        allreduce_sum(self.ws.raw[:b * b])
+        lib.ffdp_mi_finalize(V._ptr(self.ws.raw), b, -1.0, V._ptr(self.ws.table), V._stream())
+        k = p.make_kernel()
+        lib.ffdp_step_mi_grad(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, self._window(), C.byref(args), C.byref(k.c),
+                              V._ptr(self.ws.table), V._ptr(g_u), V._ptr(self.ws.miss), V._stream())
+        return -float(self.ws.table[2 * b * b + 2 * b + 1].item()), g_u
