@@ -100,65 +100,73 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ synthetic inputs
-def synth_inputs(shape, loss, seed, device):
-    """Synthetic pair of the survey's recipe on the GPU: smooth
-    ellipsoidal structures with texture, M = F pushed through a smooth warp (<=0.12
-    normalized), u = smooth field + U(-0.01, 0.01) jitter, A = I + U(-0.02, 0.02),
-    t = U(-0.02, 0.02). MI: M = normalize(4 m (1 - m) + 0.02 noise)."""
+def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None):
+    """Synthetic pair of the survey's recipe on the GPU, analytic in the
+    global normalized frame so any z slab [z0, z1) of the global `shape` is generated
+    locally and consistently across ranks: smooth ellipsoidal structures with texture,
+    M = F pushed through a smooth warp, u = smooth field + sub-voxel jitter,
+    A = I + U(-0.02, 0.02), t = U(-0.02, 0.02). MI: M = normalize(4 m (1 - m) + noise).
+    reduce_minmax(lo, hi) -> (lo, hi) makes the intensity normalisation global."""
     import numpy as np
     import torch
-
-    from paper_2509_25044_b200 import voxreg
 
     g = torch.Generator(device="cpu").manual_seed(seed)
     rnd = lambda *s: torch.rand(*s, generator=g, dtype=torch.float64)
     nz, ny, nx = shape
+    z1 = nz if z1 is None else z1
+    lshape = (z1 - z0, ny, nx)
     ax = lambda n: torch.linspace(-1.0, 1.0, n, device=device, dtype=torch.float32)
-    z, y, x = ax(nz).view(nz, 1, 1), ax(ny).view(1, ny, 1), ax(nx).view(1, 1, nx)
-    f = torch.zeros(shape, dtype=torch.float32, device=device)
-    for _ in range(6):
-        c = (rnd(3) * 1.2 - 0.6).tolist()
-        r = (rnd(3) * 0.3 + 0.2).tolist()
-        inten = float(rnd(1) * 0.7 + 0.3)
-        q = ((x - c[0]) / r[0]) ** 2 + ((y - c[1]) / r[1]) ** 2 + ((z - c[2]) / r[2]) ** 2
-        f += inten * torch.sigmoid((1.0 - q) * 10.0)
-        del q
-    for _ in range(3):
-        k = (rnd(3) * 12 + 4).tolist()
-        ph = (rnd(3) * 6.28).tolist()
-        f += 0.04 * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(k[2] * z + ph[2])
-    f = (f - f.min()) / (f.max() - f.min())
+    z, y, x = ax(nz)[z0:z1].view(-1, 1, 1), ax(ny).view(1, ny, 1), ax(nx).view(1, 1, nx)
+    blobs = [((rnd(3) * 1.2 - 0.6).tolist(), (rnd(3) * 0.3 + 0.2).tolist(), float(rnd(1) * 0.7 + 0.3))
+             for _ in range(6)]
+    tex = [((rnd(3) * 12 + 4).tolist(), (rnd(3) * 6.28).tolist()) for _ in range(3)]
+
+    def f_at(X, Y, Z):
+        out = torch.zeros(torch.broadcast_shapes(X.shape, Y.shape, Z.shape), dtype=torch.float32, device=device)
+        for c, r, inten in blobs:
+            out += inten * torch.sigmoid((1.0 - (((X - c[0]) / r[0]) ** 2 + ((Y - c[1]) / r[1]) ** 2 +
+                                                 ((Z - c[2]) / r[2]) ** 2)) * 10.0)
+        for k, ph in tex:
+            out += 0.04 * torch.sin(k[0] * X + ph[0]) * torch.sin(k[1] * Y + ph[1]) * torch.sin(k[2] * Z + ph[2])
+        return out
 
     def smooth_field(amp):
-        u = torch.zeros(shape + (3,), dtype=torch.float32, device=device)
-        for c in range(3):
-            for _ in range(3):
-                k = (rnd(3) * 3 + 0.5).tolist()
-                ph = (rnd(3) * 6.28).tolist()
-                a = float(rnd(1) * 2 - 1) * amp
-                u[..., c] += a * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(k[2] * z + ph[2])
+        modes = [[((rnd(3) * 3 + 0.5).tolist(), (rnd(3) * 6.28).tolist(), float(rnd(1) * 2 - 1) * amp)
+                  for _ in range(3)] for _ in range(3)]
+        u = torch.zeros(lshape + (3,), dtype=torch.float32, device=device)
+        for cpt in range(3):
+            for k, ph, a in modes[cpt]:
+                u[..., cpt] += a * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(
+                    k[2] * z + ph[2])
         return u
 
+    def normalize(v):
+        lo, hi = float(v.min()), float(v.max())
+        if reduce_minmax is not None:
+            lo, hi = reduce_minmax(lo, hi)
+        return ((v - lo) / (hi - lo)).clamp_(0.0, 1.0)
+
+    f = normalize(f_at(x, y, z))
     u_true = smooth_field(0.04)
-    m = voxreg.fused_sample(f, u_true, voxreg.SamplerArgs())
+    m = normalize(f_at(x + u_true[..., 0], y + u_true[..., 1], z + u_true[..., 2]))
     del u_true
-    m = (m - m.min()) / (m.max() - m.min())
     if loss == "mi":
-        noise = torch.randn(shape, generator=torch.Generator(device=device).manual_seed(seed + 1), device=device)
-        m = 4.0 * m * (1.0 - m) + 0.02 * noise
+        noise = torch.randn(lshape, generator=torch.Generator(device=device).manual_seed(seed + 1 + z0), device=device)
+        m = normalize(4.0 * m * (1.0 - m) + 0.02 * noise)
         del noise
-        m = (m - m.min()) / (m.max() - m.min())
     u = smooth_field(0.02)
     # sub-voxel jitter (+-0.02 voxel) keeps samples off cell faces; a registration warp is
     # smooth (it is Gaussian-smoothed every iteration, registration.hpp:316), so the
     # parity tests' U(-0.01, 0.01)-normalized jitter (+-1.3 voxels at 256^3) would be an
     # unrealistically rough field for a throughput benchmark
     jit = torch.tensor([0.04 / (nx - 1), 0.04 / (ny - 1), 0.04 / (nz - 1)], device=device)
-    u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2), device=device) - 0.5) * jit
+    u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2 + z0), device=device)
+          - 0.5) * jit
     aff = rnd(12).numpy() * 0.04 - 0.02
     A = np.eye(3) + aff[:9].reshape(3, 3)
     t = aff[9:]
-    torch.cuda.synchronize()
+    if torch.device(device).type == "cuda":
+        torch.cuda.synchronize()
     return f.contiguous(), m.contiguous(), u.contiguous(), A, t
 
 
@@ -253,30 +261,109 @@ class Stepper:
         return -float(self.ws.table[2 * b * b + 2 * b + 1].item())
 
 
+def run_sharded(args, rank, world, local_rank, dev):
+    """N > 1: weak scaling over z slabs of a (world * nz) x ny x nx volume, one rank per
+    GPU over NCCL (paper_2509_25044_b200.dist.ShardedStep): per step the u halo
+    exchange, the fused kernel(s) on the slab and the loss / histogram allreduce."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200 import voxreg
+
+    shape, loss, cfg = WORKLOADS[args.workload]
+    gshape = (shape[0] * world, shape[1], shape[2])
+    spec = D.make_shard_spec(gshape, world, rank)
+
+    def reduce_minmax(lo, hi):
+        t = torch.tensor([lo, -hi], dtype=torch.float64, device=dev)
+        D.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t[0]), -float(t[1])
+
+    f, m, u, A, t = synth_inputs(gshape, loss, 1234, dev, spec.lo, spec.hi, reduce_minmax)
+    params = voxreg.LossParams(kind=loss, bins=32)
+    st = D.ShardedStep(f, m, spec, A, t, params)
+    for _ in range(args.warmup):
+        st.step(u)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    loss_val = None
+    for _ in range(args.steps):
+        loss_val, _ = st.step(u)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks.stop()
+    tt = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    D.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_step = float(tt.item()) / args.steps
+    nvox_total = gshape[0] * gshape[1] * gshape[2]
+    value = nvox_total / (ms_step * 1e-3) / 1e9
+    hbm, hbm_kind = peaks()
+    nloc = f.numel()
+    per_gpu_gbs = BYTES_PER_VOXEL[loss] * nloc / (ms_step * 1e-3) / 1e9
+    # end to end: host (pinned) inputs of the rank's slab copied in every step, loss read back
+    hf, hm, hu = (x.cpu().pin_memory() for x in (f, m, u))
+    steps_e2e = max(3, min(args.steps, 10))
+    dist.barrier()
+    e0.record()
+    for _ in range(steps_e2e):
+        f.copy_(hf, non_blocking=True)
+        m.copy_(hm, non_blocking=True)
+        u.copy_(hu, non_blocking=True)
+        st.reload(f, m)  # new pair: F halo planes + moving window rebuilt from the copied slabs
+        lv, _ = st.step(u)
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / steps_e2e], device=dev, dtype=torch.float64)
+    D.all_reduce(te, op=dist.ReduceOp.MAX)
+    return {
+        "metric": METRIC, "value": round(value, 3), "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 coordinates / moment sums)", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}] per GPU, weak scaling",
+                   "volume": "x".join(str(s) for s in gshape[::-1]), "loss": loss, "voxels_per_gpu": nloc,
+                   "parallelism": f"z-slab x{world} ({dist.get_backend()} halo + allreduce)",
+                   "l2": "inputs exceed the 126 MB L2; no flush between steps"},
+        "loss": loss_val,
+        "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": round(per_gpu_gbs, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(per_gpu_gbs / hbm, 4), "traffic": None, "peak_kind": hbm_kind,
+                     "algorithmic_bytes_per_voxel": BYTES_PER_VOXEL[loss]},
+        "gpu_launches": (1 if loss == "lncc" else 4) * args.steps,
+        "window_fetches": st.window_fetches,
+        "clocks": clocks.summary(),
+        "e2e": {"value": round(nvox_total / (float(te.item()) * 1e-3) / 1e9, 4), "unit": "Gvoxel/s",
+                "h2d_bytes_per_step": 4 * (f.numel() + m.numel() + u.numel()), "d2h_bytes_per_step": 8},
+    }
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
 
+    local_rank %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     from paper_2509_25044_b200._lib import lib
     so = lib.load()
     if so.ffdp_device_check() != 0:
         raise RuntimeError(so.ffdp_last_error().decode())
+    if world > 1:
+        return run_sharded(args, rank, world, local_rank, dev), None
     shape, loss, cfg = WORKLOADS[args.workload]
-    # weak scaling: every rank owns a full per-GPU workload (independent z-slab shards
-    # of a world-size-times-taller volume need no data-path collective for MI pass 2;
-    # see DESIGN.md "multi-GPU")
-    f, m, u, A, t = synth_inputs(shape, loss, 1234 + rank, dev)
+    f, m, u, A, t = synth_inputs(shape, loss, 1234, dev)
     st = Stepper(f, m, u, A, t, loss)
     hbm, hbm_kind = peaks()
     for _ in range(args.warmup):
         st.step()
     torch.cuda.synchronize()
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
@@ -291,14 +378,8 @@ def run_ours(args, rank, world, local_rank):
         graph.replay()
     e1.record()
     torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
     clocks.stop()
     ms = e0.elapsed_time(e1)
-    if dist is not None:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
     # per-kernel device time: the same K steps launched with events around each kernel
     recs = [st.step(record=True) for _ in range(args.steps)]
     torch.cuda.synchronize()
@@ -449,10 +530,12 @@ def main():
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        # FFDP_DIST_BACKEND=gloo runs the sharded path with several ranks on one GPU
+        # (host-staged exchanges; a functional check, not a scaling measurement)
+        dist.init_process_group(os.environ.get("FFDP_DIST_BACKEND", "nccl"))
     out, st = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:
             try:
                 out["cpu_baseline"] = cpu_reference(loss, cpu_sample_for(loss), 2, os.cpu_count() or 1)
             except Exception as e:  # the baseline is reported, never required

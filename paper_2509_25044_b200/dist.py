@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -98,6 +98,48 @@ def _world():
     return 0, 1
 
 
+def _staged() -> bool:
+    """gloo moves CPU tensors only: CUDA tensors are staged through host memory (used to
+    run the sharded path with several ranks on one GPU; NCCL moves device memory)."""
+    return dist.is_initialized() and dist.get_backend() == "gloo"
+
+
+def _p2p(ops_spec):
+    """ops_spec: list of (kind, tensor, peer), kind 'send'|'recv'. Runs them as one batch,
+    staging CUDA tensors through the host under gloo."""
+    staged = _staged()
+    ops, back = [], []
+    for kind, t, peer in ops_spec:
+        buf = t
+        if staged and t.is_cuda:
+            buf = t.detach().cpu() if kind == "send" else torch.empty(t.shape, dtype=t.dtype)
+            if kind == "recv":
+                back.append((t, buf))
+        elif kind == "send":
+            buf = t.contiguous()
+        ops.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, buf, peer))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for t, buf in back:
+        t.copy_(buf)
+
+
+def _collective(fn, t: torch.Tensor, *a, **kw):
+    if _staged() and t.is_cuda:
+        h = t.detach().cpu()
+        fn(h, *a, **kw)
+        t.copy_(h)
+        return t
+    fn(t, *a, **kw)
+    return t
+
+
+def all_reduce(t: torch.Tensor, op=None) -> torch.Tensor:
+    """dist.all_reduce that also runs under gloo on CUDA tensors (host staging)."""
+    return _collective(dist.all_reduce, t, op=op if op is not None else dist.ReduceOp.SUM)
+
+
 def halo_exchange(slab: torch.Tensor, spec: ShardSpec, pad: int) -> Tuple[torch.Tensor, int, int]:
     """halo_exchange (fabric.hpp:315-370): the slab with up to `pad` planes from each
     neighbour along z (dim 0); rank 0 has no left halo, the last rank no right halo.
@@ -119,13 +161,12 @@ def halo_exchange(slab: torch.Tensor, spec: ShardSpec, pad: int) -> Tuple[torch.
     out[lo:lo + slab.shape[0]].copy_(slab)
     ops = []
     if r > 0:  # my first planes become the left neighbour's right halo, and vice versa
-        ops.append(dist.P2POp(dist.isend, slab[:pad].contiguous(), r - 1))
-        ops.append(dist.P2POp(dist.irecv, out[:lo], r - 1))
+        ops.append(("send", slab[:pad], r - 1))
+        ops.append(("recv", out[:lo], r - 1))
     if r < w - 1:
-        ops.append(dist.P2POp(dist.isend, slab[slab.shape[0] - pad:].contiguous(), r + 1))
-        ops.append(dist.P2POp(dist.irecv, out[lo + slab.shape[0]:], r + 1))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
+        ops.append(("send", slab[slab.shape[0] - pad:], r + 1))
+        ops.append(("recv", out[lo + slab.shape[0]:], r + 1))
+    _p2p(ops)
     return out, lo, hi
 
 
@@ -137,11 +178,11 @@ def allreduce_sum(t: torch.Tensor, ordered: bool = False) -> torch.Tensor:
     if w == 1:
         return t
     if not ordered:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return t
-    parts = [torch.empty_like(t) for _ in range(w)]
-    dist.all_gather(parts, t)
-    acc = torch.zeros_like(t)
+        return all_reduce(t)
+    src = t.detach().cpu() if (_staged() and t.is_cuda) else t
+    parts = [torch.empty_like(src) for _ in range(w)]
+    dist.all_gather(parts, src)
+    acc = torch.zeros_like(src)
     for p in parts:
         acc += p
     t.copy_(acc)
@@ -156,10 +197,10 @@ def fetch_planes(slab: torch.Tensor, spec: ShardSpec, z0: int, z1: int) -> torch
     nz = spec.global_shape[0]
     z0, z1 = max(0, int(z0)), min(nz, int(z1))
     out = torch.zeros((max(0, z1 - z0),) + tuple(slab.shape[1:]), dtype=slab.dtype, device=slab.device)
-    req = torch.tensor([z0, z1], dtype=torch.int64, device=slab.device if slab.is_cuda else "cpu")
     if w == 1:
         out.copy_(slab[z0 - spec.lo:z1 - spec.lo])
         return out
+    req = torch.tensor([z0, z1], dtype=torch.int64, device="cpu" if (_staged() or not slab.is_cuda) else slab.device)
     reqs = [torch.empty_like(req) for _ in range(w)]
     dist.all_gather(reqs, req)
     reqs = [tuple(int(v) for v in q.tolist()) for q in reqs]
@@ -169,35 +210,20 @@ def fetch_planes(slab: torch.Tensor, spec: ShardSpec, z0: int, z1: int) -> torch
         # what I send to peer: my planes inside peer's request
         a, b = max(reqs[peer][0], spec.lo), min(reqs[peer][1], spec.hi)
         if peer != r and a < b:
-            ops.append(dist.P2POp(dist.isend, slab[a - spec.lo:b - spec.lo].contiguous(), peer))
+            ops.append(("send", slab[a - spec.lo:b - spec.lo], peer))
         # what I receive from peer: peer's planes inside my request
         plo, phi = ranges[peer]
         a2, b2 = max(z0, plo), min(z1, phi)
         if peer != r and a2 < b2:
-            ops.append(dist.P2POp(dist.irecv, out[a2 - z0:b2 - z0], peer))
+            ops.append(("recv", out[a2 - z0:b2 - z0], peer))
     a, b = max(z0, spec.lo), min(z1, spec.hi)
     if a < b:
         out[a - z0:b - z0].copy_(slab[a - spec.lo:b - spec.lo])
-    if ops:
-        for q in dist.batch_isend_irecv(ops):
-            q.wait()
+    _p2p(ops)
     return out
 
 
 # ------------------------------------------------------------------ the sharded step
-@dataclass
-class ShardedStepState:
-    spec: ShardSpec
-    f_halo: torch.Tensor           # F slab + r halo planes (static within a scale)
-    halo_lo: int
-    halo_hi: int
-    m_window: Optional[object] = None  # voxreg-style window: padded tensor + [z0, z1)
-    m_z0: int = 0
-    m_z1: int = 0
-    window_fetches: int = 0
-    extra: dict = field(default_factory=dict)
-
-
 class ShardedStep:
     """The deformable step (registration.hpp:277-312) on one rank's z slab.
 
@@ -213,7 +239,7 @@ class ShardedStep:
         self.V = voxreg
         self.params = params or voxreg.LossParams()
         self.spec = spec
-        self.A = np.eye(3) if A is None else np.asarray(A, dtype=np.float64)
+        self.A = np.eye(3) if A is None else np.asarray(A, dtype=np.float64).reshape(3, 3)
         self.t = np.zeros(3) if t is None else np.asarray(t, dtype=np.float64)
         self.f = f_slab.to(torch.float32).contiguous()
         self.m = m_slab.to(torch.float32).contiguous()
@@ -223,6 +249,17 @@ class ShardedStep:
         self.margin = int(margin_planes)
         self.m_z0 = self.m_z1 = None
         self.window_fetches = 0
+        self.shifts = None
+
+    def reload(self, f_slab: torch.Tensor = None, m_slab: torch.Tensor = None):
+        """New image contents of the same geometry (a new pair, or a new scale's resampled
+        images): refreshes the F halo planes, drops the moving window and the moment shift."""
+        if f_slab is not None:
+            self.f.copy_(f_slab)
+            self.f_halo, self.hlo, self.hhi = halo_exchange(self.f, self.spec, self.pad)
+        if m_slab is not None:
+            self.m.copy_(m_slab)
+        self.m_z0 = self.m_z1 = None
         self.shifts = None
 
     # -- moving window ------------------------------------------------------------------
@@ -240,6 +277,19 @@ class ShardedStep:
         pad[2:-2, 2:-2, 2:-2].copy_(planes)
         self.m_pad, self.m_z0, self.m_z1 = pad, z0, z1
         self.window_fetches += 1
+
+    def _affine_z_range(self, z0: int, z1: int) -> Tuple[int, int]:
+        """Moving planes [a, b) the affine part of the warp maps lattice planes [z0, z1)
+        into (z_src = A[2] . x + t[2] is linear, so the slab's corners bound it); the
+        displacement's reach is covered by the margin and, past it, by the miss retry."""
+        nz = self.spec.global_shape[0]
+        zs = []
+        for zz in (axis_coord(z0, nz), axis_coord(z1 - 1, nz)):
+            for xx in (-1.0, 1.0):
+                for yy in (-1.0, 1.0):
+                    zn = self.A[2, 0] * xx + self.A[2, 1] * yy + self.A[2, 2] * zz + self.t[2]
+                    zs.append((zn + 1.0) * 0.5 * (nz - 1))
+        return int(math.floor(min(zs))) - 1, int(math.ceil(max(zs))) + 2
 
     def _window(self):
         from ._lib import Dims, ImageWindow
@@ -259,13 +309,14 @@ class ShardedStep:
         n_total = spec.global_shape[0] * ny * nx
         g_u = torch.empty_like(u_slab)
         if self.m_z0 is None:
-            self._ensure_window(spec.lo - lo - self.margin, spec.hi + hi + self.margin)
+            a, b = self._affine_z_range(spec.lo - lo, spec.hi + hi)
+            self._ensure_window(a - self.margin, b + self.margin)
         if p.kind == "lncc" and self.shifts is None:
             # the moment shift must be the same on every rank (it is part of the arithmetic)
             mm = torch.tensor([self.f.min(), -self.f.max(), self.m.min(), -self.m.max()], dtype=torch.float64,
                               device=self.f.device)
             if spec.world > 1:
-                dist.all_reduce(mm, op=dist.ReduceOp.MIN)
+                all_reduce(mm, op=dist.ReduceOp.MIN)
             v = mm.tolist()
             self.shifts = (0.5 * (v[0] - v[1]), 0.5 * (v[2] - v[3]))
         from ._lib import lib
@@ -286,7 +337,7 @@ class ShardedStep:
             # a miss on any rank means the step has to be redone everywhere (collective agreement)
             miss = self.ws.miss.to(torch.int64)
             if spec.world > 1:
-                dist.all_reduce(miss, op=dist.ReduceOp.MAX)
+                all_reduce(miss, op=dist.ReduceOp.MAX)
             if int(miss.item()) == 0:
                 break
             ext = torch.empty(2, dtype=torch.int64, device=self.f.device)
