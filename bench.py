@@ -47,6 +47,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel, nvox):
+    """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed --set full capture (profiles/traffic.json, tools/profile_summary.py),
+    scaled to this launch's voxel count; None when no capture of this kernel exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)[kernel]
+        return round(t["bytes_per_voxel"] * nvox), (f"{t['bytes_per_voxel']} B/voxel from profiles/"
+                                                     f"{t['round']}_full_*.txt ({t['workload']})")
+    except Exception:
+        return None, "no ncu capture"
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -400,6 +413,7 @@ def run_ours(args, rank, world, local_rank):
         dom = max(kern_ms, key=kern_ms.get)
         dom_bytes = (20 if "hist" in dom else 32) * nvox
     achieved = dom_bytes / (kern_ms[dom] * 1e-3) / 1e9
+    traffic = ncu_traffic(dom.split("+")[0], nvox)
     step_gbs = BYTES_PER_VOXEL[loss] * nvox / (ms_step * 1e-3) / 1e9
 
     # end to end through the public API with host buffers (pinned), H2D + step + D2H(loss)
@@ -416,7 +430,8 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "inputs (F, M, u, g_u) exceed the 126 MB L2; no flush between steps"},
         "loss": loss_val,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": None, "peak_kind": hbm_kind,
+                     "frac": round(achieved / hbm, 4), "traffic": traffic[0], "traffic_note": traffic[1],
+                     "peak_kind": hbm_kind,
                      "algorithmic_bytes_per_voxel": dom_bytes // nvox},
         "step_roofline": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / hbm, 4),
                           "bytes_per_voxel": BYTES_PER_VOXEL[loss]},

@@ -1,0 +1,614 @@
+// ffdp/voxreg.hpp -- C++ host mirror of the voxreg operator API over the C ABI (ffdp.h).
+//
+// A voxreg caller switches its hot path to the B200 by including this header instead of
+// voxreg/sampler.hpp, lncc.hpp and mi.hpp: the same names, argument meaning, ownership
+// (outputs are fresh owning containers; LnccState is consumed by the backward) and
+// exceptions (std::invalid_argument / std::logic_error / std::runtime_error) as the
+// reference, with the containers living in device memory (Volume3 / WarpField below hold
+// fp32 device buffers; from_host / to_host move them). Header-only; link libffdp.so and
+// libcudart. No fallback: every operation runs the sm_100a kernels or throws.
+//
+// Reference interfaces mirrored (file:line under proj/include/voxreg):
+//   Dims3, Vec3, Mat3, DomainBounds   geometry.hpp:10-109
+//   Volume3, WarpField                volume.hpp:18-84
+//   SamplerArgs, SamplerGradWant,
+//   SamplerGrads                      sampler.hpp:25-52
+//   fused_sample[_accumulate],
+//   fused_sample_backward             sampler.hpp:248-300
+//   LnccState, LnccResult,
+//   lncc_forward_fused,
+//   lncc_backward_fused               lncc.hpp:25-42, 144-280
+//   ParzenKernel, JointHistogram,
+//   MiStats, MiResult, mi_forward_*,
+//   mi_backward                       mi.hpp:28-165, 235-437
+//   the deformable step's loss/grad   registration.hpp:277-312 (DeformableStep)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ffdp.h"
+
+namespace ffdp {
+namespace voxreg {
+
+// ------------------------------------------------------------------ errors
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// Maps an ffdp_status onto the reference's exception types (ffdp.h header comment).
+inline void check(int status) {
+    if (status == FFDP_OK) return;
+    const std::string msg = ffdp_last_error();
+    switch (status) {
+        case FFDP_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case FFDP_LOGIC: throw std::logic_error(msg);
+        case FFDP_RUNTIME: throw std::runtime_error(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+inline void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ geometry (geometry.hpp:10-109)
+struct Dims3 {
+    std::int64_t nx = 0, ny = 0, nz = 0;
+    std::int64_t voxels() const { return nx * ny * nz; }
+    bool positive() const { return nx > 0 && ny > 0 && nz > 0; }
+    bool operator==(const Dims3& o) const { return nx == o.nx && ny == o.ny && nz == o.nz; }
+    bool operator!=(const Dims3& o) const { return !(*this == o); }
+    ffdp_dims c() const { return ffdp_dims{nx, ny, nz}; }
+};
+
+struct Vec3 {
+    double v[3] = {0, 0, 0};
+    double& operator[](int i) { return v[i]; }
+    double operator[](int i) const { return v[i]; }
+};
+
+struct Mat3 {
+    double m[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // row-major
+    static Mat3 identity() {
+        Mat3 a;
+        a.m[0] = a.m[4] = a.m[8] = 1.0;
+        return a;
+    }
+    double& operator()(int r, int c) { return m[3 * r + c]; }
+    double operator()(int r, int c) const { return m[3 * r + c]; }
+    bool finite() const {
+        for (double x : m)
+            if (!std::isfinite(x)) return false;
+        return true;
+    }
+};
+
+struct DomainBounds {
+    Vec3 lo{{-1, -1, -1}};
+    Vec3 hi{{1, 1, 1}};
+    static DomainBounds full() { return DomainBounds{}; }
+    bool valid() const {
+        for (int c = 0; c < 3; ++c)
+            if (!std::isfinite(lo[c]) || !std::isfinite(hi[c]) || !(lo[c] <= hi[c])) return false;
+        return true;
+    }
+};
+
+// ------------------------------------------------------------------ device containers (volume.hpp:18-84)
+template <typename T>
+class DeviceArray {
+  public:
+    DeviceArray() = default;
+    explicit DeviceArray(std::size_t n) : n_(n) {
+        if (n) check_cuda(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)), "cudaMalloc");
+    }
+    DeviceArray(const DeviceArray&) = delete;
+    DeviceArray& operator=(const DeviceArray&) = delete;
+    DeviceArray(DeviceArray&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+    DeviceArray& operator=(DeviceArray&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_, n_ = o.n_;
+            o.p_ = nullptr, o.n_ = 0;
+        }
+        return *this;
+    }
+    ~DeviceArray() { release(); }
+
+    T* data() { return p_; }
+    const T* data() const { return p_; }
+    std::size_t size() const { return n_; }
+    void zero(cudaStream_t s = nullptr) {
+        if (n_) check_cuda(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s), "cudaMemsetAsync");
+    }
+    void upload(const T* host, cudaStream_t s = nullptr) {
+        if (n_) check_cuda(cudaMemcpyAsync(p_, host, n_ * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    }
+    std::vector<T> download(cudaStream_t s = nullptr) const {
+        std::vector<T> h(n_);
+        if (n_) {
+            check_cuda(cudaMemcpyAsync(h.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+            check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        }
+        return h;
+    }
+
+  private:
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+    }
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+// Volume3<float> on the device: x-fastest, index (z*ny + y)*nx + x.
+struct Volume3 {
+    Dims3 dims;
+    Vec3 spacing{{1, 1, 1}};
+    Vec3 origin{{0, 0, 0}};
+    DeviceArray<float> data;
+
+    static Volume3 zeros(Dims3 d, cudaStream_t s = nullptr) {
+        if (!d.positive()) throw std::invalid_argument("Volume3: dims must be positive");
+        Volume3 v;
+        v.dims = d;
+        v.data = DeviceArray<float>(static_cast<std::size_t>(d.voxels()));
+        v.data.zero(s);
+        return v;
+    }
+    static Volume3 uninitialized(Dims3 d) {
+        if (!d.positive()) throw std::invalid_argument("Volume3: dims must be positive");
+        Volume3 v;
+        v.dims = d;
+        v.data = DeviceArray<float>(static_cast<std::size_t>(d.voxels()));
+        return v;
+    }
+    static Volume3 from_host(Dims3 d, const float* host, cudaStream_t s = nullptr) {
+        Volume3 v = uninitialized(d);
+        v.data.upload(host, s);
+        return v;
+    }
+    std::vector<float> to_host(cudaStream_t s = nullptr) const { return data.download(s); }
+    bool same_lattice(const Volume3& o) const { return dims == o.dims; }
+};
+
+// WarpField<float> on the device: 3 interleaved components per voxel.
+struct WarpField {
+    Dims3 dims;
+    DeviceArray<float> data;
+
+    static WarpField zeros(Dims3 d, cudaStream_t s = nullptr) {
+        WarpField w = uninitialized(d);
+        w.data.zero(s);
+        return w;
+    }
+    static WarpField uninitialized(Dims3 d) {
+        if (!d.positive()) throw std::invalid_argument("WarpField: dims must be positive");
+        WarpField w;
+        w.dims = d;
+        w.data = DeviceArray<float>(static_cast<std::size_t>(3 * d.voxels()));
+        return w;
+    }
+    static WarpField from_host(Dims3 d, const float* host, cudaStream_t s = nullptr) {
+        WarpField w = uninitialized(d);
+        w.data.upload(host, s);
+        return w;
+    }
+    std::vector<float> to_host(cudaStream_t s = nullptr) const { return data.download(s); }
+};
+
+// ------------------------------------------------------------------ sampler (sampler.hpp:25-300)
+struct SamplerArgs {
+    Mat3 A = Mat3::identity();
+    Vec3 t{{0, 0, 0}};
+    Vec3 S{{1, 1, 1}};  // diagonal rescale applied to the displacement
+    DomainBounds bounds = DomainBounds::full();
+
+    void validate() const {
+        if (!A.finite()) throw std::invalid_argument("SamplerArgs: non-finite affine");
+        for (int c = 0; c < 3; ++c)
+            if (!(S[c] > 0)) throw std::invalid_argument("SamplerArgs: S must be positive");
+        if (!bounds.valid()) throw std::invalid_argument("SamplerArgs: invalid bounds");
+    }
+    ffdp_sampler_args c() const {
+        ffdp_sampler_args a;
+        std::memcpy(a.A, A.m, sizeof(a.A));
+        for (int i = 0; i < 3; ++i) {
+            a.t[i] = t[i];
+            a.S[i] = S[i];
+            a.x_min[i] = bounds.lo[i];
+            a.x_max[i] = bounds.hi[i];
+        }
+        return a;
+    }
+};
+
+struct SamplerGradWant {
+    bool image = false;
+    bool warp = false;
+    bool affine = false;
+    bool translation = false;
+    int mask() const {
+        return (image ? FFDP_WANT_IMAGE : 0) | (warp ? FFDP_WANT_WARP : 0) | (affine ? FFDP_WANT_AFFINE : 0) |
+               (translation ? FFDP_WANT_TRANSLATION : 0);
+    }
+};
+
+struct SamplerGrads {
+    std::optional<Volume3> image;
+    std::optional<WarpField> warp;
+    std::optional<Mat3> affine;
+    std::optional<Vec3> translation;
+};
+
+inline ffdp_image_window window_of(const Volume3& img) {
+    return ffdp_image_window{img.data.data(), img.dims.c(), 0, img.dims.nz, 0};
+}
+
+inline Dims3 sampler_output_dims(const Volume3& img, const WarpField* u) { return u ? u->dims : img.dims; }
+
+// fused_sample (sampler.hpp:254-263)
+inline Volume3 fused_sample(const Volume3& img, const WarpField* u, const SamplerArgs& args,
+                            cudaStream_t s = nullptr) {
+    args.validate();
+    Volume3 out = Volume3::uninitialized(sampler_output_dims(img, u));
+    out.spacing = img.spacing;
+    out.origin = img.origin;
+    const ffdp_sampler_args a = args.c();
+    check(ffdp_sampler_fwd(window_of(img), u ? u->data.data() : nullptr, out.dims.c(), &a, out.data.data(), 0,
+                           nullptr, nullptr, s));
+    return out;
+}
+
+// fused_sample_accumulate (sampler.hpp:268-276); abs_contribution is a HOST double.
+inline void fused_sample_accumulate(const Volume3& img, const WarpField* u, const SamplerArgs& args, Volume3& out,
+                                    double* abs_contribution = nullptr, cudaStream_t s = nullptr) {
+    if (out.dims != sampler_output_dims(img, u))
+        throw std::invalid_argument("fused_sample_accumulate: output lattice mismatch");
+    args.validate();
+    const ffdp_sampler_args a = args.c();
+    std::optional<DeviceArray<double>> acc;
+    if (abs_contribution) {
+        acc.emplace(1);
+        acc->zero(s);
+    }
+    check(ffdp_sampler_fwd(window_of(img), u ? u->data.data() : nullptr, out.dims.c(), &a, out.data.data(), 1,
+                           acc ? acc->data() : nullptr, nullptr, s));
+    if (abs_contribution) *abs_contribution += acc->download(s)[0];
+}
+
+// fused_sample_backward (sampler.hpp:279-300)
+inline SamplerGrads fused_sample_backward(const Volume3& upstream, const Volume3& img, const WarpField* u,
+                                          const SamplerArgs& args, const SamplerGradWant& want,
+                                          cudaStream_t s = nullptr) {
+    const Dims3 od = sampler_output_dims(img, u);
+    if (upstream.dims != od) throw std::invalid_argument("fused_sample_backward: upstream lattice mismatch");
+    args.validate();
+    SamplerGrads g;
+    if (want.image) g.image = Volume3::zeros(img.dims, s);
+    if (want.warp) g.warp = WarpField::uninitialized(od);
+    std::optional<DeviceArray<double>> gat;
+    if (want.affine || want.translation) gat.emplace(12);
+    const ffdp_sampler_args a = args.c();
+    check(ffdp_sampler_bwd(upstream.data.data(), window_of(img), u ? u->data.data() : nullptr, od.c(), &a,
+                           want.mask(), want.image ? g.image->data.data() : nullptr,
+                           want.warp ? g.warp->data.data() : nullptr, gat ? gat->data() : nullptr, nullptr, s));
+    if (gat) {
+        const std::vector<double> h = gat->download(s);
+        if (want.affine) {
+            Mat3 m;
+            std::memcpy(m.m, h.data(), 9 * sizeof(double));
+            g.affine = m;
+        }
+        if (want.translation) g.translation = Vec3{{h[9], h[10], h[11]}};
+    }
+    return g;
+}
+
+// ------------------------------------------------------------------ LNCC (lncc.hpp:25-280)
+struct LnccState {
+    Dims3 dims;
+    DeviceArray<double> channels;  // 5 x voxels: mean_f, mean_m, mean_ff, mean_mm, mean_fm
+    int window = 7;
+    double epsilon = 1e-5;
+    std::int64_t voxels = 0;
+    const double* channel(int c) const { return channels.data() + c * voxels; }
+};
+
+struct LnccResult {
+    double loss = 0;
+    std::optional<Volume3> ncc_map;  // per-voxel n_i, filled only when requested
+    bool has_map = false;
+};
+
+inline void check_lncc(const Volume3& f, const Volume3& m, int window) {
+    if (!f.same_lattice(m)) throw std::invalid_argument("lncc: lattices differ");
+    if (window < 1 || window % 2 == 0) throw std::invalid_argument("lncc: window must be odd and >= 1");
+}
+
+inline ffdp_slab full_slab(std::int64_t nz) { return ffdp_slab{0, nz, 0, nz, nz}; }
+
+// lncc_forward_fused (lncc.hpp:144-205): loss = 1 - mean(A^2 / (B C + eps)).
+inline std::pair<LnccResult, LnccState> lncc_forward_fused(const Volume3& f, const Volume3& m, int window,
+                                                           double eps, bool want_map = false,
+                                                           cudaStream_t s = nullptr) {
+    check_lncc(f, m, window);
+    LnccState st;
+    st.dims = f.dims;
+    st.voxels = f.dims.voxels();
+    st.window = window;
+    st.epsilon = eps;
+    st.channels = DeviceArray<double>(static_cast<std::size_t>(5 * st.voxels));
+    LnccResult res;
+    if (want_map) res.ncc_map = Volume3::uninitialized(f.dims);
+    res.has_map = want_map;
+    DeviceArray<double> sum(1);
+    sum.zero(s);
+    check(ffdp_lncc_fwd(f.data.data(), m.data.data(), f.dims.c(), full_slab(f.dims.nz), window, eps,
+                        st.channels.data(), want_map ? res.ncc_map->data.data() : nullptr, sum.data(), s));
+    res.loss = 1.0 - sum.download(s)[0] / static_cast<double>(st.voxels);
+    return {std::move(res), std::move(st)};
+}
+
+// lncc_backward_fused (lncc.hpp:226-280): consumes `state` (rewritten as the gamma family).
+// Returns (dL/dF, dL/dM).
+inline std::pair<Volume3, Volume3> lncc_backward_fused(double upstream, LnccState& state, const Volume3& f,
+                                                       const Volume3& m, bool ants_approx,
+                                                       cudaStream_t s = nullptr) {
+    if (state.dims != f.dims || !f.same_lattice(m))
+        throw std::invalid_argument("lncc_backward_fused: lattice mismatch");
+    const double gi = -upstream / static_cast<double>(state.voxels);
+    check(ffdp_lncc_gamma(state.channels.data(), state.voxels, state.epsilon, gi, s));
+    Volume3 gf = Volume3::uninitialized(f.dims), gm = Volume3::uninitialized(f.dims);
+    check(ffdp_lncc_combine(state.channels.data(), f.dims.c(), full_slab(f.dims.nz), state.window,
+                            ants_approx ? 1 : 0, f.data.data(), m.data.data(), gf.data.data(), gm.data.data(), s));
+    return {std::move(gf), std::move(gm)};
+}
+
+// ------------------------------------------------------------------ MI (mi.hpp:28-437)
+class ParzenKernel {
+  public:
+    static ParzenKernel gaussian(int bins, double sigma_bins = 0.5) {
+        return ParzenKernel(FFDP_PARZEN_GAUSSIAN, bins, sigma_bins);
+    }
+    static ParzenKernel bspline3(int bins) { return ParzenKernel(FFDP_PARZEN_BSPLINE3, bins, 0.5); }
+    static ParzenKernel delta(int bins) { return ParzenKernel(FFDP_PARZEN_DELTA, bins, 0.5); }
+    int bins() const { return c_.bins; }
+    double support() const { return c_.radius; }
+    double support_bins() const { return c_.radius * c_.bins; }
+    const ffdp_parzen& c() const { return c_; }
+
+  private:
+    ParzenKernel(int kind, int bins, double sigma_bins) { check(ffdp_parzen_make(kind, bins, sigma_bins, &c_)); }
+    ffdp_parzen c_{};
+};
+
+inline double bin_center(int j, int bins) { return (static_cast<double>(j) + 0.5) / static_cast<double>(bins); }
+
+struct JointHistogram {
+    int bins = 0;
+    std::int64_t samples = 0;
+    double raw_joint_sum = 0;
+    std::vector<double> p_i, p_j;
+    std::vector<double> p_ij;  // row-major [m * bins + n]
+    std::vector<double> raw_joint;
+    std::vector<double> raw_marg_i, raw_marg_j;
+};
+
+struct MiStats {
+    std::uint64_t hist_writes = 0;
+    std::uint64_t kernel_evals = 0;
+};
+
+struct MiResult {
+    double mi = 0;
+    JointHistogram hist;
+    MiStats stats;
+};
+
+namespace detail {
+inline std::size_t table_len(int b) { return static_cast<std::size_t>(2 * b * b + 2 * b + 4); }
+
+// finalize_histogram + histogram_mi (mi.hpp:181-209) from the device raw accumulators.
+inline double hist_from_raw(const DeviceArray<double>& raw, int b, std::int64_t samples, JointHistogram& h,
+                            cudaStream_t s) {
+    DeviceArray<double> table(table_len(b));
+    check(ffdp_mi_finalize(raw.data(), b, -1.0, table.data(), s));
+    const std::vector<double> t = table.download(s);
+    const std::vector<double> r = raw.download(s);
+    const std::size_t bb = static_cast<std::size_t>(b) * b;
+    h.bins = b;
+    h.samples = samples;
+    h.p_ij.assign(t.begin(), t.begin() + bb);
+    h.p_i.assign(t.begin() + bb, t.begin() + bb + b);
+    h.p_j.assign(t.begin() + bb + b, t.begin() + bb + 2 * b);
+    h.raw_joint_sum = t[2 * bb + 2 * b];
+    h.raw_joint.assign(r.begin(), r.begin() + bb);
+    h.raw_marg_i.assign(r.begin() + bb, r.begin() + bb + b);
+    h.raw_marg_j.assign(r.begin() + bb + b, r.end());
+    return t[2 * bb + 2 * b + 1];
+}
+
+inline MiResult mi_forward(const Volume3& i, const Volume3& j, int bins, const ParzenKernel& k, bool approx,
+                           cudaStream_t s) {
+    if (!i.same_lattice(j)) throw std::invalid_argument("mi: lattices differ");
+    if (bins < 2) throw std::invalid_argument("mi: bins must be >= 2");
+    if (bins != k.bins()) throw std::invalid_argument("mi: kernel bin count differs from bins");
+    const std::int64_t n = i.dims.voxels();
+    DeviceArray<double> raw(static_cast<std::size_t>(bins * bins + 2 * bins));
+    raw.zero(s);
+    DeviceArray<std::int32_t> bad(1);
+    bad.zero(s);
+    std::uint64_t stats[2] = {0, 0};
+    check(ffdp_mi_hist(i.data.data(), j.data.data(), n, &k.c(), approx ? 1 : 0, raw.data(), bad.data(), stats, s));
+    if (bad.download(s)[0]) throw std::invalid_argument("mi: intensities must lie in [0,1]");
+    MiResult r;
+    r.mi = hist_from_raw(raw, bins, n, r.hist, s);
+    r.stats.hist_writes = stats[0];
+    r.stats.kernel_evals = stats[1];
+    return r;
+}
+
+// mi_backward_impl (mi.hpp:361-421): no sample-count check (global histograms).
+inline std::pair<Volume3, Volume3> mi_backward_impl(double upstream, const Volume3& i, const Volume3& j,
+                                                    const JointHistogram& h, const ParzenKernel& k,
+                                                    cudaStream_t s) {
+    if (!i.same_lattice(j)) throw std::invalid_argument("mi_backward: lattices differ");
+    const int b = h.bins;
+    std::vector<double> rawh(h.raw_joint);
+    rawh.insert(rawh.end(), h.raw_marg_i.begin(), h.raw_marg_i.end());
+    rawh.insert(rawh.end(), h.raw_marg_j.begin(), h.raw_marg_j.end());
+    if (rawh.size() != static_cast<std::size_t>(b * b + 2 * b))
+        throw std::invalid_argument("mi_backward: malformed histogram");
+    DeviceArray<double> raw(rawh.size());
+    raw.upload(rawh.data(), s);
+    DeviceArray<double> table(table_len(b));
+    check(ffdp_mi_finalize(raw.data(), b, upstream, table.data(), s));
+    Volume3 gi = Volume3::uninitialized(i.dims), gj = Volume3::uninitialized(i.dims);
+    check(ffdp_mi_bwd(i.data.data(), j.data.data(), i.dims.voxels(), &k.c(), table.data(), gi.data.data(),
+                      gj.data.data(), s));
+    check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");  // raw/table are freed on return
+    return {std::move(gi), std::move(gj)};
+}
+}  // namespace detail
+
+// mi_forward_exact (mi.hpp:235-272)
+inline MiResult mi_forward_exact(const Volume3& i, const Volume3& j, int bins, const ParzenKernel& k,
+                                 cudaStream_t s = nullptr) {
+    return detail::mi_forward(i, j, bins, k, false, s);
+}
+
+// mi_forward_approx (mi.hpp:285-354)
+inline MiResult mi_forward_approx(const Volume3& i, const Volume3& j, int bins, const ParzenKernel& k,
+                                  cudaStream_t s = nullptr) {
+    return detail::mi_forward(i, j, bins, k, true, s);
+}
+
+// mi_backward (mi.hpp:430-437): gradients w.r.t. both images given upstream = dL/dMI.
+inline std::pair<Volume3, Volume3> mi_backward(double upstream, const Volume3& i, const Volume3& j,
+                                               const JointHistogram& h, const ParzenKernel& k,
+                                               cudaStream_t s = nullptr) {
+    if (i.dims.voxels() != h.samples) throw std::invalid_argument("mi_backward: histogram sample count mismatch");
+    return detail::mi_backward_impl(upstream, i, j, h, k, s);
+}
+
+// ------------------------------------------------------------------ the fused deformable step
+enum class LossKind { lncc, mi };
+
+// LossParams (registration.hpp:33-46) restricted to the fused step's losses.
+struct LossParams {
+    LossKind kind = LossKind::lncc;
+    int window = 7;
+    double epsilon = 1e-5;
+    bool ants_approx = true;
+    int bins = 32;
+    bool mi_bspline_kernel = true;
+    bool mi_approx_forward = false;
+};
+
+struct StepResult {
+    double loss = 0;
+    std::int32_t window_misses = 0;
+};
+
+// One deformable-step evaluation (registration.hpp:277-312 at H = 1): moved =
+// fused_sample(M, u; A, t) -> LNCC (ANTs) or Mattes MI -> g_u = fused_sample_backward(
+// dL/dmoved, want warp), as one fused kernel (LNCC) or hist + finalize + grad (MI).
+// Built once per scale (M is static within a scale, registration.hpp:249,270): holds the
+// zero-bordered copy of M and all workspace, so step() allocates nothing and, with
+// sync = false, is capturable in a CUDA graph.
+class DeformableStep {
+  public:
+    DeformableStep(const Volume3& fixed, const Volume3& moving, const LossParams& p, cudaStream_t s = nullptr)
+        : f_(fixed.data.data()), dims_(fixed.dims), p_(p), stream_(s) {
+        if (!fixed.same_lattice(moving))
+            throw std::invalid_argument("DeformableStep: F and M must share a lattice (registration.hpp:268-270)");
+        if (p.kind == LossKind::lncc && !p.ants_approx)
+            throw std::invalid_argument("DeformableStep: the fused LNCC step implements the ANTs backward");
+        if (p.kind == LossKind::mi && p.mi_approx_forward)
+            throw std::invalid_argument("DeformableStep: the fused MI step uses the exact Parzen forward");
+        const Dims3 d = dims_;
+        m_pad_ = DeviceArray<float>(static_cast<std::size_t>((d.nx + 4) * (d.ny + 4) * (d.nz + 4)));
+        check(ffdp_pad_window(moving.data.data(), d.c(), 0, d.nz, m_pad_.data(), s));
+        miss_ = DeviceArray<std::int32_t>(1);
+        sum_ = DeviceArray<double>(1);
+        if (p.kind == LossKind::lncc) {
+            DeviceArray<float> mm(2);
+            check(ffdp_minmax(fixed.data.data(), d.voxels(), mm.data(), s));
+            std::vector<float> a = mm.download(s);
+            shift_f_ = 0.5f * (a[0] + a[1]);
+            check(ffdp_minmax(moving.data.data(), d.voxels(), mm.data(), s));
+            a = mm.download(s);
+            shift_m_ = 0.5f * (a[0] + a[1]);
+        } else {
+            kernel_.emplace(p.mi_bspline_kernel ? ParzenKernel::bspline3(p.bins) : ParzenKernel::gaussian(p.bins));
+            raw_ = DeviceArray<double>(static_cast<std::size_t>(p.bins * p.bins + 2 * p.bins));
+            table_ = DeviceArray<double>(detail::table_len(p.bins));
+            scratch_ = DeviceArray<unsigned char>(static_cast<std::size_t>(ffdp_step_mi_workspace_bytes(p.bins)));
+        }
+    }
+
+    // g_u (same lattice as F) is overwritten. With sync = false nothing is read back
+    // (loss() / misses() read it later).
+    StepResult step(const WarpField& u, const SamplerArgs& args, WarpField& g_u, bool sync = true) {
+        if (u.dims != dims_ || g_u.dims != dims_) throw std::invalid_argument("sampler: warp lattice mismatch");
+        args.validate();
+        const ffdp_sampler_args a = args.c();
+        const ffdp_image_window w{m_pad_.data(), dims_.c(), 0, dims_.nz, 2};
+        miss_.zero(stream_);
+        if (p_.kind == LossKind::lncc) {
+            sum_.zero(stream_);
+            check(ffdp_step_lncc(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, p_.window, p_.epsilon,
+                                 -1.0 / static_cast<double>(dims_.voxels()), shift_f_, shift_m_, g_u.data.data(),
+                                 sum_.data(), miss_.data(), stream_));
+        } else {
+            check(ffdp_step_mi(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, &kernel_->c(), raw_.data(),
+                               table_.data(), g_u.data.data(), scratch_.data(), miss_.data(), stream_));
+        }
+        StepResult r;
+        if (sync) {
+            r.loss = loss();
+            r.window_misses = miss_.download(stream_)[0];
+        }
+        return r;
+    }
+
+    double loss() const {
+        if (p_.kind == LossKind::lncc) return 1.0 - sum_.download(stream_)[0] / static_cast<double>(dims_.voxels());
+        const int b = p_.bins;
+        double v = 0;
+        check_cuda(cudaMemcpyAsync(&v, table_.data() + 2 * b * b + 2 * b + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                                   stream_),
+                   "D2H");
+        check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+        return -v;
+    }
+
+    const Dims3& dims() const { return dims_; }
+
+  private:
+    const float* f_;
+    Dims3 dims_;
+    LossParams p_;
+    cudaStream_t stream_;
+    DeviceArray<float> m_pad_;
+    DeviceArray<std::int32_t> miss_;
+    DeviceArray<double> sum_, raw_, table_;
+    DeviceArray<unsigned char> scratch_;
+    std::optional<ParzenKernel> kernel_;
+    float shift_f_ = 0, shift_m_ = 0;
+};
+
+}  // namespace voxreg
+}  // namespace ffdp

@@ -55,9 +55,32 @@ def build_oracle(verbose: bool = False) -> None:
         subprocess.run(["make", "-s", "-C", od, "ref"], check=True)
 
 
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_voxreg_api.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_voxreg_api")
+
+
+def build_cpp_tests(force: bool = False, verbose: bool = False) -> str:
+    """The C++ parity suite of the host mirror (include/ffdp/voxreg.hpp), linked against
+    libffdp.so and the oracle (test infrastructure) with $ORIGIN-relative rpaths."""
+    cuda = os.path.dirname(os.path.dirname(nvcc()))
+    deps = [CPP_TEST_SRC, os.path.join(ROOT, "include", "ffdp", "voxreg.hpp"), os.path.join(ROOT, "include", "ffdp.h"),
+            LIB, os.path.join(ROOT, "oracle", "libffdp_oracle.so")]
+    if force or _stale(CPP_TEST_BIN, deps):
+        cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"),
+               "-I" + os.path.join(cuda, "include"), CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+               "-L" + HERE, "-L" + os.path.join(ROOT, "oracle"), "-L" + os.path.join(cuda, "lib64"),
+               "-lffdp", "-lffdp_oracle", "-lcudart",
+               "-Wl,-rpath,$ORIGIN/../../paper_2509_25044_b200:$ORIGIN/../../oracle:" + os.path.join(cuda, "lib64")]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return CPP_TEST_BIN
+
+
 def build_all(verbose: bool = False) -> None:
     build_lib(verbose=verbose)
     build_oracle(verbose=verbose)
+    build_cpp_tests(verbose=verbose)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,25 @@
+"""The C++ host mirror (include/ffdp/voxreg.hpp) through its own parity suite
+(tests/cpp/test_voxreg_api.cpp, built by paper_2509_25044_b200/build.py)."""
+import os
+import subprocess
+
+import pytest
+
+from paper_2509_25044_b200 import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_cpp_mirror_compiles_against_the_abi():
+    """The header-only mirror compiles (-Wall) and links against libffdp.so here (no GPU)."""
+    b = build.build_cpp_tests()
+    assert os.path.exists(b)
+
+
+@pytest.mark.gpu
+def test_cpp_mirror_parity_suite():
+    b = build.build_cpp_tests()
+    r = subprocess.run([b], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
