@@ -11,9 +11,10 @@
 // Work unit: a warp covers 32 consecutive x voxels of 4 consecutive rows (needs the
 // zero-bordered moving image, ffdp_pad_window; dense images use mi.cu's scalar path).
 // Histogram: 16 joint products per voxel rounded to fixed point by one FFMA against
-// the 1.5*2^23 magic constant and added with native shared u32 atomics; every 1024
-// voxels the CTA folds the u32 counters into a u64 shared copy (no overflow), and at
-// the end into the global u64 histogram. Integer sums: deterministic. The marginals
+// the 1.5*2^23 magic constant and added with native shared u32 atomics into lane-private
+// copies; every 1024 voxels per copy the CTA folds the copies into a u64 shared
+// histogram (the scale keeps every counter below 2^32 in between), and at the end into
+// the global u64 histogram. Integer sums: deterministic. The marginals
 // are not accumulated here: finalize_histogram derives p_i, p_j from the joint
 // (mi.hpp:181-196), so the fused step needs only the B*B joint payload.
 #include <algorithm>
@@ -23,7 +24,7 @@
 namespace ffdp {
 namespace mstep {
 
-constexpr int NT = 256;  // 8 warps x 128 voxels -> 1024 voxels per histogram fold
+constexpr int NT = 256;  // pass 2: 8 warps x 128 voxels per CTA iteration
 
 struct Params {
     Geom g;
@@ -141,23 +142,53 @@ __device__ __forceinline__ void unit_cells(const Params& P, const Unit& w, const
 }
 
 // ------------------------------------------------------------------ pass 1
+// Histogram privatisation. The lanes of a warp are x-neighbours, so they often fall in the
+// same bins, and shared atomics from several lanes of one instruction to the same address
+// serialise (8 lanes on one address cost ~8x a conflict-free instruction). Lane l
+// therefore adds into copy l % HCOPY of the counters; copies are HSTRIDE words apart with
+// HSTRIDE = 1 (mod 32), so lanes adding to the same bin of their own copies hit distinct
+// banks. Each copy only takes the voxels of HNT / HCOPY threads, which sets the fold
+// interval.
+#ifndef FFDP_MI_HIST_NT
+#define FFDP_MI_HIST_NT 1024
+#endif
+#ifndef FFDP_MI_HIST_COPIES
+#define FFDP_MI_HIST_COPIES 32
+#endif
+constexpr int HNT = FFDP_MI_HIST_NT;
+constexpr int HCOPY = FFDP_MI_HIST_COPIES;
+// voxels one copy takes per CTA iteration, and iterations between folds: a voxel adds
+// at most max(kappa)^2 * scale < 2^22 to one counter (B-spline (2/3)^2 * 2^23, gaussian
+// 0.64 * 2^22, delta 2^21), so 1024 voxels per copy per fold keep counters below 2^32.
+constexpr int HVOX_PER_COPY_ITER = (HNT / HCOPY) * 4;
+constexpr int HFOLD_ITERS = 1024 / HVOX_PER_COPY_ITER > 0 ? 1024 / HVOX_PER_COPY_ITER : 1;
+
+__host__ __device__ constexpr int hist_ld(int B) { return B + 2 * PAD; }
+__host__ __device__ constexpr int hist_stride(int B) {
+    return ((hist_ld(B) * hist_ld(B) + 31) / 32) * 32 + (32 / HCOPY);
+}
+constexpr size_t kMaxHistSmem = 227 * 1024;
+inline size_t hist_smem_bytes(int B) {
+    return sizeof(unsigned long long) * B * B + sizeof(uint32_t) * (size_t)HCOPY * hist_stride(B);
+}
+
 template <bool BSPLINE, bool FULLWIN>
-__global__ void __launch_bounds__(NT) k_step_mi_hist(const Params P) {
+__global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int B = P.p.bins;
-    const int LD = B + 2 * PAD;
-    const int nt = LD * LD;
-    unsigned long long* s64 = reinterpret_cast<unsigned long long*>(smem);
-    uint32_t* s32 = reinterpret_cast<uint32_t*>(smem + sizeof(unsigned long long) * nt);
-    for (int i = threadIdx.x; i < nt; i += NT) {
-        s64[i] = 0ull;
-        s32[i] = 0u;
-    }
+    const int LD = hist_ld(B);
+    const int CS = hist_stride(B);
+    unsigned long long* s64 = reinterpret_cast<unsigned long long*>(smem);  // interior B x B
+    uint32_t* s32 = reinterpret_cast<uint32_t*>(smem + sizeof(unsigned long long) * B * B);
+    for (int i = threadIdx.x; i < B * B; i += HNT) s64[i] = 0ull;
+    for (int i = threadIdx.x; i < HCOPY * CS; i += HNT) s32[i] = 0u;
     __syncthreads();
     int miss = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t stride = (int64_t)gridDim.x * (NT / 32);
-    for (int64_t base = (int64_t)blockIdx.x * (NT / 32); base < P.nunits; base += stride) {
+    uint32_t* mine = s32 + (lane % HCOPY) * CS + PAD * LD + PAD;
+    const int64_t stride = (int64_t)gridDim.x * (HNT / 32);
+    int iter = 0;
+    for (int64_t base = (int64_t)blockIdx.x * (HNT / 32); base < P.nunits; base += stride) {
         const int64_t unit = base + warp;
         if (unit < P.nunits) {
             const Unit w = unit_coords(P, (uint32_t)unit, lane);
@@ -169,76 +200,50 @@ __global__ void __launch_bounds__(NT) k_step_mi_hist(const Params P) {
             Corners cr[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
-            BS4 bI[4], bJ[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+                BS4 bI, bJ;
                 if (BSPLINE) {
-                    bI[k] = bspline_bins<false>(ff[k], B);
-                    bJ[k] = bspline_bins<false>(interp(cr[k], c[k]), B);
+                    bI = bspline_bins<false>(ff[k], B);
+                    bJ = bspline_bins<false>(interp(cr[k], c[k]), B);
                 } else {
-                    bI[k] = generic_bins<false>(P.p, (double)ff[k]);
-                    bJ[k] = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
+                    bI = generic_bins<false>(P.p, (double)ff[k]);
+                    bJ = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
                 }
                 const float sc = ok[k] ? P.fix_scale : 0.0f;  // voxels outside the lattice add nothing
 #pragma unroll
-                for (int b = 0; b < 4; ++b) bJ[k].k[b] *= sc;
-            }
-            const int mlo = min(min(bI[0].m_lo, bI[1].m_lo), min(bI[2].m_lo, bI[3].m_lo));
-            const int mhi = max(max(bI[0].m_lo, bI[1].m_lo), max(bI[2].m_lo, bI[3].m_lo));
-            const int nlo = min(min(bJ[0].m_lo, bJ[1].m_lo), min(bJ[2].m_lo, bJ[3].m_lo));
-            const int nhi = max(max(bJ[0].m_lo, bJ[1].m_lo), max(bJ[2].m_lo, bJ[3].m_lo));
-            if (mhi - mlo <= 1 && nhi - nlo <= 1) {
-                // the four footprints fit one 5 x 5 window: aggregate in registers, then 25
-                // atomics instead of 64 (neighbouring voxels share bins)
-                float wv[25];
+                for (int b = 0; b < 4; ++b) bJ.k[b] *= sc;
+                uint32_t* h = mine + bI.m_lo * LD + bJ.m_lo;
 #pragma unroll
-                for (int i = 0; i < 25; ++i) wv[i] = 0.0f;
+                for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const bool dm = bI[k].m_lo != mlo, dn = bJ[k].m_lo != nlo;
-                    const float a5[5] = {dm ? 0.0f : bI[k].k[0], dm ? bI[k].k[0] : bI[k].k[1],
-                                         dm ? bI[k].k[1] : bI[k].k[2], dm ? bI[k].k[2] : bI[k].k[3],
-                                         dm ? bI[k].k[3] : 0.0f};
-                    const float b5[5] = {dn ? 0.0f : bJ[k].k[0], dn ? bJ[k].k[0] : bJ[k].k[1],
-                                         dn ? bJ[k].k[1] : bJ[k].k[2], dn ? bJ[k].k[2] : bJ[k].k[3],
-                                         dn ? bJ[k].k[3] : 0.0f};
-#pragma unroll
-                    for (int r = 0; r < 5; ++r)
-#pragma unroll
-                        for (int cc = 0; cc < 5; ++cc) wv[5 * r + cc] = fmaf(a5[r], b5[cc], wv[5 * r + cc]);
-                }
-                uint32_t* h = s32 + (mlo + PAD) * LD + (nlo + PAD);
-#pragma unroll
-                for (int r = 0; r < 5; ++r)
-#pragma unroll
-                    for (int cc = 0; cc < 5; ++cc)
-                        // round-to-nearest through the fp64 magic constant (sums of 4 voxels exceed
-                        // the fp32 magic range); no conversion-pipe instruction
-                        atomicAdd(h + r * LD + cc,
-                                  (uint32_t)__double2loint((double)wv[5 * r + cc] + 6755399441055744.0));
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    uint32_t* h = s32 + (bI[k].m_lo + PAD) * LD + (bJ[k].m_lo + PAD);
-#pragma unroll
-                    for (int a = 0; a < 4; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-                            // one voxel stays below 2^22 at the chosen scale: fp32 magic rounding
-                            atomicAdd(h + a * LD + b, (uint32_t)(__float_as_int(fmaf(bI[k].k[a], bJ[k].k[b],
-                                                                                     12582912.0f)) - 0x4B400000));
-                }
+                    for (int b = 0; b < 4; ++b)
+                        // round to nearest through the fp32 magic constant (products < 2^22)
+                        atomicAdd(h + a * LD + b,
+                                  (uint32_t)(__float_as_int(fmaf(bI.k[a], bJ.k[b], 12582912.0f)) - 0x4B400000));
             }
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < nt; i += NT) {
-            s64[i] += s32[i];
-            s32[i] = 0u;
+        if (++iter == HFOLD_ITERS || base + stride >= P.nunits) {
+            // fold the interior B x B counters of every copy (the pad counters take the
+            // weight of bins outside [0, B), which the reference ignores: they may wrap,
+            // they are never read)
+            iter = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < B * B; i += HNT) {
+                const int q = (i / B + PAD) * LD + (i % B) + PAD;
+                unsigned long long acc = 0ull;
+#pragma unroll 8
+                for (int cp = 0; cp < HCOPY; ++cp) {
+                    acc += s32[cp * CS + q];
+                    s32[cp * CS + q] = 0u;
+                }
+                s64[i] += acc;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
-    for (int i = threadIdx.x; i < B * B; i += NT) {
-        const unsigned long long v = s64[(i / B + PAD) * LD + (i % B) + PAD];
+    for (int i = threadIdx.x; i < B * B; i += HNT) {
+        const unsigned long long v = s64[i];
         if (v) atomicAdd(&P.hist[i], v);
     }
     const unsigned anym = __ballot_sync(0xffffffffu, miss);
@@ -318,8 +323,9 @@ __global__ void k_hist_to_raw(const unsigned long long* h, int n, double inv_sca
 // (the caller then uses the scalar kernels of mi.cu).
 bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                           const ffdp_parzen& k) {
-    // zero-bordered moving image, 32-bit unit indices and in-plane offsets
-    return m.pad == 2 && k.bins <= 64 && (int64_t)d.nx * d.ny < (1LL << 31) &&
+    // zero-bordered moving image, lane-private histogram copies within shared memory,
+    // 32-bit unit indices and in-plane offsets
+    return m.pad == 2 && mstep::hist_smem_bytes(k.bins) <= mstep::kMaxHistSmem && (int64_t)d.nx * d.ny < (1LL << 31) &&
            ((d.nx + 31) / 32) * ((d.ny + 3) / 4) * (s.z_end - s.z_begin) < (1LL << 31);
 }
 
@@ -361,19 +367,26 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     cudaMemsetAsync(h, 0, sizeof(unsigned long long) * B * B, st);
     P.hist = h;
     P.miss = miss;
-    const size_t smem = (sizeof(unsigned long long) + sizeof(uint32_t)) * (B + 2 * PAD) * (B + 2 * PAD);
-    const int64_t chunks = (P.nunits + NT / 32 - 1) / (NT / 32);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, 6LL * num_sms()));
+    const size_t smem = hist_smem_bytes(B);
+    static bool attr_set = false;  // opt in to > 48 KB dynamic shared memory, once
+    if (!attr_set) {
+        for (auto fn : {k_step_mi_hist<true, true>, k_step_mi_hist<true, false>, k_step_mi_hist<false, true>,
+                        k_step_mi_hist<false, false>})
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
+        attr_set = true;
+    }
+    const int64_t chunks = (P.nunits + HNT / 32 - 1) / (HNT / 32);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)num_sms()));
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool bs = k.kind == FFDP_PARZEN_BSPLINE3;
     if (bs && full)
-        k_step_mi_hist<true, true><<<grid, NT, smem, st>>>(P);
+        k_step_mi_hist<true, true><<<grid, HNT, smem, st>>>(P);
     else if (bs)
-        k_step_mi_hist<true, false><<<grid, NT, smem, st>>>(P);
+        k_step_mi_hist<true, false><<<grid, HNT, smem, st>>>(P);
     else if (full)
-        k_step_mi_hist<false, true><<<grid, NT, smem, st>>>(P);
+        k_step_mi_hist<false, true><<<grid, HNT, smem, st>>>(P);
     else
-        k_step_mi_hist<false, false><<<grid, NT, smem, st>>>(P);
+        k_step_mi_hist<false, false><<<grid, HNT, smem, st>>>(P);
     k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
     if (!ws) scratch_free(h, st);
     return check_launch("step_mi_hist");

@@ -1,4 +1,8 @@
-for v in ty8 ty16 ty8 ty16; do
-  FFDP_LIB=$PWD/exp/libffdp_$v.so python bench.py --no-cpu --steps 50 > gpurun_out/ab_$v.json 2>&1
-  python -c "import json; d=json.load(open('gpurun_out/ab_$v.json')); print('$v', d['value'], d['kernel_ms'], 'lncc', d['secondary']['value'], d['secondary']['kernel_ms'])"
+# A/B of library variants (exp/libffdp_<v>.so) on the bench: gpu_ab.sh "<variants>" [bench args]
+V=$1; shift
+for rep in 1 2; do
+for v in $V; do
+  FFDP_LIB=$PWD/exp/libffdp_$v.so python bench.py --no-cpu --no-secondary "$@" > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
+  python -c "import json; d=json.load(open('gpurun_out/ab_$v.json')); print('$v', d['value'], d['kernel_ms'])" || tail -3 gpurun_out/ab_$v.err
+done
 done
