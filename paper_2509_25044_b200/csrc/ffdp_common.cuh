@@ -147,22 +147,19 @@ __device__ __forceinline__ double interp_f64(const Corners& k, const Cell& c) {
 // ------------------------------------------------------------------ fast row sampler
 // Conversion-free cell assignment (the f64->int / f64->f32 conversions issue at a
 // quarter of the FP64 rate on sm_100). t = f + 1.5*2^20 places floor(f) + 2^19 in
-// mantissa bits 32..51 and frac(f) in units of 2^-32 in the low word (|f| < 2^19), so
-// the 1e-9 face snap of cell_assign (resample.hpp:32-43) becomes integer compares on
-// the low word: frac < 1e-9 <=> lo <= 4, 1 - frac < 1e-9 <=> lo >= 2^32 - 4.
+// mantissa bits 32..51 and frac(f) in units of 2^-32 in the low word (|f| < 2^19).
+// The 1e-9 face snap of cell_assign (resample.hpp:32-43) is folded into the constant:
+// adding 4 more units of 2^-32 carries fractions within 4 * 2^-32 (< 1e-9) of the upper
+// face into the next cell with a low word < 4, and fractions within 4 units of the lower
+// face leave a low word <= 8; both give frac = 0 after the 23-bit truncation below, and
+// everywhere else the extra 4 units only move frac by at most one 2^-23 step.
 __device__ __forceinline__ void cell_fix(double f, int32_t& i0, float& frac) {
-    const double t = f + 1572864.0;
-    uint32_t fr = (uint32_t)__double2loint(t);
+    const double t = f + 0x1.8000000000004p+20;  // 1.5 * 2^20 + 4 * 2^-32
+    const uint32_t lo = (uint32_t)__double2loint(t);
     const int32_t hi = __double2hiint(t);
-    int32_t ip = (hi & 0xFFFFF) - 0x80000;
-    if (fr + 4u <= 8u) {  // within 1e-9 of a face (rare): snap onto it
-        ip += fr > 4u ? 1 : 0;
-        fr = 0u;
-    }
-    // |f| >= 2^19 (exponent of t off): far outside any lattice -> fully zero padded
-    if ((uint32_t)(hi - 0x41300000) >= 0x100000u) ip = -4;
-    i0 = ip;
-    frac = __uint_as_float(0x3F800000u | (fr >> 9)) - 1.0f;
+    // |f| >= 2^19 (exponent of t off) or NaN: far outside any lattice -> fully zero padded
+    i0 = (uint32_t)(hi - 0x41300000) < 0x100000u ? hi - 0x41380000 : -4;
+    frac = __uint_as_float(0x3F800000u | (lo >> 9)) - 1.0f;
 }
 
 // Division by a runtime constant without an integer divide (round-up multiplier,

@@ -49,8 +49,9 @@ struct BS4 {
     float k[4], w[4];
 };
 
+// c6: 1/6, or 1/6 times the histogram fixed-point scale (folded into the weights).
 template <bool OMEGA>
-__device__ __forceinline__ BS4 bspline_bins(float v, int B) {
+__device__ __forceinline__ BS4 bspline_bins(float v, int B, float c6 = 1.0f / 6.0f) {
     BS4 r;
     const float s = fmaf(v, (float)B, -0.5f);
     const float fl = floorf(s);
@@ -60,7 +61,6 @@ __device__ __forceinline__ BS4 bspline_bins(float v, int B) {
     r.m_lo = min(max((__float_as_int(fl + 12582912.0f) - 0x4B400000) - 1, -2), B - 2);
     const float q = 1.0f - ph;
     const float p2 = ph * ph, p3 = p2 * ph, q2 = q * q;
-    const float c6 = 1.0f / 6.0f;
     r.k[0] = q2 * q * c6;
     r.k[1] = fmaf(3.0f, p3, fmaf(-6.0f, p2, 4.0f)) * c6;
     r.k[2] = fmaf(-3.0f, p3, fmaf(3.0f, p2, fmaf(3.0f, ph, 1.0f))) * c6;
@@ -203,16 +203,16 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 BS4 bI, bJ;
+                const float sc = ok[k] ? P.fix_scale : 0.0f;  // voxels outside the lattice add nothing
                 if (BSPLINE) {
                     bI = bspline_bins<false>(ff[k], B);
-                    bJ = bspline_bins<false>(interp(cr[k], c[k]), B);
+                    bJ = bspline_bins<false>(interp(cr[k], c[k]), B, sc * (1.0f / 6.0f));
                 } else {
                     bI = generic_bins<false>(P.p, (double)ff[k]);
                     bJ = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
-                }
-                const float sc = ok[k] ? P.fix_scale : 0.0f;  // voxels outside the lattice add nothing
 #pragma unroll
-                for (int b = 0; b < 4; ++b) bJ.k[b] *= sc;
+                    for (int b = 0; b < 4; ++b) bJ.k[b] *= sc;
+                }
                 uint32_t* h = mine + bI.m_lo * LD + bJ.m_lo;
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
