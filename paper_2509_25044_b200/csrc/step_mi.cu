@@ -10,8 +10,8 @@
 //
 // Work unit: a warp covers 32 consecutive x voxels of 4 consecutive rows (needs the
 // zero-bordered moving image, ffdp_pad_window; dense images use mi.cu's scalar path).
-// Histogram: 16 joint products per voxel rounded to fixed point by one FFMA against
-// the 1.5*2^23 magic constant and added with native shared u32 atomics into lane-private
+// Histogram: 16 joint products per voxel rounded to fixed point by one denormal FMUL
+// (the bits of the product are the integer) and added with native shared u32 atomics into lane-private
 // copies; every 1024 voxels per copy the CTA folds the copies into a u64 shared
 // histogram (the scale keeps every counter below 2^32 in between), and at the end into
 // the global u64 histogram. Integer sums: deterministic. The marginals
@@ -202,25 +202,29 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
             for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+                // Fixed point by a denormal product: with the weights pre-scaled by 2^-63 and
+                // scale * 2^-86, kI * kJ lands at (scale * kI * kJ) * 2^-149, whose IEEE bits
+                // ARE round(scale * kI * kJ) (exact for values < 2^24, FMUL rounds to nearest;
+                // denormals are not flushed: no -ftz). One FMUL per product, no conversion.
                 BS4 bI, bJ;
-                const float sc = ok[k] ? P.fix_scale : 0.0f;  // voxels outside the lattice add nothing
+                const float sc = ok[k] ? P.fix_scale * 0x1p-86f : 0.0f;  // outside the lattice: adds 0
                 if (BSPLINE) {
-                    bI = bspline_bins<false>(ff[k], B);
+                    bI = bspline_bins<false>(ff[k], B, (1.0f / 6.0f) * 0x1p-63f);
                     bJ = bspline_bins<false>(interp(cr[k], c[k]), B, sc * (1.0f / 6.0f));
                 } else {
                     bI = generic_bins<false>(P.p, (double)ff[k]);
                     bJ = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) bJ.k[b] *= sc;
+                    for (int b = 0; b < 4; ++b) {
+                        bI.k[b] *= 0x1p-63f;
+                        bJ.k[b] *= sc;
+                    }
                 }
                 uint32_t* h = mine + bI.m_lo * LD + bJ.m_lo;
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        // round to nearest through the fp32 magic constant (products < 2^22)
-                        atomicAdd(h + a * LD + b,
-                                  (uint32_t)(__float_as_int(fmaf(bI.k[a], bJ.k[b], 12582912.0f)) - 0x4B400000));
+                    for (int b = 0; b < 4; ++b) atomicAdd(h + a * LD + b, __float_as_uint(bI.k[a] * bJ.k[b]));
             }
         }
         if (++iter == HFOLD_ITERS || base + stride >= P.nunits) {
