@@ -39,6 +39,7 @@ constexpr int NSLOT = 8;                         // planes p-7 .. p
 struct Smem {
     float2 raw[NSLOT][HY][HXP];  // shifted (F, Mw), zero outside the volume
     float X[5][HY][TX];          // x box sums of the channel differences
+    int4 pos[4][NT];             // per thread and sample slot: {in-plane offset, gx | gy << 16, ring index, valid}
 };
 
 struct Params {
@@ -94,46 +95,43 @@ __device__ __forceinline__ Cell cell_at(const Geom& g, const double (&kz)[3], in
 
 // The thread's four sample positions, fixed for the whole z march: k = 0, 1 its owned
 // outputs (a vertical pair, so the y sums share rows), k = 2, 3 halo positions
-// (k = 3 exists for the first NHALO - NT threads only). Recomputed (a few integer ops)
-// instead of held in registers.
-struct Pos1 {
-    int hx, hy, gx, gy;
-    bool inxy;  // inside the lattice in x, y, and an existing slot
-};
-
-__device__ __forceinline__ Pos1 pos_of(int k, int t, int x0, int y0, const Params& P) {
-    Pos1 q;
+// (k = 3 exists for the first NHALO - NT threads only). Resolved once per CTA into a
+// shared table (one LDS.128 per position and plane).
+__device__ __forceinline__ int4 pos_record(int k, int t, int x0, int y0, const Params& P) {
+    int hx, hy;
     bool slot_ok = true;
     if (k < 2) {
-        q.hx = (t & (TX - 1)) + R;
-        q.hy = 2 * (t / TX) + k + R;
+        hx = (t & (TX - 1)) + R;
+        hy = 2 * (t / TX) + k + R;
     } else {
         const int h = t + NT * (k - 2);
         slot_ok = h < NHALO;
-        halo_pos(slot_ok ? h : 0, q.hx, q.hy);
+        halo_pos(slot_ok ? h : 0, hx, hy);
     }
-    q.gx = x0 + q.hx - R;
-    q.gy = y0 + q.hy - R;
-    q.inxy = slot_ok && q.gx >= 0 && q.gx < P.nx && q.gy >= 0 && q.gy < P.ny;
-    return q;
+    const int gx = x0 + hx - R, gy = y0 + hy - R;
+    const bool in = slot_ok && gx >= 0 && gx < P.nx && gy >= 0 && gy < P.ny;
+    return make_int4(in ? gy * P.nx + gx : 0, (gx & 0xFFFF) | (gy << 16), hy * HXP + hx, in ? 1 : (slot_ok ? 0 : -1));
 }
+__device__ __forceinline__ int pos_gx(const int4& r) { return (int)(int16_t)(r.y & 0xFFFF); }
+__device__ __forceinline__ int pos_gy(const int4& r) { return r.y >> 16; }
 
 struct Pref {
     float f[4], u[4][3];
 };
 
-__device__ __forceinline__ void prefetch(const Params& P, int t, int x0, int y0, int64_t p, Pref& pf) {
+__device__ __forceinline__ void prefetch(const Params& P, const Smem& sm, int t, int64_t p, Pref& pf) {
     const bool plane_in = p >= 0 && p < P.nz_global;
-    const int64_t zoff = (p - P.buf_z0) * P.plane;
+    const int64_t zoff = plane_in ? (p - P.buf_z0) * P.plane : 0;
+    const float* fpl = P.f + zoff;
+    const float* upl = P.u + 3 * zoff;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const Pos1 q = pos_of(k, t, x0, y0, P);
-        const bool ok = plane_in && q.inxy;
-        const int64_t bi = zoff + (int64_t)q.gy * P.nx + q.gx;
-        pf.f[k] = ok ? __ldg(P.f + bi) : 0.0f;
-        pf.u[k][0] = ok ? __ldg(P.u + 3 * bi) : 0.0f;
-        pf.u[k][1] = ok ? __ldg(P.u + 3 * bi + 1) : 0.0f;
-        pf.u[k][2] = ok ? __ldg(P.u + 3 * bi + 2) : 0.0f;
+        const int4 r = sm.pos[k][t];
+        const bool ok = plane_in && r.w > 0;
+        pf.f[k] = ok ? __ldg(fpl + r.x) : 0.0f;
+        pf.u[k][0] = ok ? __ldg(upl + 3 * r.x) : 0.0f;
+        pf.u[k][1] = ok ? __ldg(upl + 3 * r.x + 1) : 0.0f;
+        pf.u[k][2] = ok ? __ldg(upl + 3 * r.x + 2) : 0.0f;
     }
 }
 
@@ -151,7 +149,7 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Pref (&pf)
     // register ping-pong: this plane's F, u were loaded during the previous plane; the
     // next plane's loads are issued now and land while this plane is processed
     const Pref& cur = pf[SLOT & 1];
-    if (p + 1 < pend) prefetch(P, t, x0, y0, p + 1, pf[(SLOT + 1) & 1]);
+    if (p + 1 < pend) prefetch(P, sm, t, p + 1, pf[(SLOT + 1) & 1]);
     const double zd = i2d((int32_t)p);
     double kz[3];
 #pragma unroll
@@ -161,29 +159,29 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Pref (&pf)
     for (int bt = 0; bt < 2; ++bt) {
         // slot 3 (second halo position) exists for the first NHALO - NT threads only
         if (bt == 1 && !__any_sync(0xffffffffu, t + NT < NHALO)) {
-            const Pos1 q = pos_of(2, t, x0, y0, P);
-            Cell c = cell_at(P.g, kz, q.gx, q.gy, cur.u[2][0], cur.u[2][1], cur.u[2][2]);
+            const int4 q = sm.pos[2][t];
+            Cell c = cell_at(P.g, kz, pos_gx(q), pos_gy(q), cur.u[2][0], cur.u[2][1], cur.u[2][2]);
             const Corners cr = gather_pad<FULLWIN>(P.g, c, miss);
             const float mw = interp(cr, c);
-            sm.raw[slot][q.hy][q.hx] =
-                (plane_in && q.inxy) ? make_float2(cur.f[2] - P.sf, mw - P.sm) : make_float2(0.f, 0.f);
+            (&sm.raw[slot][0][0])[q.z] =
+                (plane_in && q.w > 0) ? make_float2(cur.f[2] - P.sf, mw - P.sm) : make_float2(0.f, 0.f);
             continue;
         }
-        Pos1 q[2];
+        int4 q[2];
         Cell c[2];
         Corners cr[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int k = 2 * bt + i;
-            q[i] = pos_of(k, t, x0, y0, P);
-            c[i] = cell_at(P.g, kz, q[i].gx, q[i].gy, cur.u[k][0], cur.u[k][1], cur.u[k][2]);
+            q[i] = sm.pos[k][t];
+            c[i] = cell_at(P.g, kz, pos_gx(q[i]), pos_gy(q[i]), cur.u[k][0], cur.u[k][1], cur.u[k][2]);
         }
 #pragma unroll
         for (int i = 0; i < 2; ++i) cr[i] = gather_pad<FULLWIN>(P.g, c[i], miss);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int k = 2 * bt + i;
-            const bool ok = plane_in && q[i].inxy;
+            const bool ok = plane_in && q[i].w > 0;
             float2 v = make_float2(0.f, 0.f);
             if (bt == 0) {
                 float d[3];
@@ -195,7 +193,7 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Pref (&pf)
                 const float mw = interp(cr[i], c[i]);
                 if (ok) v = make_float2(cur.f[k] - P.sf, mw - P.sm);
             }
-            if (k < 3 || t + NT < NHALO) sm.raw[slot][q[i].hy][q[i].hx] = v;
+            if (q[i].w >= 0) (&sm.raw[slot][0][0])[q[i].z] = v;
         }
     }
     __syncthreads();
@@ -276,7 +274,7 @@ __device__ __forceinline__ void plane_step(const Params& P, Smem& sm, Pref (&pf)
             const float dm = (fm.y - mm) + P.sm * omwf;    // Mw - mean_M
             const float gmw = gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:404, ANTs)
             const int sq = (SLOT + 1) & 3;                 // gu of plane p-3
-            const int64_t ov = 3 * ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx);
+            const int64_t ov = 3 * ((q - P.z_begin) * P.plane + sm.pos[j][t].x);
             P.g_u[ov] = gur[sq][j][0] * gmw;
             P.g_u[ov + 1] = gur[sq][j][1] * gmw;
             P.g_u[ov + 2] = gur[sq][j][2] * gmw;
@@ -294,6 +292,8 @@ __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
     if (zc0 >= zc1) return;
     for (int i = threadIdx.x; i < NSLOT * HY * HXP; i += NT) (&sm.raw[0][0][0])[i] = make_float2(0.f, 0.f);
     const int t = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sm.pos[k][t] = pos_record(k, t, x0, y0, P);
     float gur[4][2][3];
     double Z[2][5];
 #pragma unroll
@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
     int miss = 0;
     const int64_t pstart = zc0 - R, pend = zc1 + R;
     Pref pf[2];
-    prefetch(P, t, x0, y0, pstart, pf[0]);
     __syncthreads();
+    prefetch(P, sm, t, pstart, pf[0]);
     for (int64_t p = pstart; p < pend; p += 4) {
         plane_step<0, FULLWIN>(P, sm, pf, gur, Z, nsum, miss, p, pstart, pend, x0, y0, zc0);
         plane_step<1, FULLWIN>(P, sm, pf, gur, Z, nsum, miss, p + 1, pstart, pend, x0, y0, zc0);
@@ -345,8 +345,9 @@ extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_
     if (m.pad != 2)
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: the moving image must be zero-bordered (pad = 2, "
                                                 "ffdp_pad_window)");
-    if (d.nx >= (1 << 30) || d.ny >= (1 << 30) || s.nz_global >= (1 << 30))
-        return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: lattice too large");
+    // packed 16-bit lattice coordinates and 32-bit in-plane offsets in the position table
+    if (d.nx >= 32000 || d.ny >= 32000 || d.nx * d.ny >= (1LL << 31) || s.nz_global >= (1 << 30))
+        return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: lattice too large for the fused kernel");
     Params P;
     const ffdp_dims out{d.nx, d.ny, s.nz_global};
     P.g = make_geom(m, out, *args);
