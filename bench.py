@@ -235,21 +235,23 @@ class Stepper:
                 ev[1].record()
                 return [("k_step_lncc", ev[0], ev[1])]
             return None
+        rec = self.ws.records(self.dims, self.slab)
         if not record:
             lib.ffdp_step_mi(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
                              C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.table), self._p(self.g_u),
-                             self._p(self.ws.scratch), None, s)
+                             self._p(self.ws.scratch), self._p(rec), None, s)
             return None
         self.ws.raw.zero_()
         ev[0].record()
-        lib.ffdp_step_mi_hist(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
-                              C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.scratch), None, s)
+        lib.ffdp_step_mi_hist_rec(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win,
+                                  C.byref(self.args), C.byref(self.kernel.c), self._p(self.ws.raw),
+                                  self._p(self.ws.scratch), self._p(rec), None, s)
         lib.ffdp_mi_finalize(self._p(self.ws.raw), self.bins, -1.0, self._p(self.ws.table), s)
         ev[1].record()
-        lib.ffdp_step_mi_grad(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
-                              C.byref(self.kernel.c), self._p(self.ws.table), self._p(self.g_u), None, s)
+        lib.ffdp_step_mi_grad_rec(self._p(self.f), self.dims, self.slab, C.byref(self.kernel.c),
+                                  self._p(self.ws.table), self._p(rec), self._p(self.g_u), s)
         ev[2].record()
-        return [("k_step_mi_hist+finalize", ev[0], ev[1]), ("k_step_mi_grad", ev[1], ev[2])]
+        return [("k_step_mi_hist+finalize", ev[0], ev[1]), ("k_step_mi_grad_rec", ev[1], ev[2])]
 
     def capture(self):
         """CUDA graph of one launch-only step: the timed loop replays it, so host launch

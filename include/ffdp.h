@@ -244,12 +244,35 @@ FFDP_API int64_t ffdp_step_mi_workspace_bytes(int bins);
 /*
  * The whole single-GPU MI step in one call (pass 1, finalize with upstream -1 -- the
  * loss is -MI, distops.hpp:391-392 -- and pass 2). raw (B*B + 2B doubles) is zeroed
- * here; table as ffdp_mi_finalize (the loss is -table[2B^2 + 2B + 1]). Launch-only
- * (no host synchronisation), so it can be captured in a CUDA graph.
+ * here; table as ffdp_mi_finalize (the loss is -table[2B^2 + 2B + 1]). rec: device
+ * buffer of ffdp_step_mi_record_bytes, or NULL; with it (B-spline kernel, zero-bordered
+ * window) pass 1 writes the per-voxel records and pass 2 streams them
+ * (ffdp_step_mi_hist_rec / ffdp_step_mi_grad_rec) instead of sampling the warp again.
+ * Launch-only (no host synchronisation), so it can be captured in a CUDA graph.
  */
 FFDP_API int ffdp_step_mi(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
                  const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, double* table, float* g_u,
-                 void* workspace, int32_t* miss, void* stream);
+                 void* workspace, float* rec, int32_t* miss, void* stream);
+
+/* Bytes of the pass-1 records of a slab interior: 4 floats per voxel. */
+FFDP_API int64_t ffdp_step_mi_record_bytes(ffdp_dims buf_dims, ffdp_slab slab);
+
+/*
+ * Pass 1 as ffdp_step_mi_hist, additionally writing per interior voxel the record
+ * {Mw, S_a (N_a - 1)/2 * dMw/dfrac_a (a = x, y, z)} (16 B) into rec (voxel order of the
+ * interior). B-spline kernel and a zero-bordered window (pad = 2) only.
+ */
+FFDP_API int ffdp_step_mi_hist_rec(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab,
+                                   ffdp_image_window m, const ffdp_sampler_args* args, const ffdp_parzen* kernel,
+                                   double* raw, void* workspace, float* rec, int32_t* miss, void* stream);
+
+/*
+ * Pass 2 from the records: dL/dMw = sum_m kappa_i[m] sum_n ghat[m][n] omega_j[n]
+ * (mi.hpp:392-421) with i = F, j = Mw, and g_u = record.xyz-part * dL/dMw
+ * (sampler.hpp:221-230). Streams F and the records; no warp sampling.
+ */
+FFDP_API int ffdp_step_mi_grad_rec(const float* f, ffdp_dims buf_dims, ffdp_slab slab, const ffdp_parzen* kernel,
+                                   const double* table, const float* rec, float* g_u, void* stream);
 
 /* Pass 2: re-samples Mw, dL/dMw from the ghat table (mi.hpp:392-421), g_u (3N). */
 FFDP_API int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,

@@ -556,6 +556,10 @@ class DeformableStep {
             raw_ = DeviceArray<double>(static_cast<std::size_t>(p.bins * p.bins + 2 * p.bins));
             table_ = DeviceArray<double>(detail::table_len(p.bins));
             scratch_ = DeviceArray<unsigned char>(static_cast<std::size_t>(ffdp_step_mi_workspace_bytes(p.bins)));
+            // pass-1 records: pass 2 then streams them instead of sampling the warp again
+            if (p.mi_bspline_kernel)
+                rec_ = DeviceArray<float>(
+                    static_cast<std::size_t>(ffdp_step_mi_record_bytes(d.c(), full_slab(d.nz)) / sizeof(float)));
         }
     }
 
@@ -574,7 +578,8 @@ class DeformableStep {
                                  sum_.data(), miss_.data(), stream_));
         } else {
             check(ffdp_step_mi(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, &kernel_->c(), raw_.data(),
-                               table_.data(), g_u.data.data(), scratch_.data(), miss_.data(), stream_));
+                               table_.data(), g_u.data.data(), scratch_.data(), rec_.size() ? rec_.data() : nullptr,
+                               miss_.data(), stream_));
         }
         StepResult r;
         if (sync) {
@@ -605,6 +610,7 @@ class DeformableStep {
     DeviceArray<float> m_pad_;
     DeviceArray<std::int32_t> miss_;
     DeviceArray<double> sum_, raw_, table_;
+    DeviceArray<float> rec_;
     DeviceArray<unsigned char> scratch_;
     std::optional<ParzenKernel> kernel_;
     float shift_f_ = 0, shift_m_ = 0;

@@ -90,7 +90,11 @@ _SIGS = {
                                     _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_workspace_bytes": (C.c_int64, [C.c_int]),
     "ffdp_step_mi": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
-                               _vp, _vp, _vp, _vp, _vp, _vp]),
+                               _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "ffdp_step_mi_record_bytes": (C.c_int64, [Dims, Slab]),
+    "ffdp_step_mi_hist_rec": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC),
+                                        C.POINTER(ParzenC), _vp, _vp, _vp, _vp, _vp]),
+    "ffdp_step_mi_grad_rec": (C.c_int, [_vp, Dims, Slab, C.POINTER(ParzenC), _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_grad": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
                                     _vp, _vp, _vp, _vp]),
     "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
@@ -126,7 +130,8 @@ class _Lib:
     def __getattr__(self, name):
         lib = self.load()
         fn = getattr(lib, name)
-        if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check", "ffdp_step_mi_workspace_bytes"):
+        if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check", "ffdp_step_mi_workspace_bytes",
+                    "ffdp_step_mi_record_bytes"):
             return fn
 
         def call(*args):

@@ -449,7 +449,9 @@ bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_ima
                           const ffdp_parzen& k);
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
-                 int32_t* miss, cudaStream_t st);
+                 int32_t* miss, cudaStream_t st, float* rec = nullptr);
+int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ffdp_parzen& k, const double* table,
+                const float* rec, float* g_u, cudaStream_t st);
 int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, const double* table, float* g_u, int32_t* miss,
                  cudaStream_t st);
@@ -549,14 +551,48 @@ int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims d, ffdp_slab s, 
 
 int ffdp_step_mi(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
                  const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, double* table, float* g_u,
-                 void* workspace, int32_t* miss, void* stream) {
+                 void* workspace, float* rec, int32_t* miss, void* stream) {
     if (int rc = check_parzen(kernel)) return rc;
     if (!raw || !table) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null raw/table");
     const int B = kernel->bins;
     cudaMemsetAsync(raw, 0, sizeof(double) * (B * B + 2 * B), (cudaStream_t)stream);
+    const bool use_rec = rec && kernel->kind == FFDP_PARZEN_BSPLINE3 && mi_quad_path_applies(d, s, m, *kernel);
+    if (use_rec) {
+        if (int rc = ffdp_step_mi_hist_rec(f, u, d, s, m, args, kernel, raw, workspace, rec, miss, stream)) return rc;
+        if (int rc = ffdp_mi_finalize(raw, B, -1.0, table, stream)) return rc;
+        return ffdp_step_mi_grad_rec(f, d, s, kernel, table, rec, g_u, stream);
+    }
     if (int rc = ffdp_step_mi_hist(f, u, d, s, m, args, kernel, raw, workspace, miss, stream)) return rc;
     if (int rc = ffdp_mi_finalize(raw, B, -1.0, table, stream)) return rc;
     return ffdp_step_mi_grad(f, u, d, s, m, args, kernel, table, g_u, miss, stream);
+}
+
+int64_t ffdp_step_mi_record_bytes(ffdp_dims d, ffdp_slab s) {
+    return (int64_t)sizeof(float) * 4 * d.nx * d.ny * std::max<int64_t>(0, s.z_end - s.z_begin);
+}
+
+int ffdp_step_mi_hist_rec(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
+                          const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, void* workspace,
+                          float* rec, int32_t* miss, void* stream) {
+    if (int rc = check_parzen(kernel)) return rc;
+    if (int rc = check_slab_mi(d, s)) return rc;
+    const char* why = nullptr;
+    if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
+    if (!f || !u || !raw || !m.data || !rec) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
+    if (kernel->kind != FFDP_PARZEN_BSPLINE3)
+        return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
+    if (!mi_quad_path_applies(d, s, m, *kernel))
+        return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need a zero-bordered moving window (pad = 2)");
+    return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, (unsigned long long*)workspace, miss,
+                        (cudaStream_t)stream, rec);
+}
+
+int ffdp_step_mi_grad_rec(const float* f, ffdp_dims d, ffdp_slab s, const ffdp_parzen* kernel, const double* table,
+                          const float* rec, float* g_u, void* stream) {
+    if (int rc = check_parzen(kernel)) return rc;
+    if (int rc = check_slab_mi(d, s)) return rc;
+    if (!f || !table || !rec || !g_u) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
+    return mi_grad_rec(f, d, s, *kernel, table, rec, g_u, (cudaStream_t)stream);
 }
 
 int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,

@@ -33,6 +33,7 @@ struct Params {
     const float* u;
     float* g_u;
     const double* table;
+    float4* rec;               // pass-1 records (Mw, dscale * dMw/dfrac) per interior voxel, or null
     unsigned long long* hist;  // global u64 [B*B]
     int32_t* miss;
     int32_t nx, ny, nxb, nyq;  // lattice, 32-wide x blocks, 4-row groups
@@ -172,7 +173,9 @@ inline size_t hist_smem_bytes(int B) {
     return sizeof(unsigned long long) * B * B + sizeof(uint32_t) * (size_t)HCOPY * hist_stride(B);
 }
 
-template <bool BSPLINE, bool FULLWIN>
+// REC: also write the voxel's record (Mw, dscale * dMw/dfrac) for the streaming pass 2
+// (k_step_mi_grad_rec): 16 more bytes written here save pass 2 the whole warp sampling.
+template <bool BSPLINE, bool FULLWIN, bool REC>
 __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int B = P.p.bins;
@@ -209,8 +212,18 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
                 BS4 bI, bJ;
                 const float sc = ok[k] ? P.fix_scale * 0x1p-86f : 0.0f;  // outside the lattice: adds 0
                 if (BSPLINE) {
+                    float mw;
+                    if (REC) {
+                        float d[3];
+                        mw = interp_grad(cr[k], c[k], d);
+                        if (ok[k])
+                            P.rec[w.bi + (int64_t)k * P.nx - (P.z_begin - P.buf_z0) * P.plane] =
+                                make_float4(mw, P.g.dscale[0] * d[0], P.g.dscale[1] * d[1], P.g.dscale[2] * d[2]);
+                    } else {
+                        mw = interp(cr[k], c[k]);
+                    }
                     bI = bspline_bins<false>(ff[k], B, (1.0f / 6.0f) * 0x1p-63f);
-                    bJ = bspline_bins<false>(interp(cr[k], c[k]), B, sc * (1.0f / 6.0f));
+                    bJ = bspline_bins<false>(mw, B, sc * (1.0f / 6.0f));
                 } else {
                     bI = generic_bins<false>(P.p, (double)ff[k]);
                     bJ = generic_bins<false>(P.p, interp_f64(cr[k], c[k]));
@@ -316,6 +329,65 @@ __global__ void __launch_bounds__(NT, 3) k_step_mi_grad(const Params P) {
     if (anym && P.miss && (threadIdx.x & 31) == 0) atomicAdd(P.miss, __popc(anym));
 }
 
+// Pass 2 from the pass-1 records: F and (Mw, dscale * dMw/dfrac) are streamed, dL/dMw
+// from the ghat table (mi.hpp:392-421, B-spline), g_u = record.yzw * dL/dMw. No gather,
+// no coordinates: 32 B/voxel of pure streaming (F 4 + record 16 in, g_u 12 out).
+// VEC: 4 voxels per thread with 16-byte loads and stores (aligned buffers).
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_step_mi_grad_rec(const float* __restrict__ f, const float4* __restrict__ rec,
+                                                          float* __restrict__ g_u, int64_t n, const double* table,
+                                                          int B) {
+    extern __shared__ __align__(16) float sg[];
+    const int LD = B + 2 * PAD;
+    {
+        const double* gh = table + B * B + 2 * B;
+        for (int q = threadIdx.x; q < LD * LD; q += blockDim.x) {
+            const int m = q / LD - PAD, nn = q % LD - PAD;
+            sg[q] = (m >= 0 && m < B && nn >= 0 && nn < B) ? (float)gh[m * B + nn] : 0.0f;
+        }
+        __syncthreads();
+    }
+    auto dl = [&](float fv, float mw) {
+        const BS4 bi = bspline_bins<false>(fv, B);
+        const BS4 bj = bspline_bins<true>(mw, B);
+        const float* gr = sg + (bi.m_lo + PAD) * LD + (bj.m_lo + PAD);
+        float gj = 0.0f;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            float acc = gr[a * LD] * bj.w[0];
+            acc = fmaf(gr[a * LD + 1], bj.w[1], acc);
+            acc = fmaf(gr[a * LD + 2], bj.w[2], acc);
+            acc = fmaf(gr[a * LD + 3], bj.w[3], acc);
+            gj = fmaf(bi.k[a], acc, gj);
+        }
+        return gj;
+    };
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t done = 0;
+    if (VEC) {
+        const int64_t n4 = n / 4;
+        for (int64_t i = tid; i < n4; i += stride) {
+            const float4 fv = __ldg(reinterpret_cast<const float4*>(f) + i);
+            const float4 r0 = __ldg(rec + 4 * i), r1 = __ldg(rec + 4 * i + 1), r2 = __ldg(rec + 4 * i + 2),
+                         r3 = __ldg(rec + 4 * i + 3);
+            const float g0 = dl(fv.x, r0.x), g1 = dl(fv.y, r1.x), g2 = dl(fv.z, r2.x), g3 = dl(fv.w, r3.x);
+            float4* o = reinterpret_cast<float4*>(g_u + 12 * i);
+            o[0] = make_float4(r0.y * g0, r0.z * g0, r0.w * g0, r1.y * g1);
+            o[1] = make_float4(r1.z * g1, r1.w * g1, r2.y * g2, r2.z * g2);
+            o[2] = make_float4(r2.w * g2, r3.y * g3, r3.z * g3, r3.w * g3);
+        }
+        done = n4 * 4;
+    }
+    for (int64_t i = done + tid; i < n; i += stride) {
+        const float4 r = __ldg(rec + i);
+        const float g = dl(__ldg(f + i), r.x);
+        g_u[3 * i] = r.y * g;
+        g_u[3 * i + 1] = r.z * g;
+        g_u[3 * i + 2] = r.w * g;
+    }
+}
+
 __global__ void k_hist_to_raw(const unsigned long long* h, int n, double inv_scale, double* raw) {
     for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x)
         raw[i] += (double)h[i] * inv_scale;
@@ -343,6 +415,7 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
     P.u = u;
     P.g_u = nullptr;
     P.table = nullptr;
+    P.rec = nullptr;
     P.hist = nullptr;
     P.miss = nullptr;
     P.nx = (int32_t)d.nx;
@@ -362,7 +435,7 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
 
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
-                 int32_t* miss, cudaStream_t st) {
+                 int32_t* miss, cudaStream_t st, float* rec) {
     using namespace mstep;
     Params P = make_params(f, u, d, s, m, args, k);
     const int B = k.bins;
@@ -371,11 +444,13 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     cudaMemsetAsync(h, 0, sizeof(unsigned long long) * B * B, st);
     P.hist = h;
     P.miss = miss;
+    P.rec = reinterpret_cast<float4*>(rec);
     const size_t smem = hist_smem_bytes(B);
     static bool attr_set = false;  // opt in to > 48 KB dynamic shared memory, once
     if (!attr_set) {
-        for (auto fn : {k_step_mi_hist<true, true>, k_step_mi_hist<true, false>, k_step_mi_hist<false, true>,
-                        k_step_mi_hist<false, false>})
+        for (auto fn : {k_step_mi_hist<true, true, false>, k_step_mi_hist<true, false, false>,
+                        k_step_mi_hist<false, true, false>, k_step_mi_hist<false, false, false>,
+                        k_step_mi_hist<true, true, true>, k_step_mi_hist<true, false, true>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
         attr_set = true;
     }
@@ -383,14 +458,19 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)num_sms()));
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool bs = k.kind == FFDP_PARZEN_BSPLINE3;
-    if (bs && full)
-        k_step_mi_hist<true, true><<<grid, HNT, smem, st>>>(P);
+    if (rec && !bs) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
+    if (rec && full)
+        k_step_mi_hist<true, true, true><<<grid, HNT, smem, st>>>(P);
+    else if (rec)
+        k_step_mi_hist<true, false, true><<<grid, HNT, smem, st>>>(P);
+    else if (bs && full)
+        k_step_mi_hist<true, true, false><<<grid, HNT, smem, st>>>(P);
     else if (bs)
-        k_step_mi_hist<true, false><<<grid, HNT, smem, st>>>(P);
+        k_step_mi_hist<true, false, false><<<grid, HNT, smem, st>>>(P);
     else if (full)
-        k_step_mi_hist<false, true><<<grid, HNT, smem, st>>>(P);
+        k_step_mi_hist<false, true, false><<<grid, HNT, smem, st>>>(P);
     else
-        k_step_mi_hist<false, false><<<grid, HNT, smem, st>>>(P);
+        k_step_mi_hist<false, false, false><<<grid, HNT, smem, st>>>(P);
     k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
     if (!ws) scratch_free(h, st);
     return check_launch("step_mi_hist");
@@ -419,6 +499,25 @@ int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     else
         k_step_mi_grad<false, false><<<grid, NT, smem, st>>>(P);
     return check_launch("step_mi_grad");
+}
+
+int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ffdp_parzen& k, const double* table,
+                const float* rec, float* g_u, cudaStream_t st) {
+    using namespace mstep;
+    if (k.kind != FFDP_PARZEN_BSPLINE3)
+        return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
+    const int B = k.bins;
+    const float* fi = f + (s.z_begin - s.buf_z0) * d.nx * d.ny;  // interior planes
+    const int64_t n = d.nx * d.ny * (s.z_end - s.z_begin);
+    const size_t smem = sizeof(float) * (B + 2 * PAD) * (B + 2 * PAD);
+    const bool vec = (((uintptr_t)fi | (uintptr_t)rec | (uintptr_t)g_u) & 15) == 0;
+    const int64_t work = vec ? n / 4 : n;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8LL * num_sms()));
+    if (vec)
+        k_step_mi_grad_rec<true><<<grid, 256, smem, st>>>(fi, reinterpret_cast<const float4*>(rec), g_u, n, table, B);
+    else
+        k_step_mi_grad_rec<false><<<grid, 256, smem, st>>>(fi, reinterpret_cast<const float4*>(rec), g_u, n, table, B);
+    return check_launch("step_mi_grad_rec");
 }
 
 }  // namespace ffdp

@@ -332,8 +332,15 @@ class ShardedStep:
             else:
                 k = p.make_kernel()
                 self.ws.raw.zero_()
-                lib.ffdp_step_mi_hist(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args), C.byref(k.c),
-                                      V._ptr(self.ws.raw), V._ptr(self.ws.scratch), V._ptr(self.ws.miss), stream)
+                if k.kind == V.PARZEN_BSPLINE3:
+                    rec = self.ws.records(dims, slab)
+                    lib.ffdp_step_mi_hist_rec(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args),
+                                              C.byref(k.c), V._ptr(self.ws.raw), V._ptr(self.ws.scratch), V._ptr(rec),
+                                              V._ptr(self.ws.miss), stream)
+                else:
+                    lib.ffdp_step_mi_hist(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args),
+                                          C.byref(k.c), V._ptr(self.ws.raw), V._ptr(self.ws.scratch),
+                                          V._ptr(self.ws.miss), stream)
             # a miss on any rank means the step has to be redone everywhere (collective agreement)
             miss = self.ws.miss.to(torch.int64)
             if spec.world > 1:
@@ -357,6 +364,10 @@ class ShardedStep:
         allreduce_sum(self.ws.raw[:b * b])
         lib.ffdp_mi_finalize(V._ptr(self.ws.raw), b, -1.0, V._ptr(self.ws.table), V._stream())
         k = p.make_kernel()
-        lib.ffdp_step_mi_grad(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, self._window(), C.byref(args), C.byref(k.c),
-                              V._ptr(self.ws.table), V._ptr(g_u), V._ptr(self.ws.miss), V._stream())
+        if k.kind == V.PARZEN_BSPLINE3:
+            lib.ffdp_step_mi_grad_rec(V._ptr(self.f_halo), dims, slab, C.byref(k.c), V._ptr(self.ws.table),
+                                      V._ptr(self.ws.records(dims, slab)), V._ptr(g_u), V._stream())
+        else:
+            lib.ffdp_step_mi_grad(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, self._window(), C.byref(args),
+                                  C.byref(k.c), V._ptr(self.ws.table), V._ptr(g_u), V._ptr(self.ws.miss), V._stream())
         return -float(self.ws.table[2 * b * b + 2 * b + 1].item()), g_u

@@ -499,6 +499,15 @@ class StepWorkspace:
         self.table = torch.zeros(2 * bins * bins + 2 * bins + 4, dtype=torch.float64, device=device)
         self.scratch = torch.zeros(int(lib.ffdp_step_mi_workspace_bytes(bins)), dtype=torch.uint8, device=device)
         self.bins = bins
+        self._rec = None
+
+    def records(self, dims: Dims, slab: Slab) -> torch.Tensor:
+        """Pass-1 records of the streaming MI pass 2 (16 B per interior voxel), kept across
+        steps of the same lattice."""
+        n = int(lib.ffdp_step_mi_record_bytes(dims, slab)) // 4
+        if self._rec is None or self._rec.numel() < n:
+            self._rec = torch.empty(n, dtype=torch.float32, device=self.device)
+        return self._rec
 
 
 def intensity_shift(v: torch.Tensor) -> float:
@@ -555,8 +564,9 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
             raise InvalidArgument("warp_loss_step: the fused MI step uses the exact Parzen forward")
         if ws.bins != params.bins:
             raise InvalidArgument("warp_loss_step: workspace built for a different bin count")
+        rec = ws.records(_dims(f.shape), slab) if k.kind == PARZEN_BSPLINE3 else None
         lib.ffdp_step_mi(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), C.byref(k.c), _ptr(ws.raw),
-                         _ptr(ws.table), _ptr(g_u), _ptr(ws.scratch), _ptr(ws.miss), _stream())
+                         _ptr(ws.table), _ptr(g_u), _ptr(ws.scratch), _ptr(rec), _ptr(ws.miss), _stream())
         if not sync:
             return StepResult(float("nan"), g_u)
         b = params.bins

@@ -47,6 +47,31 @@ def test_step_lncc_parity(V, lncc_case):
     assert maxrel(gu, ref["g_u"]) <= GRAD_MAXREL
 
 
+def test_step_mi_records_equal_recompute(V, mi_case):
+    """Pass 2 from the pass-1 records (ffdp_step_mi_grad_rec) and pass 2 re-sampling the
+    warp (ffdp_step_mi_grad) compute the same arithmetic: bit-identical g_u and loss."""
+    import ctypes as C
+
+    import torch
+    from paper_2509_25044_b200._lib import lib
+    si, _ = mi_case
+    f, u = dev(si.f), dev(si.u)
+    mimg = V.MovingImage(dev(si.m))
+    k = V.ParzenKernel.bspline3(32)
+    ca = V.SamplerArgs(A=si.A, t=si.t).to_c()
+    dims, slab = V._dims(f.shape), V._full_slab(f.shape[0])
+    out = []
+    for use_rec in (True, False):
+        ws = V.StepWorkspace(f.device, 32)
+        g = torch.empty_like(u)
+        rec = ws.records(dims, slab) if use_rec else None
+        lib.ffdp_step_mi(V._ptr(f), V._ptr(u), dims, slab, mimg.window(), C.byref(ca), C.byref(k.c), V._ptr(ws.raw),
+                         V._ptr(ws.table), V._ptr(g), V._ptr(ws.scratch), V._ptr(rec), V._ptr(ws.miss), V._stream())
+        out.append((host(g), float(ws.table[2 * 32 * 32 + 2 * 32 + 1].item())))
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
+
+
 def test_step_mi_parity(V, mi_case):
     si, ref = mi_case
     res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="mi", bins=32))
