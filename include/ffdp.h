@@ -205,10 +205,10 @@ FFDP_API int ffdp_mi_bwd(const float* vi, const float* vj, int64_t n, const ffdp
 /* ------------------------------------------------------------- fused step (★) */
 
 /*
- * The deformable step's hot path (registration.hpp:277-312) for LNCC in ANTs mode, as
- * ONE pass: Mw = fused_sample(M, u) for the slab + 3 halo planes, the five LNCC
- * moments, dL/dMw (lncc.hpp:226-280 with ants_approx), and g_u =
- * fused_sample_backward(dL/dMw) (sampler.hpp:221-230). Nothing but g_u is written.
+ * The deformable step's hot path (registration.hpp:277-312) for LNCC in ANTs mode:
+ * Mw = fused_sample(M, u) for the slab + 3 halo planes, the five LNCC moments, dL/dMw
+ * (lncc.hpp:226-280 with ants_approx), and g_u = fused_sample_backward(dL/dMw)
+ * (sampler.hpp:221-230).
  *   f, u: buffers described by `slab` (halo planes of radius window/2 included);
  *   g_u: interior planes only (3 floats per voxel);
  *   args: the sampler arguments of the GLOBAL output lattice (buf_dims.nx, buf_dims.ny,
@@ -217,11 +217,29 @@ FFDP_API int ffdp_mi_bwd(const float* vi, const float* vj, int64_t n, const ffdp
  *   gi: dL/dn_i (-1/N_total for the deformable step);
  *   shift_f, shift_m: intensity shifts for the moment accumulation (any value is exact
  *     up to rounding; the mid-range of the data is most accurate);
- *   sum_n: device double, += sum of n_i over the slab interior.
+ *   sum_n: device double, += sum of n_i over the slab interior;
+ *   workspace: device buffer of ffdp_step_lncc_workspace_bytes: the step runs as two
+ *     streaming passes (warp every voxel once, then the moments), or NULL:
+ *     one fused pass that re-samples the warp on every tile halo.
  */
 FFDP_API int ffdp_step_lncc(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
                    const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f, float shift_m,
-                   float* g_u, double* sum_n, int32_t* miss, void* stream);
+                   float* g_u, double* sum_n, int32_t* miss, void* workspace, void* stream);
+
+/*
+ * The two passes of ffdp_step_lncc with a workspace, separately (e.g. to time them, or
+ * to overlap the warp pass with communication): passes = 1 runs the warp sampling
+ * (Mw, dMw/du into the workspace; reads u, M), 2 the moments, dL/dMw and g_u (reads F
+ * and the workspace; adds to sum_n), 3 both. Arguments as ffdp_step_lncc.
+ */
+FFDP_API int ffdp_step_lncc_passes(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab,
+                                   ffdp_image_window m, const ffdp_sampler_args* args, int window, double eps,
+                                   double gi, float shift_f, float shift_m, float* g_u, double* sum_n, int32_t* miss,
+                                   void* workspace, int passes, void* stream);
+
+/* Bytes of the two-pass LNCC workspace: Mw for the buffer planes, dMw/du for the interior,
+ * one double per CTA for the fixed-order loss reduction. */
+FFDP_API int64_t ffdp_step_lncc_workspace_bytes(ffdp_dims buf_dims, ffdp_slab slab);
 
 /*
  * Fused MI step, pass 1 (registration.hpp:278-299 with dist_mi, distops.hpp:355-373):

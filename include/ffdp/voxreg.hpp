@@ -551,6 +551,9 @@ class DeformableStep {
             check(ffdp_minmax(moving.data.data(), d.voxels(), mm.data(), s));
             a = mm.download(s);
             shift_m_ = 0.5f * (a[0] + a[1]);
+            // two-pass step: every voxel warped once, then the moments
+            lws_ = DeviceArray<unsigned char>(
+                static_cast<std::size_t>(ffdp_step_lncc_workspace_bytes(d.c(), full_slab(d.nz))));
         } else {
             kernel_.emplace(p.mi_bspline_kernel ? ParzenKernel::bspline3(p.bins) : ParzenKernel::gaussian(p.bins));
             raw_ = DeviceArray<double>(static_cast<std::size_t>(p.bins * p.bins + 2 * p.bins));
@@ -575,7 +578,7 @@ class DeformableStep {
             sum_.zero(stream_);
             check(ffdp_step_lncc(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, p_.window, p_.epsilon,
                                  -1.0 / static_cast<double>(dims_.voxels()), shift_f_, shift_m_, g_u.data.data(),
-                                 sum_.data(), miss_.data(), stream_));
+                                 sum_.data(), miss_.data(), lws_.data(), stream_));
         } else {
             check(ffdp_step_mi(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, &kernel_->c(), raw_.data(),
                                table_.data(), g_u.data.data(), scratch_.data(), rec_.size() ? rec_.data() : nullptr,
@@ -611,7 +614,7 @@ class DeformableStep {
     DeviceArray<std::int32_t> miss_;
     DeviceArray<double> sum_, raw_, table_;
     DeviceArray<float> rec_;
-    DeviceArray<unsigned char> scratch_;
+    DeviceArray<unsigned char> scratch_, lws_;
     std::optional<ParzenKernel> kernel_;
     float shift_f_ = 0, shift_m_ = 0;
 };

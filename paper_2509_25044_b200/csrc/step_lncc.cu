@@ -326,14 +326,25 @@ __global__ void __launch_bounds__(NT, 2) k_step_lncc(const Params P) {
 
 using namespace ffdp;
 
-extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
-                              const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f,
-                              float shift_m, float* g_u, double* sum_n, int32_t* miss, void* stream) {
+namespace ffdp {
+int64_t lncc2_workspace_bytes(const ffdp_dims& d, const ffdp_slab& s);
+int lncc2_step(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
+               const ffdp_sampler_args& args, double eps, double gi, float shift_f, float shift_m, float* g_u,
+               double* sum_n, int32_t* miss, void* workspace, int passes, cudaStream_t st);
+}  // namespace ffdp
+
+extern "C" int64_t ffdp_step_lncc_workspace_bytes(ffdp_dims d, ffdp_slab s) { return lncc2_workspace_bytes(d, s); }
+
+static int step_lncc_impl(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
+                          const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f,
+                          float shift_m, float* g_u, double* sum_n, int32_t* miss, void* workspace, int passes,
+                          void* stream) {
     using namespace ffdp::lstep;
     if (window != WIN) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: the fused kernel is built for window %d", WIN);
     const char* why = nullptr;
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!f || !u || !g_u || !m.data) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: null pointer");
+    if (passes < 1 || passes > 3) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: passes must be 1, 2 or 3");
     if (d.nx < 1 || d.ny < 1 || d.nz < 1 || s.buf_nz != d.nz || s.z_begin < s.buf_z0 || s.z_end > s.buf_z0 + s.buf_nz ||
         s.z_begin >= s.z_end || s.buf_z0 < 0 || s.buf_z0 + s.buf_nz > s.nz_global)
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: inconsistent slab");
@@ -348,6 +359,10 @@ extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_
     // packed 16-bit lattice coordinates and 32-bit in-plane offsets in the position table
     if (d.nx >= 32000 || d.ny >= 32000 || d.nx * d.ny >= (1LL << 31) || s.nz_global >= (1 << 30))
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: lattice too large for the fused kernel");
+    if (workspace)
+        return lncc2_step(f, u, d, s, m, *args, eps, gi, shift_f, shift_m, g_u, sum_n, miss, workspace, passes,
+                          (cudaStream_t)stream);
+    if (passes != 3) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: separate passes need the workspace");
     Params P;
     const ffdp_dims out{d.nx, d.ny, s.nz_global};
     P.g = make_geom(m, out, *args);
@@ -388,4 +403,21 @@ extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_
     else
         k_step_lncc<false><<<grid, NT, sizeof(Smem), (cudaStream_t)stream>>>(P);
     return check_launch("step_lncc");
+}
+
+extern "C" int ffdp_step_lncc(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
+                              const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f,
+                              float shift_m, float* g_u, double* sum_n, int32_t* miss, void* workspace,
+                              void* stream) {
+    return step_lncc_impl(f, u, d, s, m, args, window, eps, gi, shift_f, shift_m, g_u, sum_n, miss, workspace, 3,
+                          stream);
+}
+
+extern "C" int ffdp_step_lncc_passes(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
+                                     const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f,
+                                     float shift_m, float* g_u, double* sum_n, int32_t* miss, void* workspace,
+                                     int passes, void* stream) {
+    if (!workspace) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: the two-pass step needs its workspace");
+    return step_lncc_impl(f, u, d, s, m, args, window, eps, gi, shift_f, shift_m, g_u, sum_n, miss, workspace,
+                          passes, stream);
 }

@@ -328,7 +328,8 @@ class ShardedStep:
                 self.ws.sum_n.zero_()
                 lib.ffdp_step_lncc(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args), p.window,
                                    p.epsilon, -1.0 / n_total, self.shifts[0], self.shifts[1], V._ptr(g_u),
-                                   V._ptr(self.ws.sum_n), V._ptr(self.ws.miss), stream)
+                                   V._ptr(self.ws.sum_n), V._ptr(self.ws.miss),
+                                   V._ptr(self.ws.lncc_workspace(dims, slab)), stream)
             else:
                 k = p.make_kernel()
                 self.ws.raw.zero_()

@@ -500,6 +500,15 @@ class StepWorkspace:
         self.scratch = torch.zeros(int(lib.ffdp_step_mi_workspace_bytes(bins)), dtype=torch.uint8, device=device)
         self.bins = bins
         self._rec = None
+        self._lncc = None
+
+    def lncc_workspace(self, dims: Dims, slab: Slab) -> torch.Tensor:
+        """Workspace of the two-pass LNCC step (Mw of the buffer planes, dMw/du of the
+        interior), kept across steps of the same lattice."""
+        n = int(lib.ffdp_step_lncc_workspace_bytes(dims, slab)) // 4
+        if self._lncc is None or self._lncc.numel() < n:
+            self._lncc = torch.empty(n, dtype=torch.float32, device=self.device)
+        return self._lncc
 
     def records(self, dims: Dims, slab: Slab) -> torch.Tensor:
         """Pass-1 records of the streaming MI pass 2 (16 B per interior voxel), kept across
@@ -553,8 +562,10 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
         if shifts is None:
             shifts = (intensity_shift(f), intensity_shift(mi.interior.contiguous()))
         ws.sum_n.zero_()
+        lws = ws.lncc_workspace(_dims(f.shape), slab)
         lib.ffdp_step_lncc(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), params.window, params.epsilon,
-                           -1.0 / n, shifts[0], shifts[1], _ptr(g_u), _ptr(ws.sum_n), _ptr(ws.miss), _stream())
+                           -1.0 / n, shifts[0], shifts[1], _ptr(g_u), _ptr(ws.sum_n), _ptr(ws.miss), _ptr(lws),
+                           _stream())
         if not sync:
             return StepResult(float("nan"), g_u)
         loss = 1.0 - float(ws.sum_n.item()) / n

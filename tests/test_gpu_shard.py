@@ -19,7 +19,7 @@ def V():
     return voxreg
 
 
-def run_slab(V, si, spec_lo, spec_hi, nz, pad, loss, window, bins=32, shifts=(0.5, 0.5)):
+def run_slab(V, si, spec_lo, spec_hi, nz, pad, loss, window, bins=32, shifts=(0.5, 0.5), two_pass=True):
     import torch
     from paper_2509_25044_b200._lib import Dims, ImageWindow, Slab, lib
     f, m, u = dev(si.f), dev(si.m), dev(si.u)
@@ -37,8 +37,12 @@ def run_slab(V, si, spec_lo, spec_hi, nz, pad, loss, window, bins=32, shifts=(0.
     s = V._stream()
     if loss == "lncc":
         sn = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ws = None
+        if two_pass:
+            ws = torch.empty(int(lib.ffdp_step_lncc_workspace_bytes(V._dims(fb.shape), slab)) // 4, device="cuda")
         lib.ffdp_step_lncc(V._ptr(fb), V._ptr(ub), V._dims(fb.shape), slab, win, C.byref(args), 7, 1e-5,
-                           -1.0 / si.f.size, shifts[0], shifts[1], V._ptr(g_u), V._ptr(sn), V._ptr(miss), s)
+                           -1.0 / si.f.size, shifts[0], shifts[1], V._ptr(g_u), V._ptr(sn), V._ptr(miss), V._ptr(ws),
+                           s)
         return float(sn.item()), g_u, int(miss.item())
     k = V.ParzenKernel.bspline3(bins)
     raw = torch.zeros(bins * bins + 2 * bins, dtype=torch.float64, device="cuda")
@@ -47,8 +51,9 @@ def run_slab(V, si, spec_lo, spec_hi, nz, pad, loss, window, bins=32, shifts=(0.
     return raw, (fb, ub, slab, win, args, k, g_u, mp), int(miss.item())
 
 
+@pytest.mark.parametrize("two_pass", [True, False])
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_lncc_slabs_equal_single_gpu(V, orc, world):
+def test_lncc_slabs_equal_single_gpu(V, orc, world, two_pass):
     from oracle import step_inputs
     from paper_2509_25044_b200 import dist as D
     si = step_inputs(orc, (40, 36, 44), seed=4242, loss="lncc")
@@ -57,7 +62,7 @@ def test_lncc_slabs_equal_single_gpu(V, orc, world):
     ref = orc.step_lncc(si.f, si.m, si.u, si.A, si.t)
     total, parts = 0.0, []
     for r, (lo, hi) in enumerate(D.shard_ranges(nz, world)):
-        sn, g, miss = run_slab(V, si, lo, hi, nz, 3, "lncc", (0, nz))
+        sn, g, miss = run_slab(V, si, lo, hi, nz, 3, "lncc", (0, nz), two_pass=two_pass)
         assert miss == 0
         total += sn
         parts.append(host(g))
