@@ -357,7 +357,7 @@ static int step_lncc_impl(const float* f, const float* u, ffdp_dims d, ffdp_slab
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: the moving image must be zero-bordered (pad = 2, "
                                                 "ffdp_pad_window)");
     // packed 16-bit lattice coordinates and 32-bit in-plane offsets in the position table
-    if (d.nx >= 32000 || d.ny >= 32000 || d.nx * d.ny >= (1LL << 31) || s.nz_global >= (1 << 30))
+    if (d.nx >= 32000 || d.ny >= 32000 || 3 * d.nx * d.ny >= (1LL << 31) || s.nz_global >= (1 << 30))
         return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: lattice too large for the fused kernel");
     if (workspace)
         return lncc2_step(f, u, d, s, m, *args, eps, gi, shift_f, shift_m, g_u, sum_n, miss, workspace, passes,

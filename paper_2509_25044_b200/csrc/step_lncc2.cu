@@ -113,7 +113,7 @@ template <int TX, int TY>
 struct Tile {
     static constexpr int NT = TX * TY / 2;          // one vertical output pair per thread
     static constexpr int HX = TX + 2 * R, HY = TY + 2 * R;
-    static constexpr int HXP = HX + 2;              // ring row pitch (float2)
+    static constexpr int HXP = HX;                  // ring row pitch: position h = hy * HX + hx is element h
     static constexpr int NPOS = HX * HY;
     static constexpr int KPOS = (NPOS + NT - 1) / NT;  // positions per thread
     static constexpr int XJOBS = HY * (TX / 4);
@@ -168,8 +168,9 @@ __device__ __forceinline__ void load_plane(const MParams& P, const int32_t (&off
 
 template <int TX, int TY, int SLOT>
 __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::Smem& sm, Pref2<TX, TY> (&pf)[2],
-                                       const int32_t (&off)[Tile<TX, TY>::KPOS], double (&Z)[2][5], double& nsum,
-                                       int64_t p, int64_t pstart, int64_t pend, int x0, int y0, int64_t zc0) {
+                                       const int32_t (&off)[Tile<TX, TY>::KPOS], const int32_t (&out_off)[2],
+                                       double (&Z)[2][5], double& nsum, int64_t p, int64_t pstart, int64_t pend,
+                                       int x0, int y0, int64_t zc0) {
     using T = Tile<TX, TY>;
     if (p >= pend) return;  // uniform across the CTA
     const int t = threadIdx.x;
@@ -181,10 +182,7 @@ __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::
 #pragma unroll
         for (int k = 0; k < T::KPOS; ++k) {
             const int h = t + T::NT * k;
-            if (h < T::NPOS) {
-                const int hy = h / T::HX, hx = h - hy * T::HX;
-                sm.raw[slot][hy][hx] = make_float2(cur.v[k].x - P.sf, cur.v[k].y);
-            }
+            if (h < T::NPOS) (&sm.raw[slot][0][0])[h] = make_float2(cur.v[k].x - P.sf, cur.v[k].y);
         }
         if (p + 1 < pend) load_plane<TX, TY>(P, off, p + 1, pf[(SLOT + 1) & 1]);
     }
@@ -192,12 +190,13 @@ __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::
     const bool emit = p >= zc0 + R;
     const int64_t q = p - R;
     const int ox = t % TX, oy0 = 2 * (t / TX);
+    // the thread's two outputs of plane q: 3 * in-plane offset (out_off[j] < 0: outside)
+    const int64_t qoff = 3 * (q - P.z_begin) * P.plane;
     float G[2][3];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        const int gx = x0 + ox, gy = y0 + oy0 + j;
-        const bool ok = emit && gx < P.nx && gy < P.ny;
-        const float* gp = P.gd + 3 * ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx);
+        const bool ok = emit && out_off[j] >= 0;
+        const float* gp = P.gd + qoff + out_off[j];
 #pragma unroll
         for (int a = 0; a < 3; ++a) G[j][a] = ok ? __ldg(gp + a) : 0.0f;
     }
@@ -241,7 +240,7 @@ __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::
     for (int j = 0; j < 2; ++j) {
         const int oy = oy0 + j;
         const int gx = x0 + ox, gy = y0 + oy;
-        if (emit && gx < P.nx && gy < P.ny) {
+        if (emit && out_off[j] >= 0) {
             const float2 fm = sm.raw[slot_q][oy + R][ox + R];
             const float cw = win_count(gx, P.nx) * win_count(gy, P.ny) * win_count(q, P.nz_global);
             const double inv = 1.0 / (double)(WIN * WIN * WIN);
@@ -271,7 +270,7 @@ __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::
             const float df = (fm.x - mf) + P.sf * omwf;    // F - mean_F
             const float dm = (fm.y - mm) + P.sm * omwf;    // Mw - mean_M
             const float gmw = gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:404, ANTs)
-            float* o = P.g_u + 3 * ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx);
+            float* o = P.g_u + qoff + out_off[j];
             o[0] = G[j][0] * gmw;
             o[1] = G[j][1] * gmw;
             o[2] = G[j][2] * gmw;
@@ -299,14 +298,19 @@ __global__ void __launch_bounds__(Tile<TX, TY>::NT, FFDP_L2_MINB) k_lncc_moments
         for (int ch = 0; ch < 5; ++ch) Z[j][ch] = 0.0;
     double nsum = 0.0;
     const int64_t pstart = zc0 - R, pend = zc1 + R;
-    int32_t off[T::KPOS];
+    int32_t off[T::KPOS], out_off[2];
     plane_offsets<TX, TY>(P, threadIdx.x, x0, y0, off);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int gx = x0 + (int)threadIdx.x % TX, gy = y0 + 2 * ((int)threadIdx.x / TX) + j;
+        out_off[j] = (gx < P.nx && gy < P.ny) ? 3 * (gy * P.nx + gx) : -1;
+    }
     Pref2<TX, TY> pf[2];
     load_plane<TX, TY>(P, off, pstart, pf[0]);
     __syncthreads();
     for (int64_t p = pstart; p < pend; p += 2) {
-        mplane<TX, TY, 0>(P, sm, pf, off, Z, nsum, p, pstart, pend, x0, y0, zc0);
-        mplane<TX, TY, 1>(P, sm, pf, off, Z, nsum, p + 1, pstart, pend, x0, y0, zc0);
+        mplane<TX, TY, 0>(P, sm, pf, off, out_off, Z, nsum, p, pstart, pend, x0, y0, zc0);
+        mplane<TX, TY, 1>(P, sm, pf, off, out_off, Z, nsum, p + 1, pstart, pend, x0, y0, zc0);
     }
     __shared__ double red[T::NT / 32];
     nsum = block_sum<T::NT>(nsum, red);
