@@ -40,32 +40,56 @@ struct SParams {
     float sm;
 };
 
+// The unit of a warp: 32 consecutive x voxels (lane = x offset) of 4 consecutive rows of
+// one plane; consecutive lanes gather neighbouring source positions (coalesced).
+struct SUnit {
+    int32_t x, y0;
+    int64_t p, bi;
+    bool vx;
+};
+
+__device__ __forceinline__ SUnit sunit(const SParams& P, int64_t unit, int lane) {
+    SUnit w;
+    const uint32_t r1 = fdiv((uint32_t)unit, P.div_nxb);
+    w.x = (int32_t)((uint32_t)unit - r1 * P.nxb) * 32 + lane;
+    const uint32_t zz = fdiv(r1, P.div_nyq);
+    w.y0 = (int32_t)(r1 - zz * P.nyq) * 4;
+    w.p = P.p0 + zz;
+    w.vx = w.x < P.nx;
+    w.bi = (w.p - P.buf_z0) * P.plane + (int64_t)w.y0 * P.nx + (w.vx ? w.x : 0);
+    return w;
+}
+
+__device__ __forceinline__ void sload(const SParams& P, const SUnit& w, float (&uu)[12]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool ok = w.vx && w.y0 + k < P.ny;
+        const int64_t i = w.bi + (int64_t)k * P.nx;
+        uu[3 * k] = ok ? __ldg(P.u + 3 * i) : 0.0f;
+        uu[3 * k + 1] = ok ? __ldg(P.u + 3 * i + 1) : 0.0f;
+        uu[3 * k + 2] = ok ? __ldg(P.u + 3 * i + 2) : 0.0f;
+    }
+}
+
+#ifndef FFDP_L2_SMINB
+#define FFDP_L2_SMINB 3
+#endif
+#ifndef FFDP_L2_SPREF
+#define FFDP_L2_SPREF 1
+#endif
 template <bool FULLWIN>
-__global__ void __launch_bounds__(256) k_lncc_sample(const SParams P) {
+__global__ void __launch_bounds__(256, FFDP_L2_SMINB) k_lncc_sample(const SParams P) {
     int miss = 0;
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * 8;
-    for (int64_t unit = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); unit < P.nunits; unit += stride) {
-        const uint32_t r1 = fdiv((uint32_t)unit, P.div_nxb);
-        const int32_t x = (int32_t)((uint32_t)unit - r1 * P.nxb) * 32 + lane;
-        const uint32_t zz = fdiv(r1, P.div_nyq);
-        const int32_t y0 = (int32_t)(r1 - zz * P.nyq) * 4;
-        const int64_t p = P.p0 + zz;
-        const bool vx = x < P.nx;
-        const int64_t bi = (p - P.buf_z0) * P.plane + (int64_t)y0 * P.nx + (vx ? x : 0);
-        float uu[12];
-        bool ok[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            ok[k] = vx && y0 + k < P.ny;
-            const int64_t i = bi + (int64_t)k * P.nx;
-            uu[3 * k] = ok[k] ? __ldg(P.u + 3 * i) : 0.0f;
-            uu[3 * k + 1] = ok[k] ? __ldg(P.u + 3 * i + 1) : 0.0f;
-            uu[3 * k + 2] = ok[k] ? __ldg(P.u + 3 * i + 2) : 0.0f;
-        }
+    int64_t unit = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    SUnit w = sunit(P, unit < P.nunits ? unit : 0, lane);
+    float uu[12];
+    if (unit < P.nunits) sload(P, w, uu);
+    for (; unit < P.nunits; unit += stride) {
         Cell c[4];
         RowBase rb;
-        rb.init(P.g, x, y0, (int32_t)p);
+        rb.init(P.g, w.x, w.y0, (int32_t)w.p);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (k) rb.step_y(P.g);
@@ -74,13 +98,22 @@ __global__ void __launch_bounds__(256) k_lncc_sample(const SParams P) {
         Corners cr[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
-        const bool interior = p >= P.z_begin && p < P.z_end;
+        const SUnit cw = w;
+        if (FFDP_L2_SPREF) {
+            // the next unit's displacements are in flight while this unit's corners land
+            const int64_t nu = unit + stride;
+            if (nu < P.nunits) {
+                w = sunit(P, nu, lane);
+                sload(P, w, uu);
+            }
+        }
+        const bool interior = cw.p >= P.z_begin && cw.p < P.z_end;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             float d[3];
             const float v = interp_grad(cr[k], c[k], d);
-            if (ok[k]) {
-                const int64_t i = bi + (int64_t)k * P.nx;
+            if (cw.vx && cw.y0 + k < P.ny) {
+                const int64_t i = cw.bi + (int64_t)k * P.nx;
                 P.mw[i] = v - P.sm;
                 if (interior) {
                     float* o = P.gd + 3 * (i - (P.z_begin - P.buf_z0) * P.plane);
@@ -88,6 +121,13 @@ __global__ void __launch_bounds__(256) k_lncc_sample(const SParams P) {
                     o[1] = P.g.dscale[1] * d[1];
                     o[2] = P.g.dscale[2] * d[2];
                 }
+            }
+        }
+        if (!FFDP_L2_SPREF) {
+            const int64_t nu = unit + stride;
+            if (nu < P.nunits) {
+                w = sunit(P, nu, lane);
+                sload(P, w, uu);
             }
         }
     }
