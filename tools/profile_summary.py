@@ -24,7 +24,7 @@ from collections import OrderedDict
 sys.path.insert(0, os.path.dirname(__file__))
 from ncu_raw_summary import WANT  # noqa: E402
 
-OURS = re.compile(r"k_step_|k_hist_to_raw|k_mi_finalize|k_zero|k_reduce|k_pad|k_sampler|k_lncc|k_mi_|k_conv")
+OURS = re.compile(r"k_step_|k_hist_to_raw|k_mi_finalize|k_zero|k_reduce|k_pad|k_sampler|k_lncc|k_mi_|k_conv|k_add_partials")
 VOXELS = {"mi256": 256 ** 3, "lncc720": 720 * 640 * 720}
 
 
@@ -73,6 +73,12 @@ def full(rep, out, workload):
                 u = units[ix[key]]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
+            stalls = sorted(((h.replace("smsp__average_warps_issue_stalled_", "").replace(
+                "_per_issue_active.ratio", ""), float(r[i] or 0)) for i, h in enumerate(hdr)
+                if "smsp__average_warps_issue_stalled" in h and h.endswith("per_issue_active.ratio")),
+                key=lambda kv: -kv[1])[:6]
+            fo.write("   top warp stall reasons (per issue): " +
+                     ", ".join(f"{k} {v:.2f}" for k, v in stalls) + "\n")
             traffic = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
             nv = VOXELS[workload]
             fo.write(f"   traffic (dram read + write) per launch: {traffic:.4e} B = {traffic / nv:.2f} B/voxel "
@@ -93,7 +99,7 @@ def main(tag, d):
         traffic = json.load(open(tp))
     for p in sorted(glob.glob(os.path.join(d, "full_*.ncu-rep"))):
         k = os.path.basename(p)[len("full_"):-len(".ncu-rep")]
-        wl = "lncc720" if "lncc" in k else "mi256"
+        wl = "lncc720" if "lncc" in k else "mi256"  # capture names: full_<kernel>
         for name, v in full(p, f"profiles/{tag}_full_{k}.txt", wl).items():
             v["round"] = tag
             traffic[name] = v
