@@ -153,12 +153,15 @@ __device__ __forceinline__ double interp_f64(const Corners& k, const Cell& c) {
 // face into the next cell with a low word < 4, and fractions within 4 units of the lower
 // face leave a low word <= 8; both give frac = 0 after the 23-bit truncation below, and
 // everywhere else the extra 4 units only move frac by at most one 2^-23 step.
+// |f| >= 2^19 or NaN needs no test: the high word is monotone in t, so f >= 2^19 (and
+// NaN) give i0 >= 2^19 and f < -2^19 gives i0 < -2^19 (a negative t's sign bit makes the
+// int32 subtraction either stay far below zero or wrap above 2^30). Every caller clamps i0
+// into the zero border (gather_pad), where such cells read only zeros, and frac is always
+// a finite value in [0, 1).
 __device__ __forceinline__ void cell_fix(double f, int32_t& i0, float& frac) {
     const double t = f + 0x1.8000000000004p+20;  // 1.5 * 2^20 + 4 * 2^-32
     const uint32_t lo = (uint32_t)__double2loint(t);
-    const int32_t hi = __double2hiint(t);
-    // |f| >= 2^19 (exponent of t off) or NaN: far outside any lattice -> fully zero padded
-    i0 = (uint32_t)(hi - 0x41300000) < 0x100000u ? hi - 0x41380000 : -4;
+    i0 = __double2hiint(t) - 0x41380000;
     frac = __uint_as_float(0x3F800000u | (lo >> 9)) - 1.0f;
 }
 
@@ -274,7 +277,7 @@ __device__ __forceinline__ void gather_n(const Geom& g, const Cell (&c)[NS], Cor
 // -2 or n reads two border zeros, like the reference's fully zero-padded samples) and
 // load the 8 corners unconditionally. With a z window, corners on non-resident planes
 // inside the volume are window misses (they read the zero border).
-template <bool FULLWIN>
+template <bool FULLWIN, bool OFF32 = false>
 __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int& miss) {
     const int32_t ix = min(max(c.i0[0], -2), g.n[0]);
     const int32_t iy = min(max(c.i0[1], -2), g.n[1]);
@@ -288,8 +291,26 @@ __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int&
         iz = min(max(z0, g.wz0 - 2), g.wz1);
     }
     const int32_t sy = (int32_t)g.sy;
-    const float* p = g.img + (int64_t)(iz - g.wz0) * g.sz + (int64_t)(iy * sy + ix);
     Corners k;
+    if (OFF32) {
+        // the resident window holds < 2^31 elements: 32-bit offsets, one wide add per row
+        const int32_t sz = (int32_t)g.sz;
+        const int32_t o = (iz - g.wz0) * sz + iy * sy + ix;
+        const float* p0 = g.img + o;
+        const float* p1 = g.img + (o + sy);
+        const float* p2 = g.img + (o + sz);
+        const float* p3 = g.img + (o + sz + sy);
+        k.v[0] = __ldg(p0);
+        k.v[1] = __ldg(p0 + 1);
+        k.v[2] = __ldg(p1);
+        k.v[3] = __ldg(p1 + 1);
+        k.v[4] = __ldg(p2);
+        k.v[5] = __ldg(p2 + 1);
+        k.v[6] = __ldg(p3);
+        k.v[7] = __ldg(p3 + 1);
+        return k;
+    }
+    const float* p = g.img + (int64_t)(iz - g.wz0) * g.sz + (int64_t)(iy * sy + ix);
     k.v[0] = __ldg(p);
     k.v[1] = __ldg(p + 1);
     k.v[2] = __ldg(p + sy);
@@ -300,6 +321,11 @@ __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int&
     k.v[6] = __ldg(p + sy);
     k.v[7] = __ldg(p + sy + 1);
     return k;
+}
+
+// The padded resident window fits 32-bit element offsets (gather_pad<.., true>).
+inline bool window_off32(const Geom& g) {
+    return (double)g.sz * (double)(g.wz1 - g.wz0 + 4) < 2147483647.0 - 4.0 * (double)g.sz;
 }
 
 // ------------------------------------------------------------------ Parzen kernels

@@ -40,7 +40,7 @@ struct Params {
     FastDiv div_nxb, div_nyq;
     int64_t plane, z_begin, buf_z0;
     int64_t nunits;
-    float fix_scale;           // 2^23 (bspline) / 2^22 (gaussian) / 2^21 (delta)
+    float fix_scale;           // 2^BS_LOG2 (bspline, k_mi_hist_bs) / 2^22 (gaussian) / 2^21 (delta)
 };
 
 // B-spline weights at bins m_lo..m_lo+3 for one intensity, fp32 (the kernel is C2,
@@ -154,7 +154,7 @@ __device__ __forceinline__ void unit_cells(const Params& P, const Unit& w, const
 #define FFDP_MI_HIST_NT 1024
 #endif
 #ifndef FFDP_MI_HIST_COPIES
-#define FFDP_MI_HIST_COPIES 32
+#define FFDP_MI_HIST_COPIES 16
 #endif
 constexpr int HNT = FFDP_MI_HIST_NT;
 constexpr int HCOPY = FFDP_MI_HIST_COPIES;
@@ -248,6 +248,198 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
             __syncthreads();
             for (int i = threadIdx.x; i < B * B; i += HNT) {
                 const int q = (i / B + PAD) * LD + (i % B) + PAD;
+                unsigned long long acc = 0ull;
+#pragma unroll 8
+                for (int cp = 0; cp < HCOPY; ++cp) {
+                    acc += s32[cp * CS + q];
+                    s32[cp * CS + q] = 0u;
+                }
+                s64[i] += acc;
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < B * B; i += HNT) {
+        const unsigned long long v = s64[i];
+        if (v) atomicAdd(&P.hist[i], v);
+    }
+    const unsigned anym = __ballot_sync(0xffffffffu, miss);
+    if (anym && P.miss && (threadIdx.x & 31) == 0) atomicAdd(P.miss, __popc(anym));
+}
+
+// ------------------------------------------------------------------ pass 1, B-spline
+// The B-spline pass 1 with the bin count as a compile-time constant (BC > 0; BC = 0 reads
+// it at run time). Differences from the generic kernel above, each worth instructions per
+// voxel in an issue-bound loop:
+//  * a 4-bin histogram pad (HPAD): a voxel outside the lattice gets the intensity -1,
+//    whose bins clamp to rows -4..-1, all pad, so it needs no weight masking; with the
+//    masking gone the fixed-point scales fold into the B-spline coefficients;
+//  * per-unit row pointers for F, u and the records (one 64-bit add per row);
+//  * with BC > 0 every counter offset of the 4 x 4 footprint is an immediate.
+#ifndef FFDP_MI_PREF
+#define FFDP_MI_PREF 0
+#endif
+#ifndef FFDP_MI_L2PF
+#define FFDP_MI_L2PF 0
+#endif
+constexpr int HPAD = 4;
+// Fixed-point scale 2^S (S = FFDP_MI_BS_LOG2, odd):
+// both weights are pre-scaled by 2^(S-149)/2 so that kI * kJ lands at 2^S kI kJ * 2^-149.
+// A voxel adds at most (2/3)^2 * 2^S to one counter, so a copy takes 2^(32-S) * 2^11
+// voxels between folds without wrapping (S = 21: 4096, S = 23: 1024).
+#ifndef FFDP_MI_BS_LOG2
+#define FFDP_MI_BS_LOG2 23
+#endif
+constexpr int BS_LOG2 = FFDP_MI_BS_LOG2;
+static_assert(BS_LOG2 % 2 == 1 && BS_LOG2 <= 23, "odd scale exponent: equal pre-scales");
+constexpr float BS_WSCALE = BS_LOG2 == 23 ? 0x1p-63f : BS_LOG2 == 21 ? 0x1p-64f : BS_LOG2 == 19 ? 0x1p-65f : 0.0f;
+constexpr float BS_FIX_SCALE = (float)(1 << BS_LOG2);
+constexpr int BS_FOLD_VOX = 1024 << (23 - BS_LOG2);
+constexpr int BS_FOLD_ITERS = BS_FOLD_VOX / HVOX_PER_COPY_ITER > 0 ? BS_FOLD_VOX / HVOX_PER_COPY_ITER : 1;
+__host__ __device__ constexpr int bs_ld(int B) { return B + 2 * HPAD; }
+__host__ __device__ constexpr int bs_stride(int B) {
+    return ((bs_ld(B) * bs_ld(B) + 31) / 32) * 32 + (32 / HCOPY);
+}
+inline size_t bs_smem_bytes(int B) {
+    return sizeof(unsigned long long) * B * B + sizeof(uint32_t) * (size_t)HCOPY * bs_stride(B);
+}
+
+// Cubic B-spline weights of the 4 bins m_lo..m_lo+3 scaled by C (mi.hpp:28-140, bspline3),
+// the scale folded into the polynomial coefficients.
+template <int BC>
+__device__ __forceinline__ int32_t bspline_scaled(float v, int B, float C, float (&k)[4]) {
+    const float fb = BC > 0 ? (float)BC : (float)B;
+    const float s = fmaf(v, fb, -0.5f);
+    const float fl = floorf(s);
+    const float ph = s - fl;
+    const float q = 1.0f - ph;
+    const float p2 = ph * ph, p3 = p2 * ph;
+    k[0] = (q * q) * (q * (C / 6.0f));
+    k[1] = fmaf(3.0f * (C / 6.0f), p3, fmaf(-6.0f * (C / 6.0f), p2, 4.0f * (C / 6.0f)));
+    k[2] = fmaf(-3.0f * (C / 6.0f), p3, fmaf(3.0f * (C / 6.0f), p2, fmaf(3.0f * (C / 6.0f), ph, C / 6.0f)));
+    k[3] = p3 * (C / 6.0f);
+    const int32_t m = (__float_as_int(fl + 12582912.0f) - 0x4B400000) - 1;
+    return min(max(m, -HPAD), (BC > 0 ? BC : B) + HPAD - 4);
+}
+
+template <bool FULLWIN, bool REC, int BC, bool OFF32>
+__global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int B = BC > 0 ? BC : P.p.bins;
+    const int LD = bs_ld(B);
+    const int CS = bs_stride(B);
+    unsigned long long* s64 = reinterpret_cast<unsigned long long*>(smem);  // interior B x B
+    uint32_t* s32 = reinterpret_cast<uint32_t*>(smem + sizeof(unsigned long long) * B * B);
+    for (int i = threadIdx.x; i < B * B; i += HNT) s64[i] = 0ull;
+    for (int i = threadIdx.x; i < HCOPY * CS; i += HNT) s32[i] = 0u;
+    __syncthreads();
+    int miss = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* mine = s32 + (lane % HCOPY) * CS + HPAD * LD + HPAD;
+    const int64_t stride = (int64_t)gridDim.x * (HNT / 32);
+    const int64_t zrec = (P.z_begin - P.buf_z0) * P.plane;  // records cover the interior planes
+    // the unit's F and u: loaded one unit ahead (FFDP_MI_PREF) so that the next unit's
+    // loads are in flight during this unit's gathers and histogram updates
+    struct Ld {
+        Unit w;
+        float ff[4], uu[12];
+        bool ok[4];
+    };
+    auto load = [&](int64_t unit, Ld& L) {
+        L.w = unit_coords(P, (uint32_t)unit, lane);
+        const float* fp = P.f + L.w.bi;
+        const float* up = P.u + 3 * L.w.bi;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            L.ok[k] = L.w.vx && (L.w.y0 + k) < P.ny;
+            L.ff[k] = L.ok[k] ? __ldg(fp) : -1.0f;  // -1: every bin in the pad rows
+            L.uu[3 * k] = L.ok[k] ? __ldg(up) : 0.0f;
+            L.uu[3 * k + 1] = L.ok[k] ? __ldg(up + 1) : 0.0f;
+            L.uu[3 * k + 2] = L.ok[k] ? __ldg(up + 2) : 0.0f;
+            fp += P.nx;
+            up += 3 * P.nx;
+        }
+    };
+    Ld nx_;
+    if (FFDP_MI_PREF && (int64_t)blockIdx.x * (HNT / 32) + warp < P.nunits)
+        load((int64_t)blockIdx.x * (HNT / 32) + warp, nx_);
+    int iter = 0;
+    for (int64_t base = (int64_t)blockIdx.x * (HNT / 32); base < P.nunits; base += stride) {
+        const int64_t unit = base + warp;
+        if (unit < P.nunits) {
+            Ld L;
+            if (FFDP_MI_PREF)
+                L = nx_;
+            else
+                load(unit, L);
+            const Unit& w = L.w;
+            const float(&ff)[4] = L.ff;
+            const bool(&ok)[4] = L.ok;
+            float4* rp = P.rec + (w.bi - zrec);
+            if (FFDP_MI_L2PF > 0 && lane < 16) {
+                // pull the F and u lines of the unit FFDP_MI_L2PF iterations ahead into L2:
+                // lanes 0-11 take the 4 x 3 lines of u, lanes 12-15 the 4 lines of F
+                const int64_t ahead = unit + FFDP_MI_L2PF * stride;
+                if (ahead < P.nunits) {
+                    const Unit wa = unit_coords(P, (uint32_t)ahead, 0);
+                    const int row = lane < 12 ? lane / 3 : lane - 12;
+                    const char* a = lane < 12 ? reinterpret_cast<const char*>(P.u + 3 * (wa.bi + (int64_t)row * P.nx)) +
+                                                    128 * (lane % 3)
+                                              : reinterpret_cast<const char*>(P.f + wa.bi + (int64_t)row * P.nx);
+                    if (wa.y0 + row < P.ny) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                }
+            }
+            Cell c[4];
+            unit_cells(P, w, L.uu, c);
+            Corners cr[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN, OFF32>(P.g, c[k], miss);
+            if (FFDP_MI_PREF && unit + stride < P.nunits) load(unit + stride, nx_);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // Fixed point by a denormal product: with both weights pre-scaled by
+                // BS_WSCALE, kI * kJ lands at (2^S kI kJ) * 2^-149, whose IEEE bits ARE
+                // round(2^S kI kJ) (FMUL rounds to nearest; no -ftz).
+                float mw;
+                if (REC) {
+                    float d[3];
+                    mw = interp_grad(cr[k], c[k], d);
+#ifdef FFDP_EXP_NOREC
+                    if (ok[k] && d[0] == 1234.5f) *rp = make_float4(mw, d[0], d[1], d[2]);
+#else
+                    if (ok[k]) *rp = make_float4(mw, P.g.dscale[0] * d[0], P.g.dscale[1] * d[1], P.g.dscale[2] * d[2]);
+#endif
+                    rp += P.nx;
+                } else {
+                    mw = interp(cr[k], c[k]);
+                }
+                float kI[4], kJ[4];
+                const int32_t mi = bspline_scaled<BC>(ff[k], B, BS_WSCALE, kI);
+                const int32_t mj = bspline_scaled<BC>(mw, B, BS_WSCALE, kJ);
+                uint32_t* h = mine + mi * LD + mj;
+#ifdef FFDP_EXP_NOATOM
+                uint32_t x = 0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) x += __float_as_uint(kI[a] * kJ[b]);
+                if (x == 0x12345) h[0] = x;
+#else
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        atomicAdd(h + a * LD + b, __float_as_uint(kI[a] * kJ[b]));
+#endif
+            }
+        }
+        if (++iter == BS_FOLD_ITERS || base + stride >= P.nunits) {
+            // fold the interior B x B counters of every copy (pad counters take the weight of
+            // bins outside [0, B) and of voxels outside the lattice: never read, may wrap)
+            iter = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < B * B; i += HNT) {
+                const int q = (i / B + HPAD) * LD + (i % B) + HPAD;
                 unsigned long long acc = 0ull;
 #pragma unroll 8
                 for (int cp = 0; cp < HCOPY; ++cp) {
@@ -401,7 +593,8 @@ bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_ima
                           const ffdp_parzen& k) {
     // zero-bordered moving image, lane-private histogram copies within shared memory,
     // 32-bit unit indices and in-plane offsets
-    return m.pad == 2 && mstep::hist_smem_bytes(k.bins) <= mstep::kMaxHistSmem && (int64_t)d.nx * d.ny < (1LL << 31) &&
+    const size_t smem = k.kind == FFDP_PARZEN_BSPLINE3 ? mstep::bs_smem_bytes(k.bins) : mstep::hist_smem_bytes(k.bins);
+    return m.pad == 2 && smem <= mstep::kMaxHistSmem && (int64_t)d.nx * d.ny < (1LL << 31) &&
            ((d.nx + 31) / 32) * ((d.ny + 3) / 4) * (s.z_end - s.z_begin) < (1LL << 31);
 }
 
@@ -428,7 +621,7 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
     P.z_begin = s.z_begin;
     P.buf_z0 = s.buf_z0;
     P.nunits = (int64_t)P.nxb * P.nyq * (s.z_end - s.z_begin);
-    P.fix_scale = k.kind == FFDP_PARZEN_BSPLINE3 ? 8388608.0f : k.kind == FFDP_PARZEN_GAUSSIAN ? 4194304.0f
+    P.fix_scale = k.kind == FFDP_PARZEN_BSPLINE3 ? mstep::BS_FIX_SCALE : k.kind == FFDP_PARZEN_GAUSSIAN ? 4194304.0f
                                                                                                  : 2097152.0f;
     return P;
 }
@@ -445,12 +638,9 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     P.hist = h;
     P.miss = miss;
     P.rec = reinterpret_cast<float4*>(rec);
-    const size_t smem = hist_smem_bytes(B);
     static bool attr_set = false;  // opt in to > 48 KB dynamic shared memory, once
     if (!attr_set) {
-        for (auto fn : {k_step_mi_hist<true, true, false>, k_step_mi_hist<true, false, false>,
-                        k_step_mi_hist<false, true, false>, k_step_mi_hist<false, false, false>,
-                        k_step_mi_hist<true, true, true>, k_step_mi_hist<true, false, true>})
+        for (auto fn : {k_step_mi_hist<false, true, false>, k_step_mi_hist<false, false, false>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
         attr_set = true;
     }
@@ -459,18 +649,32 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool bs = k.kind == FFDP_PARZEN_BSPLINE3;
     if (rec && !bs) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
-    if (rec && full)
-        k_step_mi_hist<true, true, true><<<grid, HNT, smem, st>>>(P);
-    else if (rec)
-        k_step_mi_hist<true, false, true><<<grid, HNT, smem, st>>>(P);
-    else if (bs && full)
-        k_step_mi_hist<true, true, false><<<grid, HNT, smem, st>>>(P);
-    else if (bs)
-        k_step_mi_hist<true, false, false><<<grid, HNT, smem, st>>>(P);
-    else if (full)
-        k_step_mi_hist<false, true, false><<<grid, HNT, smem, st>>>(P);
-    else
-        k_step_mi_hist<false, false, false><<<grid, HNT, smem, st>>>(P);
+    if (bs) {
+        const size_t smem = bs_smem_bytes(B);
+        const bool o32 = window_off32(P.g);
+        const int sel = (full ? 1 : 0) | (rec ? 2 : 0) | (B == 32 ? 4 : 0) | (o32 ? 8 : 0);
+        static const decltype(&k_mi_hist_bs<true, true, 32, true>) table_[16] = {
+            k_mi_hist_bs<false, false, 0, false>,  k_mi_hist_bs<true, false, 0, false>,
+            k_mi_hist_bs<false, true, 0, false>,   k_mi_hist_bs<true, true, 0, false>,
+            k_mi_hist_bs<false, false, 32, false>, k_mi_hist_bs<true, false, 32, false>,
+            k_mi_hist_bs<false, true, 32, false>,  k_mi_hist_bs<true, true, 32, false>,
+            k_mi_hist_bs<false, false, 0, true>,   k_mi_hist_bs<true, false, 0, true>,
+            k_mi_hist_bs<false, true, 0, true>,    k_mi_hist_bs<true, true, 0, true>,
+            k_mi_hist_bs<false, false, 32, true>,  k_mi_hist_bs<true, false, 32, true>,
+            k_mi_hist_bs<false, true, 32, true>,   k_mi_hist_bs<true, true, 32, true>};
+        static bool bs_attr = false;
+        if (!bs_attr) {
+            for (auto fn : table_) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
+            bs_attr = true;
+        }
+        table_[sel]<<<grid, HNT, smem, st>>>(P);
+    } else {
+        const size_t smem = hist_smem_bytes(B);
+        if (full)
+            k_step_mi_hist<false, true, false><<<grid, HNT, smem, st>>>(P);
+        else
+            k_step_mi_hist<false, false, false><<<grid, HNT, smem, st>>>(P);
+    }
     k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
     if (!ws) scratch_free(h, st);
     return check_launch("step_mi_hist");
