@@ -215,8 +215,9 @@ class Stepper:
         else:
             self.kernel = voxreg.ParzenKernel.bspline3(bins)
         self.kernel_ms = {}
-        # lncc: sample, moments, partial-sum reduction (fused: 1); mi: hist, to_raw, finalize, grad
-        self.launches_per_step = (1 if self._lws is None else 3) if loss == "lncc" else 4
+        # lncc: sample, moments, partial-sum reduction (fused: 1); mi: pass 1 (finalize fused
+        # into its last CTA) and pass 2 (memsets of the histogram are not kernels of ours)
+        self.launches_per_step = (1 if self._lws is None else 3) if loss == "lncc" else 2
 
     def _p(self, t):
         return self.C.c_void_p(t.data_ptr())
@@ -254,15 +255,15 @@ class Stepper:
             return None
         self.ws.raw.zero_()
         ev[0].record()
-        lib.ffdp_step_mi_hist_rec(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win,
-                                  C.byref(self.args), C.byref(self.kernel.c), self._p(self.ws.raw),
-                                  self._p(self.ws.scratch), self._p(rec), None, s)
-        lib.ffdp_mi_finalize(self._p(self.ws.raw), self.bins, -1.0, self._p(self.ws.table), s)
+        # pass 1 with the finalize fused into its last CTA (what ffdp_step_mi launches)
+        lib.ffdp_step_mi_hist_final(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win,
+                                    C.byref(self.args), C.byref(self.kernel.c), self._p(self.ws.raw), -1.0,
+                                    self._p(self.ws.table), self._p(self.ws.scratch), self._p(rec), None, s)
         ev[1].record()
         lib.ffdp_step_mi_grad_rec(self._p(self.f), self.dims, self.slab, C.byref(self.kernel.c),
                                   self._p(self.ws.table), self._p(rec), self._p(self.g_u), s)
         ev[2].record()
-        return [("k_step_mi_hist+finalize", ev[0], ev[1]), ("k_step_mi_grad_rec", ev[1], ev[2])]
+        return [("k_mi_hist_bs", ev[0], ev[1]), ("k_step_mi_grad_rec", ev[1], ev[2])]
 
     def capture(self):
         """CUDA graph of one launch-only step: the timed loop replays it, so host launch

@@ -285,6 +285,19 @@ FFDP_API int ffdp_step_mi_hist_rec(const float* f, const float* u, ffdp_dims buf
                                    double* raw, void* workspace, float* rec, int32_t* miss, void* stream);
 
 /*
+ * Single-rank pass 1 with the finalize fused in: ffdp_step_mi_hist_rec, then the last
+ * CTA to finish converts the histogram into raw (joint entries overwritten; the caller
+ * zeroes the marginal entries) and runs ffdp_mi_finalize(raw, B, upstream, table)
+ * (mi.hpp:181-209, 369-390). workspace (ffdp_step_mi_workspace_bytes(B)) is required: it
+ * holds the fixed-point histogram and the CTA completion counter. For a sharded step use
+ * ffdp_step_mi_hist_rec + allreduce + ffdp_mi_finalize instead.
+ */
+FFDP_API int ffdp_step_mi_hist_final(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab,
+                                     ffdp_image_window m, const ffdp_sampler_args* args, const ffdp_parzen* kernel,
+                                     double* raw, double upstream, double* table, void* workspace, float* rec,
+                                     int32_t* miss, void* stream);
+
+/*
  * Pass 2 from the records: dL/dMw = sum_m kappa_i[m] sum_n ghat[m][n] omega_j[n]
  * (mi.hpp:392-421) with i = F, j = Mw, and g_u = record.xyz-part * dL/dMw
  * (sampler.hpp:221-230). Streams F and the records; no warp sampling.

@@ -98,6 +98,8 @@ _SIGS = {
     "ffdp_step_mi_record_bytes": (C.c_int64, [Dims, Slab]),
     "ffdp_step_mi_hist_rec": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC),
                                         C.POINTER(ParzenC), _vp, _vp, _vp, _vp, _vp]),
+    "ffdp_step_mi_hist_final": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC),
+                                          C.POINTER(ParzenC), _vp, C.c_double, _vp, _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_grad_rec": (C.c_int, [_vp, Dims, Slab, C.POINTER(ParzenC), _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_grad": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
                                     _vp, _vp, _vp, _vp]),

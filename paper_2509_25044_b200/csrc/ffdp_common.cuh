@@ -427,6 +427,95 @@ __device__ __forceinline__ double block_sum(double v, double* smem /* NT/32 */) 
     return r;
 }
 
+// finalize_histogram + histogram_mi + the ghat table of mi_backward_impl
+// (mi.hpp:181-209, 369-390) by one CTA (blockDim a multiple of 32, >= B) from the raw
+// joint histogram in shared memory (rs[B*B], overwritten with p_ij), in a fixed reduction
+// order. table = p_ij[B*B], p_i[B], p_j[B], ghat[B*B], {z, mi, dot, 0}. Marginals come
+// from p_ij (mi.hpp:181-196): one warp per row / column, shuffle sums.
+__device__ __forceinline__ void mi_finalize_block(double* rs, int B, double upstream, double* __restrict__ table,
+                                                  double* red /* >= 34 doubles of shared scratch */) {
+    const int nb2 = B * B, nt = blockDim.x, nw = nt >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* pij = table;
+    double* pi = table + nb2;
+    double* pj = pi + B;
+    double* gh = pj + B;
+    double* sc = gh + nb2;
+    double acc = 0;
+    for (int q = threadIdx.x; q < nb2; q += nt) acc += rs[q];
+    acc = warp_sum(acc);
+    __syncthreads();
+    if (lane == 0) red[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double z = 0;
+        for (int i = 0; i < nw; ++i) z += red[i];
+        red[32] = z;
+    }
+    __syncthreads();
+    const double z = red[32];
+    for (int q = threadIdx.x; q < nb2; q += nt) {
+        const double p = rs[q] / z;
+        rs[q] = p;
+        pij[q] = p;
+    }
+    __syncthreads();
+    // row m / column m sums: warp m, lanes stride the B entries in a fixed order
+    for (int m = w; m < B; m += nw) {
+        double r = 0, c = 0;
+        for (int n = lane; n < B; n += 32) {
+            r += rs[m * B + n];
+            c += rs[n * B + m];
+        }
+        r = warp_sum(r);
+        c = warp_sum(c);
+        if (lane == 0) {
+            pi[m] = r;
+            pj[m] = c;
+            red[34 + m] = r;       // shared copies of the marginals for the log terms
+            red[34 + B + m] = c;
+        }
+    }
+    __syncthreads();
+    double mi = 0, dot = 0;
+    for (int q = threadIdx.x; q < nb2; q += nt) {
+        const double p = rs[q];
+        double g = 0;
+        if (p > 0) {
+            const double l = log(p / (red[34 + q / B] * red[34 + B + q % B]));
+            mi += p * l;
+            g = l - 1.0;
+            dot += g * p;
+        }
+        rs[q] = g;
+    }
+    mi = warp_sum(mi);
+    dot = warp_sum(dot);
+    __syncthreads();
+    if (lane == 0) {
+        red[w] = mi;
+        red[32 + 2 * B + 34 + w] = dot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0, d = 0;
+        for (int i = 0; i < nw; ++i) {
+            s += red[i];
+            d += red[32 + 2 * B + 34 + i];
+        }
+        sc[0] = z;
+        sc[1] = s;
+        sc[2] = d;
+        sc[3] = 0;
+        red[33] = d;
+    }
+    __syncthreads();
+    const double dt = red[33];
+    for (int q = threadIdx.x; q < nb2; q += nt) gh[q] = pij[q] > 0 ? upstream * (rs[q] - dt) / z : 0.0;
+}
+// shared scratch doubles mi_finalize_block needs for B bins and nt threads
+__host__ __device__ constexpr int mi_finalize_scratch(int B, int nt) { return 34 + 2 * B + 32 + nt / 32; }
+
 }  // namespace ffdp
 
 // ------------------------------------------------------------------ host helpers

@@ -217,75 +217,10 @@ __global__ void k_mi_approx_conv(const unsigned long long* cnt, int B, ParzenDev
 // reduction order. table = p_ij[B*B], p_i[B], p_j[B], ghat[B*B], {z, mi, dot, 0}.
 __global__ void __launch_bounds__(1024) k_mi_finalize(const double* __restrict__ raw, int B, double upstream,
                                                       double* __restrict__ table) {
-    __shared__ double red[32];
-    __shared__ double s_z, s_dot;
-    const int nb2 = B * B;
-    double* pij = table;
-    double* pi = table + nb2;
-    double* pj = pi + B;
-    double* gh = pj + B;
-    double* sc = gh + nb2;
-    double acc = 0;
-    for (int q = threadIdx.x; q < nb2; q += blockDim.x) acc += raw[q];
-    // block sum in a fixed order
-    acc = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double z = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) z += red[w];
-        s_z = z;
-    }
-    __syncthreads();
-    const double z = s_z;
-    for (int q = threadIdx.x; q < nb2; q += blockDim.x) pij[q] = raw[q] / z;
-    __syncthreads();
-    for (int m = threadIdx.x; m < B; m += blockDim.x) {
-        double r = 0, c = 0;
-        for (int nn = 0; nn < B; ++nn) {
-            r += pij[m * B + nn];
-            c += pij[nn * B + m];
-        }
-        pi[m] = r;
-        pj[m] = c;
-    }
-    __syncthreads();
-    double mi = 0, dot = 0;
-    for (int q = threadIdx.x; q < nb2; q += blockDim.x) {
-        const double p = pij[q];
-        double g = 0;
-        if (p > 0) {
-            const double l = log(p / (pi[q / B] * pj[q % B]));
-            mi += p * l;
-            g = l - 1.0;
-            dot += g * p;
-        }
-        gh[q] = g;
-    }
-    mi = warp_sum(mi);
-    dot = warp_sum(dot);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mi;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-        sc[1] = s;
-    }
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-        s_dot = s;
-        sc[0] = z;
-        sc[2] = s;
-        sc[3] = 0;
-    }
-    __syncthreads();
-    const double dt = s_dot;
-    for (int q = threadIdx.x; q < nb2; q += blockDim.x) gh[q] = pij[q] > 0 ? upstream * (gh[q] - dt) / z : 0.0;
+    __shared__ double rs[kMaxBins * kMaxBins];
+    __shared__ double red[mi_finalize_scratch(kMaxBins, 1024)];
+    for (int q = threadIdx.x; q < B * B; q += blockDim.x) rs[q] = raw[q];
+    mi_finalize_block(rs, B, upstream, table, red);
 }
 
 // d(loss)/dI and d(loss)/dJ per voxel with compact support (mi.hpp:392-421).
@@ -449,7 +384,8 @@ bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_ima
                           const ffdp_parzen& k);
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
-                 int32_t* miss, cudaStream_t st, float* rec = nullptr);
+                 int32_t* miss, cudaStream_t st, float* rec = nullptr, double* table = nullptr,
+                 double upstream = -1.0);
 int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ffdp_parzen& k, const double* table,
                 const float* rec, float* g_u, cudaStream_t st);
 int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
@@ -557,6 +493,13 @@ int ffdp_step_mi(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_
     const int B = kernel->bins;
     cudaMemsetAsync(raw, 0, sizeof(double) * (B * B + 2 * B), (cudaStream_t)stream);
     const bool use_rec = rec && kernel->kind == FFDP_PARZEN_BSPLINE3 && mi_quad_path_applies(d, s, m, *kernel);
+    if (use_rec && workspace) {
+        // one rank, caller workspace: pass 1 with the finalize fused into its last CTA
+        if (int rc = ffdp_step_mi_hist_final(f, u, d, s, m, args, kernel, raw, -1.0, table, workspace, rec, miss,
+                                             stream))
+            return rc;
+        return ffdp_step_mi_grad_rec(f, d, s, kernel, table, rec, g_u, stream);
+    }
     if (use_rec) {
         if (int rc = ffdp_step_mi_hist_rec(f, u, d, s, m, args, kernel, raw, workspace, rec, miss, stream)) return rc;
         if (int rc = ffdp_mi_finalize(raw, B, -1.0, table, stream)) return rc;
@@ -585,6 +528,23 @@ int ffdp_step_mi_hist_rec(const float* f, const float* u, ffdp_dims d, ffdp_slab
         return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need a zero-bordered moving window (pad = 2)");
     return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, (unsigned long long*)workspace, miss,
                         (cudaStream_t)stream, rec);
+}
+
+int ffdp_step_mi_hist_final(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_image_window m,
+                            const ffdp_sampler_args* args, const ffdp_parzen* kernel, double* raw, double upstream,
+                            double* table, void* workspace, float* rec, int32_t* miss, void* stream) {
+    if (int rc = check_parzen(kernel)) return rc;
+    if (int rc = check_slab_mi(d, s)) return rc;
+    const char* why = nullptr;
+    if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
+    if (!f || !u || !raw || !table || !workspace || !m.data || !rec)
+        return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
+    if (kernel->kind != FFDP_PARZEN_BSPLINE3)
+        return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
+    if (!mi_quad_path_applies(d, s, m, *kernel))
+        return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need a zero-bordered moving window (pad = 2)");
+    return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, (unsigned long long*)workspace, miss,
+                        (cudaStream_t)stream, rec, table, upstream);
 }
 
 int ffdp_step_mi_grad_rec(const float* f, ffdp_dims d, ffdp_slab s, const ffdp_parzen* kernel, const double* table,

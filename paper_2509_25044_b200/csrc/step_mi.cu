@@ -35,6 +35,10 @@ struct Params {
     const double* table;
     float4* rec;               // pass-1 records (Mw, dscale * dMw/dfrac) per interior voxel, or null
     unsigned long long* hist;  // global u64 [B*B]
+    unsigned int* done;        // fused finalize: CTA completion counter (after hist), or null
+    double* fin_table;         // fused finalize: ffdp_mi_finalize's table, or null (separate finalize)
+    double* raw_out;           // fused finalize: raw joint histogram out (may be null)
+    double upstream;
     int32_t* miss;
     int32_t nx, ny, nxb, nyq;  // lattice, 32-wide x blocks, 4-row groups
     FastDiv div_nxb, div_nyq;
@@ -168,7 +172,7 @@ __host__ __device__ constexpr int hist_ld(int B) { return B + 2 * PAD; }
 __host__ __device__ constexpr int hist_stride(int B) {
     return ((hist_ld(B) * hist_ld(B) + 31) / 32) * 32 + (32 / HCOPY);
 }
-constexpr size_t kMaxHistSmem = 227 * 1024;
+constexpr size_t kMaxHistSmem = 226 * 1024;  // leaves room for the static shared variables
 inline size_t hist_smem_bytes(int B) {
     return sizeof(unsigned long long) * B * B + sizeof(uint32_t) * (size_t)HCOPY * hist_stride(B);
 }
@@ -457,6 +461,29 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
     }
     const unsigned anym = __ballot_sync(0xffffffffu, miss);
     if (anym && P.miss && (threadIdx.x & 31) == 0) atomicAdd(P.miss, __popc(anym));
+    if (P.fin_table) {
+        // fused finalize (single-rank step): the last CTA to finish converts the global
+        // histogram, runs finalize_histogram / histogram_mi / the ghat table
+        // (mi_finalize_block) and leaves the histogram and the counter zeroed
+        __shared__ unsigned s_last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            double* rs = reinterpret_cast<double*>(smem);  // the s64 area: B*B doubles
+            const double inv = 1.0 / (double)P.fix_scale;
+            for (int i = threadIdx.x; i < B * B; i += HNT) {
+                const double v = (double)__ldcg(&P.hist[i]) * inv;
+                rs[i] = v;
+                if (P.raw_out) P.raw_out[i] = v;
+                P.hist[i] = 0ull;
+            }
+            if (threadIdx.x == 0) *P.done = 0u;
+            mi_finalize_block(rs, B, P.upstream, P.fin_table, reinterpret_cast<double*>(s32));
+        }
+    }
 }
 
 // ------------------------------------------------------------------ pass 2
@@ -524,17 +551,26 @@ __global__ void __launch_bounds__(NT, 3) k_step_mi_grad(const Params P) {
 // Pass 2 from the pass-1 records: F and (Mw, dscale * dMw/dfrac) are streamed, dL/dMw
 // from the ghat table (mi.hpp:392-421, B-spline), g_u = record.yzw * dL/dMw. No gather,
 // no coordinates: 32 B/voxel of pure streaming (F 4 + record 16 in, g_u 12 out).
-// VEC: 4 voxels per thread with 16-byte loads and stores (aligned buffers).
+// The ghat table sits in shared memory as 4 column-shifted copies (copy c holds
+// ghat_pad[r][k + c]), so the 4 consecutive bins n0..n0+3 of a row are one aligned
+// 16-byte load from copy n0 % 4: 4 LDS.128 per voxel instead of 16 scalar loads.
+// VEC: 4 voxels per thread with 16-byte loads and stores (aligned buffers), two groups
+// in flight per iteration.
+__host__ __device__ constexpr int grad_tab_floats(int B) { return 4 * (B + 2 * PAD) * ((B + 2 * PAD + 3) / 4 * 4); }
+
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_step_mi_grad_rec(const float* __restrict__ f, const float4* __restrict__ rec,
                                                           float* __restrict__ g_u, int64_t n, const double* table,
                                                           int B) {
     extern __shared__ __align__(16) float sg[];
-    const int LD = B + 2 * PAD;
+    const int LD = B + 2 * PAD;            // rows
+    const int CP = (LD + 3) / 4 * 4;       // row pitch (floats)
+    const int CS = LD * CP;                // copy size
     {
         const double* gh = table + B * B + 2 * B;
-        for (int q = threadIdx.x; q < LD * LD; q += blockDim.x) {
-            const int m = q / LD - PAD, nn = q % LD - PAD;
+        for (int q = threadIdx.x; q < 4 * CS; q += blockDim.x) {
+            const int c = q / CS, r = (q % CS) / CP, k = q % CP;
+            const int m = r - PAD, nn = k + c - PAD;
             sg[q] = (m >= 0 && m < B && nn >= 0 && nn < B) ? (float)gh[m * B + nn] : 0.0f;
         }
         __syncthreads();
@@ -542,14 +578,16 @@ __global__ void __launch_bounds__(256) k_step_mi_grad_rec(const float* __restric
     auto dl = [&](float fv, float mw) {
         const BS4 bi = bspline_bins<false>(fv, B);
         const BS4 bj = bspline_bins<true>(mw, B);
-        const float* gr = sg + (bi.m_lo + PAD) * LD + (bj.m_lo + PAD);
+        const int n0 = bj.m_lo + PAD;
+        const float4* gr = reinterpret_cast<const float4*>(sg + (n0 & 3) * CS + (bi.m_lo + PAD) * CP + (n0 & ~3));
         float gj = 0.0f;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-            float acc = gr[a * LD] * bj.w[0];
-            acc = fmaf(gr[a * LD + 1], bj.w[1], acc);
-            acc = fmaf(gr[a * LD + 2], bj.w[2], acc);
-            acc = fmaf(gr[a * LD + 3], bj.w[3], acc);
+            const float4 g = gr[a * (CP / 4)];
+            float acc = g.x * bj.w[0];
+            acc = fmaf(g.y, bj.w[1], acc);
+            acc = fmaf(g.z, bj.w[2], acc);
+            acc = fmaf(g.w, bj.w[3], acc);
             gj = fmaf(bi.k[a], acc, gj);
         }
         return gj;
@@ -559,15 +597,29 @@ __global__ void __launch_bounds__(256) k_step_mi_grad_rec(const float* __restric
     int64_t done = 0;
     if (VEC) {
         const int64_t n4 = n / 4;
-        for (int64_t i = tid; i < n4; i += stride) {
-            const float4 fv = __ldg(reinterpret_cast<const float4*>(f) + i);
-            const float4 r0 = __ldg(rec + 4 * i), r1 = __ldg(rec + 4 * i + 1), r2 = __ldg(rec + 4 * i + 2),
-                         r3 = __ldg(rec + 4 * i + 3);
+        auto group = [&](const float4 fv, const float4 r0, const float4 r1, const float4 r2, const float4 r3,
+                         int64_t i) {
             const float g0 = dl(fv.x, r0.x), g1 = dl(fv.y, r1.x), g2 = dl(fv.z, r2.x), g3 = dl(fv.w, r3.x);
             float4* o = reinterpret_cast<float4*>(g_u + 12 * i);
             o[0] = make_float4(r0.y * g0, r0.z * g0, r0.w * g0, r1.y * g1);
             o[1] = make_float4(r1.z * g1, r1.w * g1, r2.y * g2, r2.z * g2);
             o[2] = make_float4(r2.w * g2, r3.y * g3, r3.z * g3, r3.w * g3);
+        };
+        int64_t i = tid;
+        for (; i + stride < n4; i += 2 * stride) {
+            const int64_t j = i + stride;
+            const float4 fa = __ldg(reinterpret_cast<const float4*>(f) + i);
+            const float4 fb = __ldg(reinterpret_cast<const float4*>(f) + j);
+            const float4 a0 = __ldg(rec + 4 * i), a1 = __ldg(rec + 4 * i + 1), a2 = __ldg(rec + 4 * i + 2),
+                         a3 = __ldg(rec + 4 * i + 3);
+            const float4 b0 = __ldg(rec + 4 * j), b1 = __ldg(rec + 4 * j + 1), b2 = __ldg(rec + 4 * j + 2),
+                         b3 = __ldg(rec + 4 * j + 3);
+            group(fa, a0, a1, a2, a3, i);
+            group(fb, b0, b1, b2, b3, j);
+        }
+        for (; i < n4; i += stride) {
+            const float4 fa = __ldg(reinterpret_cast<const float4*>(f) + i);
+            group(fa, __ldg(rec + 4 * i), __ldg(rec + 4 * i + 1), __ldg(rec + 4 * i + 2), __ldg(rec + 4 * i + 3), i);
         }
         done = n4 * 4;
     }
@@ -610,6 +662,10 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
     P.table = nullptr;
     P.rec = nullptr;
     P.hist = nullptr;
+    P.done = nullptr;
+    P.fin_table = nullptr;
+    P.raw_out = nullptr;
+    P.upstream = -1.0;
     P.miss = nullptr;
     P.nx = (int32_t)d.nx;
     P.ny = (int32_t)d.ny;
@@ -628,14 +684,22 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
 
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
-                 int32_t* miss, cudaStream_t st, float* rec) {
+                 int32_t* miss, cudaStream_t st, float* rec, double* table, double upstream) {
     using namespace mstep;
     Params P = make_params(f, u, d, s, m, args, k);
     const int B = k.bins;
+    // fused finalize (table != null): B-spline pass 1 only, workspace holds the counter
+    const bool fin = table && ws && k.kind == FFDP_PARZEN_BSPLINE3;
     unsigned long long* h = ws ? ws : (unsigned long long*)scratch_alloc(sizeof(unsigned long long) * B * B, st);
     if (!h) return set_error(FFDP_CUDA, "step_mi: scratch allocation failed");
-    cudaMemsetAsync(h, 0, sizeof(unsigned long long) * B * B, st);
+    cudaMemsetAsync(h, 0, sizeof(unsigned long long) * (B * B + (fin ? 1 : 0)), st);
     P.hist = h;
+    if (fin) {
+        P.done = reinterpret_cast<unsigned int*>(h + B * B);
+        P.fin_table = table;
+        P.raw_out = raw;
+        P.upstream = upstream;
+    }
     P.miss = miss;
     P.rec = reinterpret_cast<float4*>(rec);
     static bool attr_set = false;  // opt in to > 48 KB dynamic shared memory, once
@@ -675,7 +739,7 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
         else
             k_step_mi_hist<false, false, false><<<grid, HNT, smem, st>>>(P);
     }
-    k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
+    if (!fin) k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
     if (!ws) scratch_free(h, st);
     return check_launch("step_mi_hist");
 }
@@ -713,7 +777,13 @@ int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ff
     const int B = k.bins;
     const float* fi = f + (s.z_begin - s.buf_z0) * d.nx * d.ny;  // interior planes
     const int64_t n = d.nx * d.ny * (s.z_end - s.z_begin);
-    const size_t smem = sizeof(float) * (B + 2 * PAD) * (B + 2 * PAD);
+    const size_t smem = sizeof(float) * grad_tab_floats(B);
+    static bool attr_set = false;  // B up to 64: the 4 table copies may exceed 48 KB
+    if (!attr_set) {
+        for (auto fn : {k_step_mi_grad_rec<true>, k_step_mi_grad_rec<false>})
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * grad_tab_floats(64)));
+        attr_set = true;
+    }
     const bool vec = (((uintptr_t)fi | (uintptr_t)rec | (uintptr_t)g_u) & 15) == 0;
     const int64_t work = vec ? n / 4 : n;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8LL * num_sms()));
