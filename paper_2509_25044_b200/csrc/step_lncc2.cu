@@ -22,6 +22,10 @@
 
 #include "ffdp_common.cuh"
 
+#ifndef FFDP_L2_PREDLOAD
+#define FFDP_L2_PREDLOAD 1
+#endif
+
 namespace ffdp {
 namespace l2 {
 
@@ -164,10 +168,9 @@ struct Tile {
     };
 };
 
-__device__ __forceinline__ float win_count(int64_t g, int64_t n) {
-    const int64_t lo = g - R < 0 ? 0 : g - R;
-    const int64_t hi = g + R >= n ? n - 1 : g + R;
-    return (float)(hi - lo + 1);
+// in-lattice extent of the window of position g along an axis of n voxels (< 2^31)
+__device__ __forceinline__ float win_count(int32_t g, int32_t n) {
+    return (float)(min(g + R, n - 1) - max(g - R, 0) + 1);
 }
 
 template <int TX, int TY>
@@ -198,19 +201,31 @@ __device__ __forceinline__ void load_plane(const MParams& P, const int32_t (&off
     const int64_t zoff = in ? (p - P.buf_z0) * P.plane : 0;
     const float* fp = P.f + zoff;
     const float* mp = P.mw + zoff;
+    // opaque plane bases: each load address is then one wide multiply-add of the offset
+    asm("" : "+l"(fp), "+l"(mp));
 #pragma unroll
     for (int k = 0; k < T::KPOS; ++k) {
+        // off < 0 (outside the lattice): load a valid element and discard it, so the loads
+        // need no predicate and no 64-bit select
+#if FFDP_L2_PREDLOAD
+        const bool ok = in && off[k] >= 0;
+        const uint32_t o = (uint32_t)off[k];
+        pf.v[k] = ok ? make_float2(__ldg(fp + o), __ldg(mp + o)) : make_float2(P.sf, 0.f);
+#else
+        const uint32_t o = (uint32_t)max(off[k], 0);
+        const float a = __ldg(fp + o), b = __ldg(mp + o);
         const bool ok = in && off[k] >= 0;
         // consumed one plane later (register ping-pong): no arithmetic on the loaded values here
-        pf.v[k] = ok ? make_float2(__ldg(fp + off[k]), __ldg(mp + off[k])) : make_float2(P.sf, 0.f);
+        pf.v[k] = ok ? make_float2(a, b) : make_float2(P.sf, 0.f);
+#endif
     }
 }
 
 template <int TX, int TY, int SLOT>
 __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::Smem& sm, Pref2<TX, TY> (&pf)[2],
                                        const int32_t (&off)[Tile<TX, TY>::KPOS], const int32_t (&out_off)[2],
-                                       double (&Z)[2][5], double& nsum, int64_t p, int64_t pstart, int64_t pend,
-                                       int x0, int y0, int64_t zc0) {
+                                       const float (&cxy)[2], double (&Z)[2][5], double& nsum, int64_t p,
+                                       int64_t pstart, int64_t pend, int64_t zc0) {
     using T = Tile<TX, TY>;
     if (p >= pend) return;  // uniform across the CTA
     const int t = threadIdx.x;
@@ -276,13 +291,13 @@ __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::
         s += sm.X[ch][oy0 + WIN][ox] - sm.X[ch][oy0][ox];
         Z[1][ch] += (double)s;
     }
+    const float cz = win_count((int32_t)q, (int32_t)P.nz_global);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int oy = oy0 + j;
-        const int gx = x0 + ox, gy = y0 + oy;
         if (emit && out_off[j] >= 0) {
             const float2 fm = sm.raw[slot_q][oy + R][ox + R];
-            const float cw = win_count(gx, P.nx) * win_count(gy, P.ny) * win_count(q, P.nz_global);
+            const float cw = cxy[j] * cz;
             const double inv = 1.0 / (double)(WIN * WIN * WIN);
             const double W = (double)cw * inv;
             const double Sf = Z[j][0], Sm = Z[j][1];
@@ -339,18 +354,20 @@ __global__ void __launch_bounds__(Tile<TX, TY>::NT, FFDP_L2_MINB) k_lncc_moments
     double nsum = 0.0;
     const int64_t pstart = zc0 - R, pend = zc1 + R;
     int32_t off[T::KPOS], out_off[2];
+    float cxy[2];  // in-lattice x * y extent of the output's window (zero-padded border)
     plane_offsets<TX, TY>(P, threadIdx.x, x0, y0, off);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int gx = x0 + (int)threadIdx.x % TX, gy = y0 + 2 * ((int)threadIdx.x / TX) + j;
         out_off[j] = (gx < P.nx && gy < P.ny) ? 3 * (gy * P.nx + gx) : -1;
+        cxy[j] = win_count(gx, P.nx) * win_count(gy, P.ny);
     }
     Pref2<TX, TY> pf[2];
     load_plane<TX, TY>(P, off, pstart, pf[0]);
     __syncthreads();
     for (int64_t p = pstart; p < pend; p += 2) {
-        mplane<TX, TY, 0>(P, sm, pf, off, out_off, Z, nsum, p, pstart, pend, x0, y0, zc0);
-        mplane<TX, TY, 1>(P, sm, pf, off, out_off, Z, nsum, p + 1, pstart, pend, x0, y0, zc0);
+        mplane<TX, TY, 0>(P, sm, pf, off, out_off, cxy, Z, nsum, p, pstart, pend, zc0);
+        mplane<TX, TY, 1>(P, sm, pf, off, out_off, cxy, Z, nsum, p + 1, pstart, pend, zc0);
     }
     __shared__ double red[T::NT / 32];
     nsum = block_sum<T::NT>(nsum, red);
