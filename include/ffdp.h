@@ -145,6 +145,29 @@ FFDP_API int ffdp_sampler_bwd(const float* upstream, ffdp_image_window img, cons
 FFDP_API int ffdp_convolve_axis(const float* in, float* out, ffdp_dims dims, int channels, int axis, const double* taps,
                        int ntaps, int mode, int64_t lo_global, int64_t n_global, void* stream);
 
+/*
+ * gp_convolve (distops.hpp:54-101; separable_convolve, smoothing.hpp:98-105) of a z-slab:
+ * x, y and z passes of the (odd, <= 9) host taps over a 1- or 3-channel field in one
+ * z-marching kernel. `in` holds buffer planes [buf_z0, buf_z0 + buf_nz) (buf_dims.nz =
+ * buf_nz), which must include the ntaps/2 halo planes on each side that exist in the
+ * global lattice (the halo exchange's job, fabric.hpp:315-370); `out` receives planes
+ * [z_begin, z_end). mode 0 = zero_pad, 1 = renormalize (EdgeMode, smoothing.hpp:17-23).
+ * Taps depend only on global coordinates, so a sharded call equals the unsharded one.
+ */
+FFDP_API int ffdp_gp_convolve(const float* in, float* out, ffdp_dims buf_dims, ffdp_slab slab, int channels,
+                              const double* taps, int ntaps, int mode, void* stream);
+
+/*
+ * The gradient half of the warp update (registration.hpp:313-316) fused:
+ * g_s = gp_convolve(g_u, taps, renormalize) (g_u buffer planes incl. halo, as `in`
+ * above) and adam_step(u, g_s, {m1, m2, step}, lr) (adam.hpp:30-50) on the interior
+ * planes of u, m1, m2 (updated in place; the smoothed gradient never reaches HBM).
+ * step = the Adam step counter after this update (1 on the first call).
+ */
+FFDP_API int ffdp_sobolev_adam(const float* g_u, float* u, float* m1, float* m2, ffdp_dims buf_dims, ffdp_slab slab,
+                               const double* taps, int ntaps, double lr, double beta1, double beta2, double eps,
+                               int64_t step, void* stream);
+
 /* -------------------------------------------------------------------------- LNCC */
 
 /*

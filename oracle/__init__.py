@@ -119,6 +119,10 @@ class Oracle:
         L.or_rng_uniform_int.argtypes = [C.POINTER(Rng), C.c_int64, C.c_int64]
         L.or_rng_uniform_int.restype = C.c_int64
         L.or_random_volume.argtypes = [C.POINTER(Rng), _dp, C.c_int64, C.c_double, C.c_double]
+        L.or_adam_step.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double,
+                                   C.c_int64]
+        L.or_warp_update.argtypes = [_dp, _dp, _dp, _dp, Dims, C.c_double, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, C.c_double, C.c_int64]
 
     # -- sampler (sampler.hpp:165-300) -------------------------------------------------
     def sample(self, img, u=None, A=None, t=None, S=None, bounds=None, out_shape=None, upstream=None,
@@ -178,6 +182,23 @@ class Oracle:
         self.lib.or_separable_convolve(_p(d), _dims_of(d.shape), channels, _p(taps), len(taps),
                                        1 if mode == "renormalize" else 0)
         return d
+
+    # -- warp update (adam.hpp:30-50, registration.hpp:313-317) ------------------------
+    def adam_step(self, param, grad, m1, m2, lr, step, beta1=0.9, beta2=0.999, eps=1e-8):
+        """Returns (param, m1, m2) after adam_step; step = the state counter after it."""
+        p, g, a, b = (_f64(x).copy() for x in (param, grad, m1, m2))
+        self.lib.or_adam_step(_p(p), _p(g), _p(a), _p(b), p.size, lr, beta1, beta2, eps, step)
+        return p, a, b
+
+    def warp_update(self, g_u, u, m1, m2, lr, step, sigma_grad=1.0, sigma_warp=0.5, beta1=0.9, beta2=0.999,
+                    eps=1e-8):
+        """One deformable warp update on one rank: returns (u, m1, m2)."""
+        g = _f64(g_u)
+        uu, a, b = (_f64(x).copy() for x in (u, m1, m2))
+        if self.lib.or_warp_update(_p(g), _p(uu), _p(a), _p(b), _dims_of(uu.shape[:3]), sigma_grad, sigma_warp, lr,
+                                   beta1, beta2, eps, step):
+            raise ValueError("warp_update: bad sigma")
+        return uu, a, b
 
     # -- LNCC (lncc.hpp:144-280) ---------------------------------------------------------
     def lncc_forward(self, f, m, window=7, eps=1e-5, want_map=False):
@@ -318,6 +339,8 @@ class Reference:
         L.ref_parzen_eval.argtypes = [C.c_int, C.c_int, C.c_double, _dp, C.c_int64, _dp, _dp]
         L.ref_synth_pair.argtypes = [C.c_uint64, _i64p, C.c_int, C.c_double, _dp, _dp, _dp]
         L.ref_gp_convolve.argtypes = [_dp, _i64p, C.c_int, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.ref_warp_update.argtypes = [_dp, _dp, _dp, _dp, _i64p, C.c_double, C.c_double, C.c_double, C.c_int64,
+                                      C.c_int]
         L.ref_step.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _i64p, _dp, _dp, C.c_int, C.c_double, C.c_int,
                                C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
 
@@ -393,6 +416,14 @@ class Reference:
         self._check(self.lib.ref_gp_convolve(_p(v), _arr_dims(v.shape), channels, _p(taps), len(taps),
                                              int(renormalize), int(sync), world, _p(out)))
         return out
+
+    def warp_update(self, g_u, u, m1, m2, lr, step, sigma_grad=1.0, sigma_warp=0.5, world=1):
+        """registration.hpp:313-317 over `world` ranks (gp_convolve halos): (u, m1, m2)."""
+        g = _f64(g_u)
+        uu, a, b = (_f64(x).copy() for x in (u, m1, m2))
+        self._check(self.lib.ref_warp_update(_p(g), _p(uu), _p(a), _p(b), _arr_dims(uu.shape[:3]), sigma_grad,
+                                             sigma_warp, lr, step, world))
+        return uu, a, b
 
     def step(self, loss_kind, f, m, u, A=None, t=None, window=7, eps=1e-5, ants=True, bins=32, kind="bspline3",
              approx=False, world=1, fp32=False):

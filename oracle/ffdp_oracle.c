@@ -315,6 +315,40 @@ OR_API int or_gaussian_smooth(double* data, or_dims dims, int channels, double s
     return 0;
 }
 
+/* adam_step (adam.hpp:30-50): bias-corrected Adam over a flat buffer, fp64 arithmetic;
+ * `step` is the state's step counter AFTER the increment (1 on the first call). */
+OR_API void or_adam_step(double* param, const double* grad, double* m1, double* m2, int64_t n, double lr,
+                         double beta1, double beta2, double eps, int64_t step) {
+    const double c1 = 1.0 - pow(beta1, (double)step);
+    const double c2 = 1.0 - pow(beta2, (double)step);
+    for (int64_t i = 0; i < n; ++i) {
+        const double g = grad[i];
+        const double m = beta1 * m1[i] + (1.0 - beta1) * g;
+        const double v = beta2 * m2[i] + (1.0 - beta2) * g * g;
+        m1[i] = m;
+        m2[i] = v;
+        param[i] = param[i] - lr * (m / c1) / (sqrt(v / c2) + eps);
+    }
+}
+
+/* The warp update of one deformable iteration (registration.hpp:313-317) on one rank:
+ * g_s = separable renormalized Gaussian(sigma_grad) of g_u; adam_step(u, g_s);
+ * u = separable renormalized Gaussian(sigma_warp) of u. g_u is not modified. */
+OR_API int or_warp_update(const double* g_u, double* u, double* m1, double* m2, or_dims dims, double sigma_grad,
+                          double sigma_warp, double lr, double beta1, double beta2, double eps, int64_t step) {
+    double tg[4096], tw[4096];
+    const int ng = or_gaussian_taps(sigma_grad, tg, 4096), nw = or_gaussian_taps(sigma_warp, tw, 4096);
+    if (ng < 0 || nw < 0) return 1;
+    const int64_t n = 3 * dims_voxels(dims);
+    double* gs = (double*)malloc((size_t)n * sizeof(double));
+    memcpy(gs, g_u, (size_t)n * sizeof(double));
+    or_separable_convolve(gs, dims, 3, tg, ng, 1);
+    or_adam_step(u, gs, m1, m2, n, lr, beta1, beta2, eps, step);
+    or_separable_convolve(u, dims, 3, tw, nw, 1);
+    free(gs);
+    return 0;
+}
+
 /* ------------------------------------------------------------- lncc.hpp:63-90 */
 static inline double lncc_ncc(double muf, double mum, double muff, double mumm, double mufm, double eps) {
     const double a = mufm - muf * mum;

@@ -265,6 +265,45 @@ int ref_gp_convolve(const double* v, const int64_t* dims, int channels, const do
     });
 }
 
+// The warp update of the deformable loop over H ranks (registration.hpp:313-317):
+// gp_convolve(g_u, gaussian_taps(sigma_grad), renormalize) -> adam_step -> gp_convolve(u,
+// gaussian_taps(sigma_warp), renormalize); `step` = the Adam step counter after this call.
+int ref_warp_update(const double* g_u, double* u, double* m1, double* m2, const int64_t* dims, double sigma_grad,
+                    double sigma_warp, double lr, int64_t step, int world) {
+    return guarded([&] {
+        const Dims3 d = D(dims);
+        const auto gw = warp<double>(g_u, d);
+        const auto uw = warp<double>(u, d);
+        const auto w1 = warp<double>(m1, d);
+        const auto w2 = warp<double>(m2, d);
+        const auto taps_grad = gaussian_taps(sigma_grad);
+        const auto taps_warp = gaussian_taps(sigma_warp);
+        std::vector<WarpField<double>> ru(static_cast<std::size_t>(world)), r1(ru.size()), r2(ru.size());
+        WorkerGroup group(world);
+        group.run([&](WorkerContext& ctx) {
+            const auto spec = make_shard_spec(d, world, ctx.rank());
+            auto u_slab = extract_slab(uw, spec);
+            auto adam = AdamState<double>::zeros(u_slab.data.size());
+            const auto s1 = extract_slab(w1, spec), s2 = extract_slab(w2, spec);
+            std::copy(s1.data.begin(), s1.data.end(), adam.m1.begin());
+            std::copy(s2.data.begin(), s2.data.end(), adam.m2.begin());
+            adam.step = step - 1;
+            auto g = gp_convolve(ctx, extract_slab(gw, spec), taps_grad, spec, EdgeMode::renormalize, true);
+            adam_step<double>(u_slab.data, g.data, adam, lr);
+            u_slab = gp_convolve(ctx, u_slab, taps_warp, spec, EdgeMode::renormalize, true);
+            const auto k = static_cast<std::size_t>(ctx.rank());
+            ru[k] = std::move(u_slab);
+            r1[k] = WarpField<double>::zeros(s1.dims);
+            r2[k] = WarpField<double>::zeros(s2.dims);
+            std::copy(adam.m1.begin(), adam.m1.end(), r1[k].data.begin());
+            std::copy(adam.m2.begin(), adam.m2.end(), r2[k].data.begin());
+        });
+        put(gather_warp(ru, d).data, u);
+        put(gather_warp(r1, d).data, m1);
+        put(gather_warp(r2, d).data, m2);
+    });
+}
+
 // The deformable step over H ranks. loss_kind 0 = LNCC, 1 = MI. fp32 = 1 runs the
 // reference's T=float instantiation on the same inputs.
 int ref_step(int loss_kind, int fp32, const double* f, const double* m, const double* u, const int64_t* dims,

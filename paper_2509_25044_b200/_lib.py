@@ -103,6 +103,9 @@ _SIGS = {
     "ffdp_step_mi_grad_rec": (C.c_int, [_vp, Dims, Slab, C.POINTER(ParzenC), _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_grad": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
                                     _vp, _vp, _vp, _vp]),
+    "ffdp_gp_convolve": (C.c_int, [_vp, _vp, Dims, Slab, C.c_int, _vp, C.c_int, C.c_int, _vp]),
+    "ffdp_sobolev_adam": (C.c_int, [_vp, _vp, _vp, _vp, Dims, Slab, _vp, C.c_int, C.c_double, C.c_double,
+                                    C.c_double, C.c_double, C.c_int64, _vp]),
     "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_minmax": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_pad_window": (C.c_int, [_vp, Dims, C.c_int64, C.c_int64, _vp, _vp]),

@@ -372,3 +372,32 @@ class ShardedStep:
             lib.ffdp_step_mi_grad(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, self._window(), C.byref(args),
                                   C.byref(k.c), V._ptr(self.ws.table), V._ptr(g_u), V._ptr(self.ws.miss), V._stream())
         return -float(self.ws.table[2 * b * b + 2 * b + 1].item()), g_u
+
+
+# ------------------------------------------------------------------ warp update
+def sharded_warp_update(u_slab: torch.Tensor, g_u_slab: torch.Tensor, state, spec: ShardSpec, lr_norm: float,
+                        sigma_grad: float = 1.0, sigma_warp: float = 0.5) -> torch.Tensor:
+    """The warp update of one deformable iteration on a z-slab (registration.hpp:313-317):
+    halo_exchange of g_u (the gaussian radius, fabric.hpp:315-370), ffdp_sobolev_adam
+    (gp_convolve(g_u, renormalize) fused with adam_step, distops.hpp:54-101 /
+    adam.hpp:30-50) on the slab, halo_exchange of the updated u and ffdp_gp_convolve of
+    it. The taps depend only on global planes, so the result equals the unsharded update.
+    u_slab, state.m1 and state.m2 are updated in place; returns the smoothed u slab."""
+    from . import voxreg as V
+    from ._lib import lib
+    u_slab = V._warp(u_slab, "warp_update")
+    g_u_slab = V._warp(g_u_slab, "warp_update")
+    nz_g, ny, nx = spec.global_shape
+    tg, tw = V.gaussian_taps(sigma_grad), V.gaussian_taps(sigma_warp)
+    g_h, lo, hi = halo_exchange(g_u_slab, spec, len(tg) // 2)
+    slab = Slab(spec.lo - lo, spec.thickness + lo + hi, spec.lo, spec.hi, nz_g)
+    state.step += 1
+    lib.ffdp_sobolev_adam(V._ptr(g_h), V._ptr(u_slab), V._ptr(state.m1), V._ptr(state.m2),
+                          V._dims(g_h.shape), slab, V._taps_ptr(tg), len(tg), lr_norm, state.beta1, state.beta2,
+                          state.eps, state.step, V._stream())
+    u_h, lo, hi = halo_exchange(u_slab, spec, len(tw) // 2)
+    slab = Slab(spec.lo - lo, spec.thickness + lo + hi, spec.lo, spec.hi, nz_g)
+    out = torch.empty_like(u_slab)
+    lib.ffdp_gp_convolve(V._ptr(u_h), V._ptr(out), V._dims(u_h.shape), slab, 3, V._taps_ptr(tw), len(tw), 1,
+                         V._stream())
+    return out

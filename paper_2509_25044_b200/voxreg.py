@@ -28,6 +28,7 @@ __all__ = [
     "fused_sample_backward", "LnccState", "LnccResult", "lncc_forward_fused", "lncc_backward_fused",
     "ParzenKernel", "JointHistogram", "MiStats", "MiResult", "mi_forward_exact", "mi_forward_approx", "mi_backward",
     "LossParams", "StepResult", "warp_loss_step", "convolve_axis", "box_taps", "gaussian_taps",
+    "gp_convolve", "AdamState", "adam_step", "warp_update", "deformable_lr_norm",
 ]
 
 
@@ -255,6 +256,85 @@ def convolve_axis(x: torch.Tensor, axis: int, taps, renormalize: bool = False, l
     out = torch.empty_like(x)
     lib.ffdp_convolve_axis(_ptr(x), _ptr(out), _dims(x.shape), ch, axis, taps.ctypes.data_as(C.POINTER(C.c_double)),
                            len(taps), 1 if renormalize else 0, lo_global, n_global, _stream())
+    return out
+
+
+def _taps_ptr(taps: np.ndarray):
+    return taps.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def gp_convolve(x: torch.Tensor, taps, mode: str = "zero_pad", slab: Optional[Slab] = None) -> torch.Tensor:
+    """gp_convolve / separable_convolve (distops.hpp:84-101, smoothing.hpp:98-105): x, y, z
+    passes of `taps` over a volume (nz,ny,nx) or warp (nz,ny,nx,3), EdgeMode "zero_pad" or
+    "renormalize". One z-marching kernel (ffdp_gp_convolve). With a slab, x holds the
+    buffer planes (incl. the halo) and the result the slab's interior planes."""
+    if mode not in ("zero_pad", "renormalize"):
+        raise InvalidArgument(f"gp_convolve: unknown edge mode {mode!r}")
+    x = x.to(torch.float32).contiguous()
+    ch = 3 if x.dim() == 4 else 1
+    taps = np.ascontiguousarray(taps, dtype=np.float64)
+    if taps.size % 2 == 0:
+        raise InvalidArgument("gp_convolve: kernel must be odd")
+    slab = slab or _full_slab(x.shape[0])
+    out = torch.empty((slab.z_end - slab.z_begin,) + tuple(x.shape[1:]), dtype=torch.float32, device=x.device)
+    lib.ffdp_gp_convolve(_ptr(x), _ptr(out), _dims(x.shape), slab, ch, _taps_ptr(taps), len(taps),
+                         1 if mode == "renormalize" else 0, _stream())
+    return out
+
+
+@dataclass
+class AdamState:
+    """AdamState (adam.hpp:14-28) of a warp field: first / second moments in fp32 (the
+    reference's T storage), the step counter and the hyper-parameters."""
+    m1: torch.Tensor
+    m2: torch.Tensor
+    step: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    @staticmethod
+    def zeros(like: torch.Tensor) -> "AdamState":
+        return AdamState(torch.zeros_like(like, dtype=torch.float32), torch.zeros_like(like, dtype=torch.float32))
+
+
+def adam_step(param: torch.Tensor, grad: torch.Tensor, state: AdamState, lr: float) -> None:
+    """adam_step (adam.hpp:30-50) on a warp field, in place: the Adam epilogue of
+    ffdp_sobolev_adam with a single unit tap (no smoothing)."""
+    param, grad = _warp(param, "adam_step"), _warp(grad, "adam_step")
+    if param.shape != grad.shape or param.shape != state.m1.shape or param.shape != state.m2.shape:
+        raise InvalidArgument("adam_step: shape mismatch")
+    state.step += 1
+    one = np.ones(1)
+    lib.ffdp_sobolev_adam(_ptr(grad), _ptr(param), _ptr(state.m1), _ptr(state.m2), _dims(param.shape),
+                          _full_slab(param.shape[0]), _taps_ptr(one), 1, lr, state.beta1, state.beta2, state.eps,
+                          state.step, _stream())
+
+
+def deformable_lr_norm(shape, lr: float) -> float:
+    """registration.hpp:257-264: the learning rate in voxels of the level converted to
+    normalized units by the mean voxel pitch."""
+    nz, ny, nx = shape[:3]
+    return lr * (2.0 / (nx - 1) + 2.0 / (ny - 1) + 2.0 / (nz - 1)) / 3.0
+
+
+def warp_update(u: torch.Tensor, g_u: torch.Tensor, state: AdamState, lr_norm: float, sigma_grad: float = 1.0,
+                sigma_warp: float = 0.5, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The warp update of one deformable iteration (registration.hpp:313-317) at H = 1:
+    g_s = gp_convolve(g_u, gaussian_taps(sigma_grad), renormalize); adam_step(u, g_s,
+    state, lr_norm) -- fused in one kernel, u updated in place -- then the returned field
+    gp_convolve(u, gaussian_taps(sigma_warp), renormalize) (into `out` if given)."""
+    u, g_u = _warp(u, "warp_update"), _warp(g_u, "warp_update")
+    if u.shape != g_u.shape or u.shape != state.m1.shape or u.shape != state.m2.shape:
+        raise InvalidArgument("adam_step: shape mismatch")
+    slab = _full_slab(u.shape[0])
+    tg, tw = gaussian_taps(sigma_grad), gaussian_taps(sigma_warp)
+    state.step += 1
+    lib.ffdp_sobolev_adam(_ptr(g_u), _ptr(u), _ptr(state.m1), _ptr(state.m2), _dims(u.shape), slab, _taps_ptr(tg),
+                          len(tg), lr_norm, state.beta1, state.beta2, state.eps, state.step, _stream())
+    if out is None:
+        out = torch.empty_like(u)
+    lib.ffdp_gp_convolve(_ptr(u), _ptr(out), _dims(u.shape), slab, 3, _taps_ptr(tw), len(tw), 1, _stream())
     return out
 
 

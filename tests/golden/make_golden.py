@@ -137,6 +137,20 @@ def main():
     g["gp_w"] = wv
     g["gp_gauss_H3"] = ref.gp_convolve(wv, orc.gaussian_taps(1.0), 3, True, True)
 
+    # --- the warp update (registration.hpp:313-317): gp_convolve(g_u) -> adam_step ->
+    #     gp_convolve(u), two consecutive Adam steps, H = 1 and 3
+    r = orc.rng(701)
+    sh = (11, 9, 10)
+    wu_g = orc.random_volume(r, sh + (3,), -1e-3, 1e-3)
+    wu_u = orc.random_volume(r, sh + (3,), -0.02, 0.02)
+    z = np.zeros(sh + (3,))
+    g.update({"wu_g": wu_g, "wu_u": wu_u})
+    for world in (1, 3):
+        u1, a1, b1 = ref.warp_update(wu_g, wu_u, z, z, 0.01, 1, world=world)
+        u2, a2, b2 = ref.warp_update(0.5 * wu_g, u1, a1, b1, 0.01, 2, world=world)
+        g.update({f"wu_H{world}_u1": u1, f"wu_H{world}_m1": a1, f"wu_H{world}_v1": b1, f"wu_H{world}_u2": u2,
+                  f"wu_H{world}_m2": a2, f"wu_H{world}_v2": b2})
+
     path = os.path.join(OUT, "voxreg_golden.npz")
     np.savez_compressed(path, **g)
     print(f"wrote {path}: {len(g)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

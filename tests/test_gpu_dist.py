@@ -62,3 +62,47 @@ def test_sharded_step_matches_unsharded_oracle(orc, world, loss):
     assert losses[0] == pytest.approx(ref["loss"], rel=1e-5)
     g = np.concatenate([out[r][1] for r in range(world)], axis=0)
     assert maxrel(g, ref["g_u"]) <= 1e-4
+
+
+WU_SHAPE = (17, 20, 36)
+
+
+def w_warp_update(rank, world):
+    """dist.sharded_warp_update over real ranks (gloo halo exchange of g_u and of u)."""
+    import torch
+
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200 import voxreg as V
+    rng = np.random.default_rng(77)
+    g = rng.uniform(-1e-3, 1e-3, WU_SHAPE + (3,)).astype(np.float32)
+    u = rng.uniform(-0.02, 0.02, WU_SHAPE + (3,)).astype(np.float32)
+    spec = D.make_shard_spec(WU_SHAPE, world, rank)
+    dev = torch.device("cuda", 0)
+    us = torch.from_numpy(np.ascontiguousarray(u[spec.lo:spec.hi])).to(dev)
+    gs = torch.from_numpy(np.ascontiguousarray(g[spec.lo:spec.hi])).to(dev)
+    st = V.AdamState.zeros(us)
+    out = D.sharded_warp_update(us, gs, st, spec, 0.01)
+    out = D.sharded_warp_update(out, 0.5 * gs, st, spec, 0.01)
+    return out.cpu().numpy(), st.m1.cpu().numpy()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_warp_update_matches_single_gpu(world):
+    """registration.hpp:313-317 on `world` ranks equals the single-GPU warp update exactly."""
+    need_gpu()
+    import torch
+
+    from paper_2509_25044_b200 import voxreg as V
+    rng = np.random.default_rng(77)
+    g = rng.uniform(-1e-3, 1e-3, WU_SHAPE + (3,)).astype(np.float32)
+    u = rng.uniform(-0.02, 0.02, WU_SHAPE + (3,)).astype(np.float32)
+    ut = torch.from_numpy(u).cuda()
+    gt = torch.from_numpy(g).cuda()
+    st = V.AdamState.zeros(ut)
+    ref = V.warp_update(ut, gt, st, 0.01)
+    ref = V.warp_update(ref, 0.5 * gt, st, 0.01)
+    out = spawn(w_warp_update, world)
+    got = np.concatenate([out[r][0] for r in range(world)], axis=0)
+    m1 = np.concatenate([out[r][1] for r in range(world)], axis=0)
+    assert np.array_equal(got, ref.cpu().numpy())
+    assert np.array_equal(m1, st.m1.cpu().numpy())

@@ -125,3 +125,20 @@ def test_shard_ranges(orc):
     assert [orc.shard_range(10, 3, r) for r in range(3)] == [(0, 4), (4, 7), (7, 10)]
     with pytest.raises(ValueError):
         orc.shard_range(2, 3, 0)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_warp_update(orc, golden, world):
+    """registration.hpp:313-317: gp_convolve(g_u, gaussian 1.0, renormalize) -> adam_step
+    (adam.hpp:30-50) -> gp_convolve(u, gaussian 0.5, renormalize), two Adam steps; the
+    sharded reference (halo exchange) equals the single-rank restatement."""
+    g, u = golden["wu_g"], golden["wu_u"]
+    z = np.zeros_like(u)
+    u1, a1, b1 = orc.warp_update(g, u, z, z, 0.01, 1)
+    close(u1, golden[f"wu_H{world}_u1"], tol=1e-14)
+    close(a1, golden[f"wu_H{world}_m1"], tol=1e-14)
+    close(b1, golden[f"wu_H{world}_v1"], tol=1e-14)
+    u2, a2, b2 = orc.warp_update(0.5 * g, u1, a1, b1, 0.01, 2)
+    close(u2, golden[f"wu_H{world}_u2"], tol=1e-14)
+    close(a2, golden[f"wu_H{world}_m2"], tol=1e-14)
+    close(b2, golden[f"wu_H{world}_v2"], tol=1e-14)
