@@ -462,6 +462,59 @@ def run_ours(args, rank, world, local_rank):
     return out, st
 
 
+def run_warp_update(shape, steps, hbm, hbm_kind):
+    """The warp update after the step (registration.hpp:313-317):
+    ffdp_sobolev_adam (gp_convolve(g_u, gaussian 1.0) + adam_step, 84 B/voxel: reads g_u,
+    u, m1, m2, writes u, m1, m2) and ffdp_gp_convolve(u, gaussian 0.5) (24 B/voxel), each
+    timed with CUDA events on the launching stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2509_25044_b200 import voxreg as V
+    from paper_2509_25044_b200._lib import lib
+    nz, ny, nx = shape
+    g = torch.empty((nz, ny, nx, 3), device="cuda").uniform_(-1e-6, 1e-6)
+    u = torch.empty_like(g).uniform_(-0.01, 0.01)
+    m1, m2, out = torch.zeros_like(g), torch.zeros_like(g), torch.empty_like(g)
+    slab = V._full_slab(nz)
+    dims = V._dims(g.shape)
+    tg, tw = V.gaussian_taps(1.0), V.gaussian_taps(0.5)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    lr = V.deformable_lr_norm(shape, 0.5)
+
+    def once(k, ev=None):
+        if ev:
+            ev[0].record()
+        lib.ffdp_sobolev_adam(V._ptr(g), V._ptr(u), V._ptr(m1), V._ptr(m2), dims, slab, V._taps_ptr(tg), len(tg), lr,
+                              0.9, 0.999, 1e-8, k, s)
+        if ev:
+            ev[1].record()
+        lib.ffdp_gp_convolve(V._ptr(u), V._ptr(out), dims, slab, 3, V._taps_ptr(tw), len(tw), 1, s)
+        if ev:
+            ev[2].record()
+
+    for k in range(3):
+        once(k + 1)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for k, ev in enumerate(evs):
+        once(k + 4, ev)
+    torch.cuda.synchronize()
+    t_adam = sum(e[0].elapsed_time(e[1]) for e in evs) / steps
+    t_conv = sum(e[1].elapsed_time(e[2]) for e in evs) / steps
+    n = nz * ny * nx
+    gbs = lambda b, ms: b * n / (ms * 1e-3) / 1e9
+    return {"lattice": f"{nx}x{ny}x{nz}", "ms": round(t_adam + t_conv, 4),
+            "kernel_ms": {"k_smooth<3,3,adam> (sobolev_adam)": round(t_adam, 4),
+                          "k_smooth<2,3,store> (gp_convolve)": round(t_conv, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(gbs(108, t_adam + t_conv), 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(gbs(108, t_adam + t_conv) / hbm, 4), "peak_kind": hbm_kind,
+                         "algorithmic_bytes_per_voxel": 108,
+                         "per_kernel_frac": {"sobolev_adam": round(gbs(84, t_adam) / hbm, 4),
+                                             "gp_convolve": round(gbs(24, t_conv) / hbm, 4)}},
+            "gpu_launches": 2 * steps}
+
+
 def run_e2e(args, st, f, m, u, A, t, loss, world):
     import torch
     steps = max(3, min(args.steps, 20))
@@ -584,6 +637,9 @@ def main():
             sec, _ = run_ours(a2, rank, world, local_rank)
             out["secondary"] = {k: sec[k] for k in ("value", "unit", "ms_per_step", "config", "roofline",
                                                     "step_roofline", "kernel_ms", "clocks", "e2e", "loss")}
+            torch.cuda.empty_cache()
+            hbm, hbm_kind = peaks()
+            out["warp_update"] = run_warp_update(WORKLOADS["lncc720"][0], max(5, min(args.steps, 20)), hbm, hbm_kind)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -58,12 +58,23 @@ __device__ __forceinline__ float wsum(const Params& P, int64_t g, int64_t n) {
     return s;
 }
 
+constexpr int NSTAGE = 3;  // input planes in flight (cp.async ring)
+
 template <int R, int CH>
 struct Smem {
     static constexpr int HX = TX + 2 * R, HY = TY + 2 * R, ROW = CH * HX;
-    float raw[2][HY][ROW];  // haloed input plane (double-buffered: the next plane loads during this one)
-    float X[HY][TX * CH];   // x-convolved rows (the top barrier of the next plane protects it)
+    float raw[NSTAGE][HY][ROW];  // haloed input planes, filled by cp.async (zero-fill outside)
+    float X[HY][TX * CH];        // x-convolved rows (the top barrier of the next plane protects it)
 };
+
+// 4-byte asynchronous global -> shared copy; src_bytes = 0 writes a zero (no global read).
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int R, int CH, bool ADAM>
 __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
@@ -81,46 +92,94 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
     // renormalize (smoothing.hpp:75-90): divide by the in-lattice tap sum of each axis
     // (the full tap sum for full windows)
     const float wxy = P.renorm ? wsum<R>(P, gx, P.nx) * wsum<R>(P, gy, P.ny) : 1.0f;
+    float wfull = 0.0f;
+#pragma unroll
+    for (int k = 0; k <= 2 * R; ++k) wfull += P.w[k];
+    const float inv_xy_full = 1.0f / (wxy * wfull);
     float ring[2 * R + 1][CH];
 #pragma unroll
     for (int k = 0; k < 2 * R + 1; ++k)
 #pragma unroll
         for (int c = 0; c < CH; ++c) ring[k][c] = 0.0f;
 
-    // the haloed tile of plane p: rows of CH * HX consecutive floats (zero outside the
-    // lattice, and for planes outside the volume)
-    auto load = [&](int64_t p, int buf) {
+    // The haloed tile of plane p, as rows of CH * HX consecutive floats, copied
+    // asynchronously (zero outside the lattice and for planes outside the volume). A
+    // thread's tile elements are fixed for the whole z march: their in-plane source
+    // offsets (-1 outside the lattice) are computed once. Each thread always commits one
+    // group per plane (possibly empty) so the wait counts line up.
+    constexpr int NEL = S::HY * S::ROW, KL = (NEL + NT - 1) / NT;
+    int32_t src_off[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+        const int q = t + k * NT;
+        const int r = q / S::ROW, e = q - r * S::ROW;
+        const int yy = y0 - R + r;
+        const int xe = (x0 - R) * CH + e;
+        src_off[k] = (q < NEL && yy >= 0 && yy < P.ny && xe >= 0 && xe < P.nx * CH) ? yy * P.nx * CH + xe : -1;
+    }
+    auto issue = [&](int64_t p, int stage) {
         const bool pin = p >= 0 && p < P.nz_global;
         const float* src = P.in + (pin ? (p - P.buf_z0) * P.plane * CH : 0);
-        for (int q = t; q < S::HY * S::ROW; q += NT) {
-            const int r = q / S::ROW, e = q - r * S::ROW;
-            const int yy = y0 - R + r;
-            const int xe = (x0 - R) * CH + e;  // element index along the row
-            const bool ok = pin && yy >= 0 && yy < P.ny && xe >= 0 && xe < P.nx * CH;
-            sm.raw[buf][r][e] = ok ? __ldg(src + (int64_t)yy * P.nx * CH + xe) : 0.0f;
+        float* dst = &sm.raw[stage][0][0];
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const int q = t + k * NT;
+            if (q < NEL) {
+                const bool ok = pin && src_off[k] >= 0;
+                cp_async4(dst + q, ok ? src + src_off[k] : P.in, ok ? 4 : 0);
+            }
         }
+        cp_async_commit();
     };
 
     const int64_t pstart = zc0 - R, pend = zc1 + R;  // input planes of this chunk
-    load(pstart, 0);
-    int buf = 0;
-    for (int64_t p = pstart; p < pend; ++p, buf ^= 1) {
-        __syncthreads();  // raw[buf] complete; X free
-        if (p + 1 < pend) load(p + 1, buf ^ 1);
-        // x taps: rows of the haloed tile, TX outputs each
-        for (int q = t; q < S::HY * TX; q += NT) {
-            const int r = q / TX, x = q - r * TX;
-            float acc[CH];
 #pragma unroll
-            for (int c = 0; c < CH; ++c) acc[c] = 0.0f;
+    for (int k = 0; k < NSTAGE - 1; ++k) {
+        if (pstart + k < pend) issue(pstart + k, k);
+        else cp_async_commit();
+    }
+    // Adam operands of the next output voxel, loaded one plane ahead
+    float pu[CH], pm1[CH], pm2[CH];
+    auto fetch = [&](int64_t q) {
+        const int64_t o = ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx) * CH;
 #pragma unroll
-            for (int k = 0; k <= 2 * R; ++k)
+        for (int c = 0; c < CH; ++c) {
+            pu[c] = P.u[o + c];
+            pm1[c] = P.m1[o + c];
+            pm2[c] = P.m2[o + c];
+        }
+    };
+    if (ADAM && own) fetch(zc0);
+    int stage = 0;
+    for (int64_t p = pstart; p < pend; ++p) {
+        // plane p + NSTAGE - 1 goes into the stage read two planes ago (freed by the
+        // barrier after that plane's x taps)
+        const int st_next = stage == 0 ? NSTAGE - 1 : stage - 1;
+        if (p + NSTAGE - 1 < pend) issue(p + NSTAGE - 1, st_next);
+        else cp_async_commit();
+        cp_async_wait<NSTAGE - 1>();  // this thread's copies of plane p have landed
+        __syncthreads();             // everyone's have; X is free
+        // x taps: a job is a run of XR outputs of one channel of one row, sliding over the
+        // XR + 2R inputs in registers (runs of 8 measured no faster for R = 3); job order
+        // (run, channel) inside a row keeps a row's lanes on distinct banks
+        constexpr int XR = 4;
+        for (int j = t; j < S::HY * CH * (TX / XR); j += NT) {
+            const int r = j / (CH * (TX / XR)), rc = j - r * (CH * (TX / XR));
+            const int m = rc / CH, c = rc - m * CH;
+            const float* in = &sm.raw[stage][r][XR * m * CH + c];
+            float w_[XR + 2 * R];
 #pragma unroll
-                for (int c = 0; c < CH; ++c) acc[c] = fmaf(P.w[k], sm.raw[buf][r][(x + k) * CH + c], acc[c]);
+            for (int i = 0; i < XR + 2 * R; ++i) w_[i] = in[i * CH];
 #pragma unroll
-            for (int c = 0; c < CH; ++c) sm.X[r][x * CH + c] = acc[c];
+            for (int o = 0; o < XR; ++o) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int k = 0; k <= 2 * R; ++k) acc = fmaf(P.w[k], w_[o + k], acc);
+                sm.X[r][(XR * m + o) * CH + c] = acc;
+            }
         }
         __syncthreads();
+        stage = stage + 1 == NSTAGE ? 0 : stage + 1;
         // y taps into the z ring
 #pragma unroll
         for (int k = 0; k < 2 * R; ++k)
@@ -136,25 +195,38 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
         // z taps: output plane q = p - R
         const int64_t q = p - R;
         if (q < zc0 || !own) continue;
-        const float inv = P.renorm ? 1.0f / (wxy * wsum<R>(P, q, P.nz_global)) : 1.0f;
+        // the z divisor only differs from the full tap sum within R planes of a face
+        const float inv = !P.renorm ? 1.0f
+                          : (q >= R && q + R < P.nz_global) ? inv_xy_full
+                                                            : 1.0f / (wxy * wsum<R>(P, q, P.nz_global));
         const int64_t o = ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx) * CH;
+        float v[CH];
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-            float v = 0.0f;
+            float a = 0.0f;
 #pragma unroll
-            for (int k = 0; k <= 2 * R; ++k) v = fmaf(P.w[k], ring[k][c], v);
-            v *= inv;
-            if (ADAM) {
-                const float m = fmaf(P.b1, P.m1[o + c], P.omb1 * v);
-                const float s2 = fmaf(P.b2, P.m2[o + c], P.omb2 * v * v);
+            for (int k = 0; k <= 2 * R; ++k) a = fmaf(P.w[k], ring[k][c], a);
+            v[c] = a * inv;
+        }
+        if (ADAM) {
+            float cu[CH], c1[CH], c2[CH];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) cu[c] = pu[c], c1[c] = pm1[c], c2[c] = pm2[c];
+            if (q + 1 < zc1) fetch(q + 1);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const float m = fmaf(P.b1, c1[c], P.omb1 * v[c]);
+                const float s2 = fmaf(P.b2, c2[c], P.omb2 * v[c] * v[c]);
                 P.m1[o + c] = m;
                 P.m2[o + c] = s2;
-                P.u[o + c] -= P.lr_c1 * m / (sqrtf(s2 * P.inv_c2) + P.eps);
-            } else {
-                P.out[o + c] = v;
+                P.u[o + c] = cu[c] - P.lr_c1 * m / (sqrtf(s2 * P.inv_c2) + P.eps);
             }
+        } else {
+#pragma unroll
+            for (int c = 0; c < CH; ++c) P.out[o + c] = v[c];
         }
     }
+    cp_async_wait<0>();
 }
 
 // Planes per z chunk: the fewest (waves x planes-with-halo) over chunk counts.
