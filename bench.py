@@ -308,7 +308,7 @@ def run_sharded(args, rank, world, local_rank, dev):
         return float(t[0]), -float(t[1])
 
     f, m, u, A, t = synth_inputs(gshape, loss, 1234, dev, spec.lo, spec.hi, reduce_minmax)
-    params = voxreg.LossParams(kind=loss, bins=32)
+    params = voxreg.LossParams(kind=loss, bins=32, mi_bspline_kernel=True)
     st = D.ShardedStep(f, m, spec, A, t, params)
     for _ in range(args.warmup):
         st.step(u)

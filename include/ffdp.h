@@ -168,6 +168,27 @@ FFDP_API int ffdp_sobolev_adam(const float* g_u, float* u, float* m1, float* m2,
                                const double* taps, int ntaps, double lr, double beta1, double beta2, double eps,
                                int64_t step, void* stream);
 
+/* ------------------------------------------------------------------- multi-scale */
+
+/* The lattice resample_scale produces (resample.hpp:52-57): ceil(n * factor) per axis;
+ * FFDP_INVALID_ARGUMENT for a non-finite / non-positive factor or a dimension < 2. */
+FFDP_API int ffdp_resample_dims(ffdp_dims dims, double factor, ffdp_dims* out);
+
+/*
+ * resample_scale (resample.hpp:48-103): for factor < 1 gaussian_smooth(v, 0.5 / factor)
+ * (renormalized, factor >= 1/4) then trilinear resampling onto ffdp_resample_dims(dims,
+ * factor) keeping the first and last voxel centres. scratch: device float[voxels of
+ * dims] for the smoothed volume, or NULL (stream-ordered allocation).
+ */
+FFDP_API int ffdp_resample_scale(const float* in, ffdp_dims dims, double factor, float* out, float* scratch,
+                                 void* stream);
+
+/* resample_warp (resample.hpp:108-146): trilinear on each channel onto out_dims. */
+FFDP_API int ffdp_resample_warp(const float* in, ffdp_dims dims, float* out, ffdp_dims out_dims, void* stream);
+
+/* normalize_intensities (registration.hpp:100-115): min-max to [0, 1] (constant -> 0). */
+FFDP_API int ffdp_normalize(const float* in, int64_t n, float* out, void* stream);
+
 /* -------------------------------------------------------------------------- LNCC */
 
 /*

@@ -513,7 +513,7 @@ struct LossParams {
     double epsilon = 1e-5;
     bool ants_approx = true;
     int bins = 32;
-    bool mi_bspline_kernel = true;
+    bool mi_bspline_kernel = false;  // the reference default (registration.hpp:40)
     bool mi_approx_forward = false;
 };
 

@@ -119,6 +119,11 @@ class Oracle:
         L.or_rng_uniform_int.argtypes = [C.POINTER(Rng), C.c_int64, C.c_int64]
         L.or_rng_uniform_int.restype = C.c_int64
         L.or_random_volume.argtypes = [C.POINTER(Rng), _dp, C.c_int64, C.c_double, C.c_double]
+        L.or_resample_scale.argtypes = [_dp, Dims, C.c_double, _dp, C.POINTER(Dims)]
+        L.or_resample_warp.argtypes = [_dp, Dims, _dp, Dims]
+        L.or_deformable_stage.argtypes = [_dp, _dp, Dims, _dp, _dp, C.c_int, _dp, C.POINTER(C.c_int), C.c_double,
+                                          C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                          C.c_int, _dp, _dp]
         L.or_adam_step.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double,
                                    C.c_int64]
         L.or_warp_update.argtypes = [_dp, _dp, _dp, _dp, Dims, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -182,6 +187,41 @@ class Oracle:
         self.lib.or_separable_convolve(_p(d), _dims_of(d.shape), channels, _p(taps), len(taps),
                                        1 if mode == "renormalize" else 0)
         return d
+
+    # -- multi-scale (resample.hpp:48-146) ----------------------------------------------
+    def resample_scale(self, v, factor):
+        v = _f64(v)
+        nd = Dims()
+        if self.lib.or_resample_scale(_p(v), _dims_of(v.shape), factor, None, C.byref(nd)):
+            raise ValueError("resample_scale: bad factor")
+        out = np.zeros((nd.nz, nd.ny, nd.nx))
+        self.lib.or_resample_scale(_p(v), _dims_of(v.shape), factor, _p(out), C.byref(nd))
+        return out
+
+    def resample_warp(self, w, shape):
+        w = _f64(w)
+        out = np.zeros(tuple(shape) + (3,))
+        self.lib.or_resample_warp(_p(w), _dims_of(w.shape[:3]), _p(out), _dims_of(shape))
+        return out
+
+    def deformable_stage(self, fixed, moving, steps, A=None, t=None, lr=0.5, sigma_grad=1.0, sigma_warp=0.5,
+                         loss="lncc", window=7, eps=1e-5, ants=True, bins=32, mi_kind="gaussian"):
+        """deformable_stage (registration.hpp:230-331) at H = 1: (warp, trace).
+        steps = [(downsample, iterations), ...]."""
+        f, m = _f64(fixed), _f64(moving)
+        A, t, _, _ = _args(A, t, None, None)
+        ds = np.array([s[0] for s in steps], dtype=np.float64)
+        its = (C.c_int * len(steps))(*[int(s[1]) for s in steps])
+        warp = np.zeros(f.shape + (3,))
+        trace = np.zeros(max(1, sum(int(s[1]) for s in steps)))
+        rc = self.lib.or_deformable_stage(_p(f), _p(m), _dims_of(f.shape), _p(A), _p(t), len(steps), _p(ds), its, lr,
+                                          sigma_grad, sigma_warp, 0 if loss == "lncc" else 1, window, eps, int(ants),
+                                          bins, KERNEL_KINDS[mi_kind], _p(warp), _p(trace))
+        if rc == 1:
+            raise ValueError("deformable_stage: invalid schedule")
+        if rc == 2:
+            raise ArithmeticError("deformable stage diverged (non-finite loss)")
+        return warp, trace[:sum(int(s[1]) for s in steps)]
 
     # -- warp update (adam.hpp:30-50, registration.hpp:313-317) ------------------------
     def adam_step(self, param, grad, m1, m2, lr, step, beta1=0.9, beta2=0.999, eps=1e-8):
@@ -339,6 +379,12 @@ class Reference:
         L.ref_parzen_eval.argtypes = [C.c_int, C.c_int, C.c_double, _dp, C.c_int64, _dp, _dp]
         L.ref_synth_pair.argtypes = [C.c_uint64, _i64p, C.c_int, C.c_double, _dp, _dp, _dp]
         L.ref_gp_convolve.argtypes = [_dp, _i64p, C.c_int, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        L.ref_resample_scale.argtypes = [_dp, _i64p, C.c_double, _dp, _i64p]
+        L.ref_resample_warp.argtypes = [_dp, _i64p, _i64p, _dp]
+        L.ref_normalize.argtypes = [_dp, _i64p, _dp]
+        L.ref_deformable_stage.argtypes = [_dp, _dp, _i64p, _dp, _dp, C.c_int, _dp, C.POINTER(C.c_int), C.c_double,
+                                           C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                           C.c_int, C.c_int, _dp, _dp]
         L.ref_warp_update.argtypes = [_dp, _dp, _dp, _dp, _i64p, C.c_double, C.c_double, C.c_double, C.c_int64,
                                       C.c_int]
         L.ref_step.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _i64p, _dp, _dp, C.c_int, C.c_double, C.c_int,
@@ -416,6 +462,42 @@ class Reference:
         self._check(self.lib.ref_gp_convolve(_p(v), _arr_dims(v.shape), channels, _p(taps), len(taps),
                                              int(renormalize), int(sync), world, _p(out)))
         return out
+
+    def resample_scale(self, v, factor):
+        v = _f64(v)
+        nd = np.zeros(3, dtype=np.int64)
+        self._check(self.lib.ref_resample_scale(_p(v), _arr_dims(v.shape), factor, None,
+                                                nd.ctypes.data_as(_i64p)))
+        out = np.zeros((int(nd[2]), int(nd[1]), int(nd[0])))
+        self._check(self.lib.ref_resample_scale(_p(v), _arr_dims(v.shape), factor, _p(out),
+                                                nd.ctypes.data_as(_i64p)))
+        return out
+
+    def resample_warp(self, w, shape):
+        w = _f64(w)
+        out = np.zeros(tuple(shape) + (3,))
+        self._check(self.lib.ref_resample_warp(_p(w), _arr_dims(w.shape[:3]), _arr_dims(shape), _p(out)))
+        return out
+
+    def normalize(self, v):
+        v = _f64(v)
+        out = np.zeros_like(v)
+        self._check(self.lib.ref_normalize(_p(v), _arr_dims(v.shape), _p(out)))
+        return out
+
+    def deformable_stage(self, fixed, moving, steps, A=None, t=None, lr=0.5, sigma_grad=1.0, sigma_warp=0.5,
+                         loss="lncc", window=7, eps=1e-5, ants=True, bins=32, mi_kind="gaussian", world=1):
+        f, m = _f64(fixed), _f64(moving)
+        A, t, _, _ = _args(A, t, None, None)
+        ds = np.array([s[0] for s in steps], dtype=np.float64)
+        its = (C.c_int * len(steps))(*[int(s[1]) for s in steps])
+        warp = np.zeros(f.shape + (3,))
+        trace = np.zeros(max(1, sum(int(s[1]) for s in steps)))
+        self._check(self.lib.ref_deformable_stage(_p(f), _p(m), _arr_dims(f.shape), _p(A), _p(t), len(steps), _p(ds),
+                                                  its, lr, sigma_grad, sigma_warp, 0 if loss == "lncc" else 1, window,
+                                                  eps, int(ants), bins, KERNEL_KINDS[mi_kind], world, _p(warp),
+                                                  _p(trace)))
+        return warp, trace[:sum(int(s[1]) for s in steps)]
 
     def warp_update(self, g_u, u, m1, m2, lr, step, sigma_grad=1.0, sigma_warp=0.5, world=1):
         """registration.hpp:313-317 over `world` ranks (gp_convolve halos): (u, m1, m2)."""

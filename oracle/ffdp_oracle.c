@@ -349,6 +349,77 @@ OR_API int or_warp_update(const double* g_u, double* u, double* m1, double* m2, 
     return 0;
 }
 
+/* resample_scale / resample_warp (resample.hpp:48-146): per-axis fractional index
+ * i (n_src - 1) / (n_dst - 1), cell_assign (floor + 1e-9 face snap), upper corner clamped. */
+static void rs_axis(int64_t i, int64_t ns, int64_t nd, int64_t* i0, int64_t* i1, double* w1) {
+    const double f = nd > 1 ? (double)i * (double)(ns - 1) / (double)(nd - 1) : 0.0;
+    double fr;
+    int64_t lo;
+    cell_assign(f, &lo, &fr);
+    *i0 = lo < ns - 1 ? lo : ns - 1;
+    *i1 = lo + 1 < ns - 1 ? lo + 1 : ns - 1;
+    *w1 = fr;
+}
+
+static void rs_trilinear(const double* in, or_dims sd, int channels, double* out, or_dims dd) {
+    for (int64_t z = 0; z < dd.nz; ++z) {
+        int64_t z0, z1;
+        double wz;
+        rs_axis(z, sd.nz, dd.nz, &z0, &z1, &wz);
+        for (int64_t y = 0; y < dd.ny; ++y) {
+            int64_t y0, y1;
+            double wy;
+            rs_axis(y, sd.ny, dd.ny, &y0, &y1, &wy);
+            for (int64_t x = 0; x < dd.nx; ++x) {
+                int64_t x0, x1;
+                double wx;
+                rs_axis(x, sd.nx, dd.nx, &x0, &x1, &wx);
+                const int64_t xs[2] = {x0, x1}, ys[2] = {y0, y1}, zs[2] = {z0, z1};
+                for (int c = 0; c < channels; ++c) {
+                    double acc = 0;
+                    for (int bz = 0; bz < 2; ++bz)
+                        for (int by = 0; by < 2; ++by)
+                            for (int bx = 0; bx < 2; ++bx) {
+                                const double w = (bx ? wx : 1 - wx) * (by ? wy : 1 - wy) * (bz ? wz : 1 - wz);
+                                acc += w * in[((zs[bz] * sd.ny + ys[by]) * sd.nx + xs[bx]) * channels + c];
+                            }
+                    out[((z * dd.ny + y) * dd.nx + x) * channels + c] = acc;
+                }
+            }
+        }
+    }
+}
+
+/* Returns 1 on a bad factor / a resulting dim < 2 (std::invalid_argument). out_dims is
+ * written first so callers can size `out`; pass out = NULL to query. */
+OR_API int or_resample_scale(const double* in, or_dims d, double factor, double* out, or_dims* out_dims) {
+    if (!isfinite(factor) || factor <= 0) return 1;
+    or_dims nd = d;
+    if (factor != 1.0) {
+        nd.nx = (int64_t)ceil((double)d.nx * factor);
+        nd.ny = (int64_t)ceil((double)d.ny * factor);
+        nd.nz = (int64_t)ceil((double)d.nz * factor);
+        if (nd.nx < 2 || nd.ny < 2 || nd.nz < 2) return 1;
+    }
+    *out_dims = nd;
+    if (!out) return 0;
+    const int64_t n = dims_voxels(d);
+    if (factor == 1.0) {
+        memcpy(out, in, (size_t)n * sizeof(double));
+        return 0;
+    }
+    double* src = (double*)malloc((size_t)n * sizeof(double));
+    memcpy(src, in, (size_t)n * sizeof(double));
+    if (factor < 1.0) or_gaussian_smooth(src, d, 1, 0.5 / factor);
+    rs_trilinear(src, d, 1, out, nd);
+    free(src);
+    return 0;
+}
+
+OR_API void or_resample_warp(const double* in, or_dims d, double* out, or_dims nd) {
+    rs_trilinear(in, d, 3, out, nd);
+}
+
 /* ------------------------------------------------------------- lncc.hpp:63-90 */
 static inline double lncc_ncc(double muf, double mum, double muff, double mumm, double mufm, double eps) {
     const double a = mufm - muf * mum;
@@ -932,4 +1003,76 @@ OR_API double or_step_mi(const double* f, const double* m, or_dims d, const doub
     free(p_ij);
     free(gm);
     return -mi;
+}
+
+/*
+ * deformable_stage (registration.hpp:230-331) at H = 1: per scale, resample F and M
+ * (resample_scale with factor 1 / downsample), carry the warp over (resample_warp, zeros
+ * at the first scale), convert lr to normalized units (257-264), then `iterations` times:
+ * the step (LNCC ANTs / exact or MI) -> trace[k++] = loss -> the warp update
+ * (or_warp_update, 313-317). Finally the warp is resampled onto F's lattice. Returns 0,
+ * 1 (invalid argument) or 2 (non-finite loss: NumericalError, trace up to it kept).
+ * loss_kind 0 = LNCC, 1 = MI (mi_kind: 0 gaussian, 1 bspline3).
+ */
+OR_API int or_deformable_stage(const double* fixed, const double* moving, or_dims d, const double* A,
+                               const double* t, int nsteps, const double* downsample, const int* iterations,
+                               double lr, double sigma_grad, double sigma_warp, int loss_kind, int window,
+                               double eps, int ants, int bins, int mi_kind, double* warp_out, double* trace) {
+    if (nsteps < 1 || !(lr > 0) || !(sigma_grad >= 0) || !(sigma_warp >= 0)) return 1;
+    for (int s = 0; s < nsteps; ++s)
+        if (!(downsample[s] >= 1) || iterations[s] < 0 || (s > 0 && downsample[s] > downsample[s - 1])) return 1;
+    or_parzen k;
+    if (loss_kind == 1 && or_parzen_make(mi_kind, bins, 0.5, &k)) return 1;
+    double* warp = NULL;
+    or_dims wd = d;
+    int tk = 0;
+    for (int s = 0; s < nsteps; ++s) {
+        const double factor = 1.0 / downsample[s];
+        or_dims sd;
+        if (or_resample_scale(fixed, d, factor, NULL, &sd)) {
+            free(warp);
+            return 1;
+        }
+        const int64_t n = dims_voxels(sd);
+        double* fs = (double*)malloc(sizeof(double) * (size_t)n);
+        double* ms = (double*)malloc(sizeof(double) * (size_t)n);
+        or_resample_scale(fixed, d, factor, fs, &sd);
+        or_resample_scale(moving, d, factor, ms, &sd);
+        double* u = (double*)calloc(3 * (size_t)n, sizeof(double));
+        if (warp) or_resample_warp(warp, wd, u, sd);
+        free(warp);
+        warp = u;
+        wd = sd;
+        const double pitch = (2.0 / (double)(sd.nx - 1) + 2.0 / (double)(sd.ny - 1) + 2.0 / (double)(sd.nz - 1)) / 3.0;
+        const double lr_norm = lr * pitch;
+        double* m1 = (double*)calloc(3 * (size_t)n, sizeof(double));
+        double* m2 = (double*)calloc(3 * (size_t)n, sizeof(double));
+        double* g = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+        int bad = 0;
+        for (int it = 0; it < iterations[s]; ++it) {
+            const double loss = loss_kind == 0 ? or_step_lncc(fs, ms, sd, warp, A, t, window, eps, ants, g, NULL, NULL)
+                                               : or_step_mi(fs, ms, sd, warp, A, t, &k, 0, g, NULL, NULL, NULL);
+            trace[tk++] = loss;
+            if (!isfinite(loss)) {
+                bad = 1;
+                break;
+            }
+            or_warp_update(g, warp, m1, m2, sd, sigma_grad, sigma_warp, lr_norm, 0.9, 0.999, 1e-8, it + 1);
+        }
+        free(fs);
+        free(ms);
+        free(m1);
+        free(m2);
+        free(g);
+        if (bad) {
+            free(warp);
+            return 2;
+        }
+    }
+    if (wd.nx != d.nx || wd.ny != d.ny || wd.nz != d.nz)
+        or_resample_warp(warp, wd, warp_out, d);
+    else
+        memcpy(warp_out, warp, sizeof(double) * 3 * (size_t)dims_voxels(d));
+    free(warp);
+    return 0;
 }

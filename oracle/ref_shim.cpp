@@ -304,6 +304,57 @@ int ref_warp_update(const double* g_u, double* u, double* m1, double* m2, const 
     });
 }
 
+// resample_scale (resample.hpp:48-103) and resample_warp (108-146).
+int ref_resample_scale(const double* v, const int64_t* dims, double factor, double* out, int64_t* out_dims) {
+    return guarded([&] {
+        const auto r = resample_scale(vol<double>(v, D(dims)), factor);
+        out_dims[0] = r.dims.nx;
+        out_dims[1] = r.dims.ny;
+        out_dims[2] = r.dims.nz;
+        if (out) put(r.data, out);
+    });
+}
+
+int ref_resample_warp(const double* w, const int64_t* dims, const int64_t* out_dims, double* out) {
+    return guarded([&] { put(resample_warp(warp<double>(w, D(dims)), D(out_dims)).data, out); });
+}
+
+// normalize_intensities (registration.hpp:100-115).
+int ref_normalize(const double* v, const int64_t* dims, double* out) {
+    return guarded([&] { put(detail::normalize_intensities(vol<double>(v, D(dims))).data, out); });
+}
+
+// deformable_stage (registration.hpp:230-331) on `world` ranks; trace = one loss per
+// iteration. loss_kind 0 = LNCC, 1 = MI; mi_kind 0 gaussian, 1 bspline3.
+int ref_deformable_stage(const double* fixed, const double* moving, const int64_t* dims, const double* A,
+                         const double* t, int nsteps, const double* downsample, const int* iterations, double lr,
+                         double sigma_grad, double sigma_warp, int loss_kind, int window, double eps, int ants,
+                         int bins, int mi_kind, int world, double* warp_out, double* trace) {
+    return guarded([&] {
+        const Dims3 d = D(dims);
+        ScaleSchedule sch;
+        for (int s = 0; s < nsteps; ++s) sch.steps.push_back(ScaleStep{downsample[s], iterations[s]});
+        sch.lr = lr;
+        sch.sigma_grad = sigma_grad;
+        sch.sigma_warp = sigma_warp;
+        sch.loss.kind = loss_kind == 0 ? LossKind::lncc : LossKind::mi;
+        sch.loss.window = window;
+        sch.loss.epsilon = eps;
+        sch.loss.ants_approx = ants != 0;
+        sch.loss.bins = bins;
+        sch.loss.mi_bspline_kernel = mi_kind == 1;
+        AffineMap aff;
+        for (int i = 0; i < 9; ++i) aff.matrix.m[i] = A[i];
+        aff.translation = Vec3{t[0], t[1], t[2]};
+        DeformableOptions opts;
+        opts.shards = world;
+        std::vector<TraceEntry> tr;
+        const auto w = deformable_stage(vol<double>(fixed, d), vol<double>(moving, d), aff, sch, opts, &tr);
+        put(w.data, warp_out);
+        for (std::size_t i = 0; i < tr.size(); ++i) trace[i] = tr[i].loss;
+    });
+}
+
 // The deformable step over H ranks. loss_kind 0 = LNCC, 1 = MI. fp32 = 1 runs the
 // reference's T=float instantiation on the same inputs.
 int ref_step(int loss_kind, int fp32, const double* f, const double* m, const double* u, const int64_t* dims,

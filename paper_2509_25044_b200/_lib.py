@@ -106,6 +106,10 @@ _SIGS = {
     "ffdp_gp_convolve": (C.c_int, [_vp, _vp, Dims, Slab, C.c_int, _vp, C.c_int, C.c_int, _vp]),
     "ffdp_sobolev_adam": (C.c_int, [_vp, _vp, _vp, _vp, Dims, Slab, _vp, C.c_int, C.c_double, C.c_double,
                                     C.c_double, C.c_double, C.c_int64, _vp]),
+    "ffdp_resample_dims": (C.c_int, [Dims, C.c_double, C.POINTER(Dims)]),
+    "ffdp_resample_scale": (C.c_int, [_vp, Dims, C.c_double, _vp, _vp, _vp]),
+    "ffdp_resample_warp": (C.c_int, [_vp, Dims, _vp, Dims, _vp]),
+    "ffdp_normalize": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_minmax": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_pad_window": (C.c_int, [_vp, Dims, C.c_int64, C.c_int64, _vp, _vp]),

@@ -32,7 +32,7 @@ namespace ffdp {
 namespace sm {
 
 constexpr int TX = 32, TY = 16, NT = TX * TY;  // one output column per thread
-constexpr int kMaxR = 4;
+constexpr int kMaxR = 6;  // gaussian sigma <= 2 (resample_scale's anti-alias at factor 1/4)
 
 struct Params {
     const float* in;   // buffer planes [buf_z0, buf_z0 + buf_nz), CH per voxel
@@ -269,6 +269,8 @@ int dispatch(const Params& P, int R, int CH, cudaStream_t st) {
             case 2: return launch<2, 3, ADAM>(P, st);
             case 3: return launch<3, 3, ADAM>(P, st);
             case 4: return launch<4, 3, ADAM>(P, st);
+            case 5: return launch<5, 3, ADAM>(P, st);
+            case 6: return launch<6, 3, ADAM>(P, st);
         }
     } else if (!ADAM) {
         switch (R) {
@@ -277,6 +279,8 @@ int dispatch(const Params& P, int R, int CH, cudaStream_t st) {
             case 2: return launch<2, 1, false>(P, st);
             case 3: return launch<3, 1, false>(P, st);
             case 4: return launch<4, 1, false>(P, st);
+            case 5: return launch<5, 1, false>(P, st);
+            case 6: return launch<6, 1, false>(P, st);
         }
     }
     return set_error(FFDP_INVALID_ARGUMENT, "gp_convolve: radius %d / %d channels not supported (radius <= %d)", R,

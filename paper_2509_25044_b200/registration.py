@@ -1,0 +1,189 @@
+"""The deformable registration driver around the fused step (registration.hpp:33-331),
+re-exposed over libffdp: the reference's ScaleStep / ScaleSchedule / TraceEntry /
+NumericalError and deformable_stage, plus resample_scale / resample_warp /
+normalize_intensities (resample.hpp:48-146, registration.hpp:100-115).
+
+Per scale everything stays in HBM: F and M are resampled on the device, M is
+zero-bordered once (it is static within a scale, registration.hpp:249,270), and each
+iteration is three launches -- the fused warp + loss step (warp_loss_step), the fused
+Sobolev + Adam update of u (ffdp_sobolev_adam) and the warp smoothing (ffdp_gp_convolve)
+-- plus a device-side copy of the loss into the scale's trace. The host reads the trace
+once per scale; a non-finite loss raises NumericalError then (the reference raises in the
+same iteration; the returned trace is the same up to the failing entry).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import voxreg as V
+from ._lib import Dims, InvalidArgument, lib
+
+
+# ---------------------------------------------------------------- multi-scale plumbing
+def resample_dims(shape, factor: float):
+    """The (nz, ny, nx) lattice resample_scale produces (resample.hpp:52-57)."""
+    nz, ny, nx = shape[:3]
+    out = Dims()
+    lib.ffdp_resample_dims(Dims(nx, ny, nz), factor, C.byref(out))
+    return (out.nz, out.ny, out.nx)
+
+
+def resample_scale(v: torch.Tensor, factor: float, scratch: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """resample_scale (resample.hpp:48-103): Gaussian anti-alias (sigma 0.5 / factor) when
+    shrinking, then trilinear onto ceil(n * factor) keeping the end voxel centres."""
+    v = V._vol(v, "resample_scale")
+    shape = resample_dims(v.shape, factor)
+    out = torch.empty(shape, dtype=torch.float32, device=v.device)
+    lib.ffdp_resample_scale(V._ptr(v), V._dims(v.shape), factor, V._ptr(out), V._ptr(scratch), V._stream())
+    return out
+
+
+def resample_warp(w: torch.Tensor, shape) -> torch.Tensor:
+    """resample_warp (resample.hpp:108-146): trilinear per channel onto `shape`."""
+    w = V._warp(w, "resample_warp")
+    out = torch.empty(tuple(shape[:3]) + (3,), dtype=torch.float32, device=w.device)
+    lib.ffdp_resample_warp(V._ptr(w), V._dims(w.shape), V._ptr(out), V._dims(shape), V._stream())
+    return out
+
+
+def normalize_intensities(v: torch.Tensor) -> torch.Tensor:
+    """normalize_intensities (registration.hpp:100-115): min-max to [0, 1], constant -> 0."""
+    v = V._vol(v, "normalize_intensities")
+    out = torch.empty_like(v)
+    lib.ffdp_normalize(V._ptr(v), v.numel(), V._ptr(out), V._stream())
+    return out
+
+
+# ---------------------------------------------------------------- schedule
+@dataclass
+class ScaleStep:
+    """ScaleStep (registration.hpp:48-51): downsample 4 = quarter resolution."""
+    downsample: float = 1.0
+    iterations: int = 0
+
+
+@dataclass
+class ScaleSchedule:
+    """ScaleSchedule (registration.hpp:53-73)."""
+    steps: List[ScaleStep] = field(default_factory=list)
+    lr: float = 0.5
+    sigma_grad: float = 1.0
+    sigma_warp: float = 0.5
+    loss: V.LossParams = field(default_factory=V.LossParams)
+
+    def validate(self):
+        if not self.steps:
+            raise InvalidArgument("schedule: no scale steps")
+        for i, s in enumerate(self.steps):
+            if not s.downsample >= 1:
+                raise InvalidArgument("schedule: downsample factors must be >= 1")
+            if s.iterations < 0:
+                raise InvalidArgument("schedule: iterations must be >= 0")
+            if i > 0 and s.downsample > self.steps[i - 1].downsample:
+                raise InvalidArgument("schedule: factors must be non-increasing toward 1")
+        if not (self.lr > 0) or not (self.sigma_grad >= 0) or not (self.sigma_warp >= 0):
+            raise InvalidArgument("schedule: bad lr/sigma")
+
+
+@dataclass
+class TraceEntry:
+    """TraceEntry (registration.hpp:75-79)."""
+    scale_index: int = 0
+    iteration: int = 0
+    loss: float = 0.0
+
+
+class NumericalError(RuntimeError):
+    """NumericalError (registration.hpp:81-85), carrying the trace so far."""
+
+    def __init__(self, what: str, trace: Sequence[TraceEntry]):
+        super().__init__(what)
+        self.trace = list(trace)
+
+
+@dataclass
+class DeformableOptions:
+    """DeformableOptions (registration.hpp:221-224); shards > 1 runs through
+    dist.ShardedStep / dist.sharded_warp_update under torch.distributed."""
+    shards: int = 1
+    gp_sync: bool = True
+
+
+# ---------------------------------------------------------------- the driver
+class _Scale:
+    """One scale's device state: F_s, the zero-bordered M_s, the workspace, the trace."""
+
+    def __init__(self, f_s, m_s, params: V.LossParams, iterations: int):
+        self.f = f_s
+        self.m = V.MovingImage(m_s)
+        self.params = params
+        self.ws = V.StepWorkspace(f_s.device, params.bins)
+        self.shifts = (V.intensity_shift(f_s), V.intensity_shift(m_s)) if params.kind == "lncc" else None
+        self.g_u = torch.empty(tuple(f_s.shape) + (3,), dtype=torch.float32, device=f_s.device)
+        self.trace = torch.zeros(max(1, iterations), dtype=torch.float64, device=f_s.device)
+        self.n = f_s.numel()
+
+    def step(self, u, A, t, it):
+        V.warp_loss_step(self.f, self.m, u, A, t, self.params, g_u=self.g_u, ws=self.ws, shifts=self.shifts,
+                         sync=False)
+        if self.params.kind == "lncc":
+            # loss = 1 - sum_n / N (dist_lncc, distops.hpp:309-318)
+            self.trace[it:it + 1].copy_(1.0 - self.ws.sum_n / self.n)
+        else:
+            b = self.params.bins
+            self.trace[it:it + 1].copy_(-self.ws.table[2 * b * b + 2 * b + 1:2 * b * b + 2 * b + 2])
+        return self.g_u
+
+
+def deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine=None, schedule: Optional[ScaleSchedule] = None,
+                     opts: Optional[DeformableOptions] = None, trace: Optional[List[TraceEntry]] = None,
+                     scale_index_base: int = 0) -> torch.Tensor:
+    """deformable_stage (registration.hpp:230-331) on one GPU: greedy multi-scale
+    optimisation of the displacement field on top of the affine (A, t) (identity by
+    default). Returns the warp on F's lattice, (nz, ny, nx, 3) fp32; appends one
+    TraceEntry per iteration to `trace`."""
+    schedule = schedule or ScaleSchedule()
+    schedule.validate()
+    opts = opts or DeformableOptions()
+    if opts.shards < 1:
+        raise InvalidArgument("deformable_stage: shards must be >= 1")
+    if opts.shards > 1:
+        raise InvalidArgument("deformable_stage: shards > 1 runs one process per GPU (dist.sharded_deformable_stage)")
+    fixed, moving = V._vol(fixed, "deformable_stage"), V._vol(moving, "deformable_stage")
+    if tuple(fixed.shape) != tuple(moving.shape):
+        raise InvalidArgument("deformable_stage: F and M must share a lattice (registration.hpp:268-270)")
+    A, t = (np.eye(3), np.zeros(3)) if affine is None else (np.asarray(affine[0]), np.asarray(affine[1]))
+    warp = None
+    for s, step in enumerate(schedule.steps):
+        factor = 1.0 / step.downsample
+        f_s = fixed if factor == 1.0 else resample_scale(fixed, factor)
+        m_s = moving if factor == 1.0 else resample_scale(moving, factor)
+        shape = tuple(f_s.shape)
+        warp = resample_warp(warp, shape) if warp is not None else torch.zeros(shape + (3,), device=fixed.device)
+        # registration.hpp:257-264: lr in voxels of the level -> normalized units
+        lr_norm = V.deformable_lr_norm(shape, schedule.lr)
+        sc = _Scale(f_s, m_s, schedule.loss, step.iterations)
+        adam = V.AdamState.zeros(warp)
+        spare = torch.empty_like(warp)
+        for it in range(step.iterations):
+            g_u = sc.step(warp, A, t, it)
+            out = V.warp_update(warp, g_u, adam, lr_norm, schedule.sigma_grad, schedule.sigma_warp, out=spare)
+            warp, spare = out, warp
+        losses = sc.trace[:step.iterations].tolist()
+        entries = [TraceEntry(scale_index_base + s, i, v) for i, v in enumerate(losses)]
+        bad = next((i for i, v in enumerate(losses) if not np.isfinite(v)), None)
+        if bad is not None:
+            if trace is not None:
+                trace.extend(entries[:bad + 1])
+            raise NumericalError("deformable stage diverged (non-finite loss)",
+                                 (trace or []) if trace is not None else entries[:bad + 1])
+        if trace is not None:
+            trace.extend(entries)
+    if tuple(warp.shape[:3]) != tuple(fixed.shape):
+        warp = resample_warp(warp, fixed.shape)
+    return warp

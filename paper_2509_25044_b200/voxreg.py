@@ -554,7 +554,7 @@ class LossParams:
     epsilon: float = 1e-5
     ants_approx: bool = True
     bins: int = 32
-    mi_bspline_kernel: bool = True
+    mi_bspline_kernel: bool = False  # the reference default (registration.hpp:40): Gaussian Parzen
     mi_approx_forward: bool = False
 
     def make_kernel(self) -> ParzenKernel:

@@ -330,6 +330,7 @@ static void step_tests() {
         auto g = V::WarpField::uninitialized(dims(p.d));
         V::LossParams lp;
         lp.kind = V::LossKind::mi;
+        lp.mi_bspline_kernel = true;
         V::DeformableStep step(f, m, lp);
         auto r = step.step(u, args_of(p), g);
         or_parzen ok;

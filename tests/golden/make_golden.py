@@ -151,6 +151,17 @@ def main():
         g.update({f"wu_H{world}_u1": u1, f"wu_H{world}_m1": a1, f"wu_H{world}_v1": b1, f"wu_H{world}_u2": u2,
                   f"wu_H{world}_m2": a2, f"wu_H{world}_v2": b2})
 
+    # --- multi-scale plumbing (resample.hpp:48-146, registration.hpp:100-115)
+    rv = orc.random_volume(orc.rng(801), (13, 17, 19), 0.0, 2.0)
+    g["rs_v"] = rv
+    for f in (0.5, 0.25, 0.37, 2.0):
+        g[f"rs_scale_{f}"] = ref.resample_scale(rv, f)
+    rw = orc.random_volume(orc.rng(802), (7, 9, 11, 3), -0.1, 0.1)
+    g["rs_w"] = rw
+    for sh in ((13, 17, 19), (4, 5, 6), (1, 9, 11)):
+        g["rs_warp_" + "x".join(map(str, sh))] = ref.resample_warp(rw, sh)
+    g["rs_norm"] = ref.normalize(rv)
+
     path = os.path.join(OUT, "voxreg_golden.npz")
     np.savez_compressed(path, **g)
     print(f"wrote {path}: {len(g)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

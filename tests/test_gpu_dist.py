@@ -32,7 +32,7 @@ def w_sharded(rank, world, loss):
     f = torch.from_numpy(np.ascontiguousarray(si.f[sl])).to(dev)
     m = torch.from_numpy(np.ascontiguousarray(si.m[sl])).to(dev)
     u = torch.from_numpy(np.ascontiguousarray(si.u[sl])).to(dev)
-    st = D.ShardedStep(f, m, spec, si.A, si.t, V.LossParams(kind=loss, bins=32), margin_planes=2)
+    st = D.ShardedStep(f, m, spec, si.A, si.t, V.LossParams(kind=loss, bins=32, mi_bspline_kernel=True), margin_planes=2)
     loss_v, g_u = st.step(u)
     loss_2, g_2 = st.step(u)  # a second step reuses the window: identical
     assert loss_2 == loss_v and torch.equal(g_2, g_u)

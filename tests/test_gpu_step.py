@@ -74,7 +74,7 @@ def test_step_mi_records_equal_recompute(V, mi_case):
 
 def test_step_mi_parity(V, mi_case):
     si, ref = mi_case
-    res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="mi", bins=32))
+    res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="mi", bins=32, mi_bspline_kernel=True))
     assert res.window_misses == 0
     assert res.loss == pytest.approx(ref["loss"], rel=LOSS_RTOL)
     gu = host(res.g_u)
@@ -100,7 +100,7 @@ def test_step_lncc_matches_operator_chain(V, lncc_case):
 def test_step_deterministic_mi(V, mi_case):
     si, _ = mi_case
     f, m, u = dev(si.f), dev(si.m), dev(si.u)
-    p = V.LossParams(kind="mi")
+    p = V.LossParams(kind="mi", mi_bspline_kernel=True)
     a = V.warp_loss_step(f, m, u, si.A, si.t, p)
     b = V.warp_loss_step(f, m, u, si.A, si.t, p)
     assert a.loss == b.loss  # integer fixed-point histogram: order independent
@@ -114,6 +114,6 @@ def test_step_mi_sparse_histogram(V, orc, shape, seed):
     from oracle import step_inputs
     si = step_inputs(orc, shape, seed=seed, loss="mi")
     ref = orc.step_mi(si.f, si.m, si.u, orc.parzen("bspline3", 32), si.A, si.t)
-    res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="mi", bins=32))
+    res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="mi", bins=32, mi_bspline_kernel=True))
     assert res.loss == pytest.approx(ref["loss"], rel=LOSS_RTOL)
     assert maxrel(host(res.g_u), ref["g_u"]) <= GRAD_MAXREL

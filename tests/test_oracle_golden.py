@@ -142,3 +142,14 @@ def test_warp_update(orc, golden, world):
     close(u2, golden[f"wu_H{world}_u2"], tol=1e-14)
     close(a2, golden[f"wu_H{world}_m2"], tol=1e-14)
     close(b2, golden[f"wu_H{world}_v2"], tol=1e-14)
+
+
+def test_resample_and_normalize(orc, golden):
+    """resample_scale (anti-alias + trilinear, resample.hpp:48-103), resample_warp
+    (108-146) and normalize_intensities (registration.hpp:100-115), bit for bit."""
+    v = golden["rs_v"]
+    for f in (0.5, 0.25, 0.37, 2.0):
+        close(orc.resample_scale(v, f), golden[f"rs_scale_{f}"], tol=0.0)
+    for sh in ((13, 17, 19), (4, 5, 6), (1, 9, 11)):
+        close(orc.resample_warp(golden["rs_w"], sh), golden["rs_warp_" + "x".join(map(str, sh))], tol=0.0)
+    close(orc.normalize(v), golden["rs_norm"], tol=0.0)
