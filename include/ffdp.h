@@ -189,6 +189,15 @@ FFDP_API int ffdp_resample_warp(const float* in, ffdp_dims dims, float* out, ffd
 /* normalize_intensities (registration.hpp:100-115): min-max to [0, 1] (constant -> 0). */
 FFDP_API int ffdp_normalize(const float* in, int64_t n, float* out, void* stream);
 
+/* jacobian_positive_fraction (metrics.hpp:145-176) of a warp (lattice >= 3 per axis):
+ * the fraction of interior voxels with det(I + du/dx) > 0; synchronises the stream. */
+FFDP_API int ffdp_jacobian_positive(const float* u, ffdp_dims dims, double* fraction, void* stream);
+
+/* dist_mse on one slab (distops.hpp:260-282): *sum += sum (moved - fixed)^2 (fp64);
+ * grad (may be NULL) = 2 (moved - fixed) / n_total. loss = allreduce(sum) / n_total. */
+FFDP_API int ffdp_mse(const float* fixed, const float* moved, int64_t n, int64_t n_total, float* grad, double* sum,
+                      void* stream);
+
 /* -------------------------------------------------------------------------- LNCC */
 
 /*

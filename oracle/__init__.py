@@ -124,6 +124,10 @@ class Oracle:
         L.or_deformable_stage.argtypes = [_dp, _dp, Dims, _dp, _dp, C.c_int, _dp, C.POINTER(C.c_int), C.c_double,
                                           C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
                                           C.c_int, _dp, _dp]
+        L.or_affine_stage.argtypes = [_dp, _dp, Dims, C.c_int, _dp, C.POINTER(C.c_int), C.c_double, C.c_int, C.c_int,
+                                      C.c_double, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.or_jacobian_positive.argtypes = [_dp, Dims]
+        L.or_jacobian_positive.restype = C.c_double
         L.or_adam_step.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double,
                                    C.c_int64]
         L.or_warp_update.argtypes = [_dp, _dp, _dp, _dp, Dims, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -222,6 +226,27 @@ class Oracle:
         if rc == 2:
             raise ArithmeticError("deformable stage diverged (non-finite loss)")
         return warp, trace[:sum(int(s[1]) for s in steps)]
+
+    def affine_stage(self, fixed, moving, steps, lr=0.5, loss="mi", window=7, eps=1e-5, ants=True, bins=32,
+                     mi_kind="gaussian"):
+        """affine_stage (registration.hpp:176-219): (A, t, trace)."""
+        f, m = _f64(fixed), _f64(moving)
+        ds = np.array([s[0] for s in steps], dtype=np.float64)
+        its = (C.c_int * len(steps))(*[int(s[1]) for s in steps])
+        A, t = np.zeros(9), np.zeros(3)
+        trace = np.zeros(max(1, sum(int(s[1]) for s in steps)))
+        rc = self.lib.or_affine_stage(_p(f), _p(m), _dims_of(f.shape), len(steps), _p(ds), its, lr,
+                                      {"mse": 0, "lncc": 1, "mi": 2}[loss], window, eps, int(ants), bins,
+                                      KERNEL_KINDS[mi_kind], _p(A), _p(t), _p(trace))
+        if rc == 1:
+            raise ValueError("affine_stage: invalid schedule")
+        if rc == 2:
+            raise ArithmeticError("affine stage diverged (non-finite loss)")
+        return A.reshape(3, 3), t, trace[:sum(int(s[1]) for s in steps)]
+
+    def jacobian_positive(self, u):
+        u = _f64(u)
+        return self.lib.or_jacobian_positive(_p(u), _dims_of(u.shape[:3]))
 
     # -- warp update (adam.hpp:30-50, registration.hpp:313-317) ------------------------
     def adam_step(self, param, grad, m1, m2, lr, step, beta1=0.9, beta2=0.999, eps=1e-8):
@@ -385,6 +410,9 @@ class Reference:
         L.ref_deformable_stage.argtypes = [_dp, _dp, _i64p, _dp, _dp, C.c_int, _dp, C.POINTER(C.c_int), C.c_double,
                                            C.c_double, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
                                            C.c_int, C.c_int, _dp, _dp]
+        L.ref_affine_stage.argtypes = [_dp, _dp, _i64p, C.c_int, _dp, C.POINTER(C.c_int), C.c_double, C.c_int,
+                                       C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ref_jacobian_positive.argtypes = [_dp, _i64p, _dp]
         L.ref_warp_update.argtypes = [_dp, _dp, _dp, _dp, _i64p, C.c_double, C.c_double, C.c_double, C.c_int64,
                                       C.c_int]
         L.ref_step.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _i64p, _dp, _dp, C.c_int, C.c_double, C.c_int,
@@ -498,6 +526,24 @@ class Reference:
                                                   eps, int(ants), bins, KERNEL_KINDS[mi_kind], world, _p(warp),
                                                   _p(trace)))
         return warp, trace[:sum(int(s[1]) for s in steps)]
+
+    def affine_stage(self, fixed, moving, steps, lr=0.5, loss="mi", window=7, eps=1e-5, ants=True, bins=32,
+                     mi_kind="gaussian"):
+        f, m = _f64(fixed), _f64(moving)
+        ds = np.array([s[0] for s in steps], dtype=np.float64)
+        its = (C.c_int * len(steps))(*[int(s[1]) for s in steps])
+        A, t = np.zeros(9), np.zeros(3)
+        trace = np.zeros(max(1, sum(int(s[1]) for s in steps)))
+        self._check(self.lib.ref_affine_stage(_p(f), _p(m), _arr_dims(f.shape), len(steps), _p(ds), its, lr,
+                                              {"mse": 0, "lncc": 1, "mi": 2}[loss], window, eps, int(ants), bins,
+                                              KERNEL_KINDS[mi_kind], _p(A), _p(t), _p(trace)))
+        return A.reshape(3, 3), t, trace[:sum(int(s[1]) for s in steps)]
+
+    def jacobian_positive(self, u):
+        u = _f64(u)
+        out = C.c_double()
+        self._check(self.lib.ref_jacobian_positive(_p(u), _arr_dims(u.shape[:3]), C.byref(out)))
+        return out.value
 
     def warp_update(self, g_u, u, m1, m2, lr, step, sigma_grad=1.0, sigma_warp=0.5, world=1):
         """registration.hpp:313-317 over `world` ranks (gp_convolve halos): (u, m1, m2)."""

@@ -1076,3 +1076,125 @@ OR_API int or_deformable_stage(const double* fixed, const double* moving, or_dim
     free(warp);
     return 0;
 }
+
+/* loss_and_grad (registration.hpp:123-173) on one host: 0 = MSE, 1 = LNCC (fused forward,
+ * backward with upstream 1), 2 = MI (exact forward, mi_backward_impl with upstream -1,
+ * loss = -MI). Returns the loss (NaN when the MI inputs leave [0, 1]). */
+static double loss_and_grad(int kind, const double* f, const double* moved, or_dims d, int window, double eps,
+                            int ants, const or_parzen* k, double* gm) {
+    const int64_t n = dims_voxels(d);
+    if (kind == 0) {
+        double sum = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const double dd = moved[i] - f[i];
+            sum += dd * dd;
+            gm[i] = 2.0 * dd / (double)n;
+        }
+        return sum / (double)n;
+    }
+    if (kind == 1) {
+        double* state = (double*)malloc(sizeof(double) * 5 * (size_t)n);
+        const double loss = or_lncc_forward(f, moved, d, window, eps, state, NULL);
+        or_lncc_backward(1.0, state, f, moved, d, window, eps, ants, NULL, gm);
+        free(state);
+        return loss;
+    }
+    const int b = k->bins;
+    double* raw = (double*)malloc(sizeof(double) * ((size_t)b * b + 2 * (size_t)b));
+    if (or_mi_forward_exact(f, moved, n, k, raw, NULL)) {
+        free(raw);
+        return NAN;
+    }
+    double* p_ij = (double*)malloc(sizeof(double) * ((size_t)b * b * 2 + 2 * (size_t)b));
+    double* p_i = p_ij + (size_t)b * b;
+    double* p_j = p_i + b;
+    double* ghat = p_j + b;
+    double z;
+    const double mi = or_mi_finalize(raw, b, p_ij, p_i, p_j, &z);
+    or_mi_ghat(-1.0, p_ij, p_i, p_j, z, b, ghat);
+    or_mi_backward(f, moved, n, k, ghat, NULL, gm);
+    free(raw);
+    free(p_ij);
+    return -mi;
+}
+
+/*
+ * affine_stage (registration.hpp:176-219): Adam (adam.hpp, state over all scales) on the
+ * 12 affine parameters (A row-major, then t) from the identity; per iteration
+ * moved = fused_sample(M_s, zero warp, A, t), loss_and_grad, fused_sample_backward
+ * (want affine + translation). loss_kind 0 MSE, 1 LNCC, 2 MI. Returns 0, 1 (invalid
+ * schedule) or 2 (non-finite loss).
+ */
+OR_API int or_affine_stage(const double* fixed, const double* moving, or_dims d, int nsteps, const double* downsample,
+                           const int* iterations, double lr, int loss_kind, int window, double eps, int ants,
+                           int bins, int mi_kind, double* A_out, double* t_out, double* trace) {
+    if (nsteps < 1 || !(lr > 0)) return 1;
+    for (int s = 0; s < nsteps; ++s)
+        if (!(downsample[s] >= 1) || iterations[s] < 0 || (s > 0 && downsample[s] > downsample[s - 1])) return 1;
+    or_parzen k;
+    if (loss_kind == 2 && or_parzen_make(mi_kind, bins, 0.5, &k)) return 1;
+    double params[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0}, m1[12] = {0}, m2[12] = {0};
+    int64_t step = 0;
+    int tk = 0;
+    const double S[3] = {1, 1, 1}, bounds[6] = {-1, -1, -1, 1, 1, 1};
+    for (int s = 0; s < nsteps; ++s) {
+        const double factor = 1.0 / downsample[s];
+        or_dims sd;
+        if (or_resample_scale(fixed, d, factor, NULL, &sd)) return 1;
+        const int64_t n = dims_voxels(sd);
+        double* fs = (double*)malloc(sizeof(double) * (size_t)n);
+        double* ms = (double*)malloc(sizeof(double) * (size_t)n);
+        or_resample_scale(fixed, d, factor, fs, &sd);
+        or_resample_scale(moving, d, factor, ms, &sd);
+        double* zw = (double*)calloc(3 * (size_t)n, sizeof(double));
+        double* moved = (double*)malloc(sizeof(double) * (size_t)n);
+        double* gm = (double*)malloc(sizeof(double) * (size_t)n);
+        int bad = 0;
+        for (int it = 0; it < iterations[s] && !bad; ++it) {
+            memset(moved, 0, sizeof(double) * (size_t)n);
+            or_sample_core(ms, sd, zw, sd, params, params + 9, S, bounds, moved, NULL, NULL, NULL, NULL, NULL, NULL);
+            const double loss = loss_and_grad(loss_kind, fs, moved, sd, window, eps, ants, &k, gm);
+            trace[tk++] = loss;
+            if (!isfinite(loss)) {
+                bad = 1;
+                break;
+            }
+            double grad[12] = {0};
+            or_sample_core(ms, sd, zw, sd, params, params + 9, S, bounds, NULL, gm, NULL, NULL, grad, grad + 9, NULL);
+            or_adam_step(params, grad, m1, m2, 12, lr, 0.9, 0.999, 1e-8, ++step);
+        }
+        free(fs);
+        free(ms);
+        free(zw);
+        free(moved);
+        free(gm);
+        if (bad) return 2;
+    }
+    memcpy(A_out, params, 9 * sizeof(double));
+    memcpy(t_out, params + 9, 3 * sizeof(double));
+    return 0;
+}
+
+/* jacobian_positive_fraction (metrics.hpp:145-176). Returns -1 for a lattice < 3. */
+OR_API double or_jacobian_positive(const double* u, or_dims d) {
+    if (d.nx < 3 || d.ny < 3 || d.nz < 3) return -1.0;
+    const double step[3] = {2.0 / (double)(d.nx - 1), 2.0 / (double)(d.ny - 1), 2.0 / (double)(d.nz - 1)};
+    int64_t pos = 0, tot = 0;
+    for (int64_t z = 1; z + 1 < d.nz; ++z)
+        for (int64_t y = 1; y + 1 < d.ny; ++y)
+            for (int64_t x = 1; x + 1 < d.nx; ++x) {
+                double j[3][3];
+                for (int c = 0; c < 3; ++c) {
+                    j[c][0] = (u[3 * vidx(d, x + 1, y, z) + c] - u[3 * vidx(d, x - 1, y, z) + c]) / (2 * step[0]);
+                    j[c][1] = (u[3 * vidx(d, x, y + 1, z) + c] - u[3 * vidx(d, x, y - 1, z) + c]) / (2 * step[1]);
+                    j[c][2] = (u[3 * vidx(d, x, y, z + 1) + c] - u[3 * vidx(d, x, y, z - 1) + c]) / (2 * step[2]);
+                    j[c][c] += 1.0;
+                }
+                const double det = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
+                                   j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
+                                   j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
+                pos += det > 0;
+                ++tot;
+            }
+    return (double)pos / (double)tot;
+}

@@ -18,6 +18,7 @@
 #include "voxreg/distops.hpp"
 #include "voxreg/fabric.hpp"
 #include "voxreg/lncc.hpp"
+#include "voxreg/metrics.hpp"
 #include "voxreg/mi.hpp"
 #include "voxreg/registration.hpp"
 #include "voxreg/sampler.hpp"
@@ -353,6 +354,34 @@ int ref_deformable_stage(const double* fixed, const double* moving, const int64_
         put(w.data, warp_out);
         for (std::size_t i = 0; i < tr.size(); ++i) trace[i] = tr[i].loss;
     });
+}
+
+// affine_stage (registration.hpp:176-219); loss_kind 0 MSE, 1 LNCC, 2 MI.
+int ref_affine_stage(const double* fixed, const double* moving, const int64_t* dims, int nsteps,
+                     const double* downsample, const int* iterations, double lr, int loss_kind, int window, double eps,
+                     int ants, int bins, int mi_kind, double* A_out, double* t_out, double* trace) {
+    return guarded([&] {
+        const Dims3 d = D(dims);
+        ScaleSchedule sch;
+        for (int s = 0; s < nsteps; ++s) sch.steps.push_back(ScaleStep{downsample[s], iterations[s]});
+        sch.lr = lr;
+        sch.loss.kind = loss_kind == 0 ? LossKind::mse : loss_kind == 1 ? LossKind::lncc : LossKind::mi;
+        sch.loss.window = window;
+        sch.loss.epsilon = eps;
+        sch.loss.ants_approx = ants != 0;
+        sch.loss.bins = bins;
+        sch.loss.mi_bspline_kernel = mi_kind == 1;
+        std::vector<TraceEntry> tr;
+        const AffineMap a = affine_stage(vol<double>(fixed, d), vol<double>(moving, d), sch, &tr);
+        for (int i = 0; i < 9; ++i) A_out[i] = a.matrix.m[static_cast<std::size_t>(i)];
+        for (int i = 0; i < 3; ++i) t_out[i] = a.translation[i];
+        for (std::size_t i = 0; i < tr.size(); ++i) trace[i] = tr[i].loss;
+    });
+}
+
+// jacobian_positive_fraction (metrics.hpp:145-176).
+int ref_jacobian_positive(const double* u, const int64_t* dims, double* out) {
+    return guarded([&] { *out = jacobian_positive_fraction(warp<double>(u, D(dims))); });
 }
 
 // The deformable step over H ranks. loss_kind 0 = LNCC, 1 = MI. fp32 = 1 runs the

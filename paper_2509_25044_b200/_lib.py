@@ -110,6 +110,8 @@ _SIGS = {
     "ffdp_resample_scale": (C.c_int, [_vp, Dims, C.c_double, _vp, _vp, _vp]),
     "ffdp_resample_warp": (C.c_int, [_vp, Dims, _vp, Dims, _vp]),
     "ffdp_normalize": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
+    "ffdp_jacobian_positive": (C.c_int, [_vp, Dims, C.POINTER(C.c_double), _vp]),
+    "ffdp_mse": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp, _vp, _vp]),
     "ffdp_reduce_sum_f64": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_minmax": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_pad_window": (C.c_int, [_vp, Dims, C.c_int64, C.c_int64, _vp, _vp]),

@@ -69,6 +69,57 @@ __global__ void __launch_bounds__(256) k_normalize(const float* __restrict__ in,
         out[i] = range > 0 ? (float)(((double)in[i] - lo) / range) : 0.0f;
 }
 
+// jacobian_positive_fraction (metrics.hpp:145-176): central differences over interior
+// voxels (normalized steps 2 / (n - 1)), det(I + du/dx) > 0, counted per CTA and added.
+__global__ void __launch_bounds__(256) k_jacobian_positive(const float* __restrict__ u, ffdp_dims d,
+                                                           unsigned long long* count) {
+    const int64_t ix = d.nx - 2, iy = d.ny - 2, iz = d.nz - 2, n = ix * iy * iz;
+    const double h0 = 1.0 / (2.0 * (2.0 / (double)(d.nx - 1))), h1 = 1.0 / (2.0 * (2.0 / (double)(d.ny - 1))),
+                 h2 = 1.0 / (2.0 * (2.0 / (double)(d.nz - 1)));
+    unsigned long long pos = 0;
+    for (int64_t v = blockIdx.x * 256LL + threadIdx.x; v < n; v += (int64_t)gridDim.x * 256) {
+        const int64_t x = v % ix + 1, yz = v / ix, y = yz % iy + 1, z = yz / iy + 1;
+        const int64_t c0 = ((z * d.ny + y) * d.nx + x) * 3, sx = 3, sy = 3 * d.nx, sz = 3 * d.nx * d.ny;
+        double j[3][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            j[c][0] = ((double)u[c0 + sx + c] - (double)u[c0 - sx + c]) * h0;
+            j[c][1] = ((double)u[c0 + sy + c] - (double)u[c0 - sy + c]) * h1;
+            j[c][2] = ((double)u[c0 + sz + c] - (double)u[c0 - sz + c]) * h2;
+            j[c][c] += 1.0;
+        }
+        const double det = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
+                           j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
+                           j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
+        pos += det > 0 ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, o);
+    if ((threadIdx.x & 31) == 0 && pos) atomicAdd(count, pos);
+}
+
+// dist_mse at one rank (distops.hpp:260-282, loss_and_grad mse registration.hpp:126-137):
+// sum of (moved - fixed)^2 into *sum (fp64, fixed-order per CTA then atomics of partial
+// sums -- reproducible to rounding), grad = 2 (moved - fixed) / n_total.
+__global__ void __launch_bounds__(256) k_mse(const float* __restrict__ f, const float* __restrict__ m, int64_t n,
+                                             double inv_n2, float* __restrict__ grad, double* partial) {
+    double acc = 0;
+    for (int64_t i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+        const double dd = (double)m[i] - (double)f[i];
+        acc += dd * dd;
+        if (grad) grad[i] = (float)(dd * inv_n2);
+    }
+    __shared__ double red[8];
+    acc = block_sum<256>(acc, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+__global__ void k_sum_partials(const double* partial, int nb, double* out) {
+    double s = 0;
+    for (int i = 0; i < nb; ++i) s += partial[i];
+    *out += s;
+}
+
 inline int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 16LL * num_sms())); }
 
 }  // namespace rs
@@ -154,6 +205,36 @@ int ffdp_normalize(const float* in, int64_t n, float* out, void* stream) {
     rs::k_normalize<<<rs::grid_for(n), 256, 0, st>>>(in, n, mm, out);
     scratch_free(mm, st);
     return check_launch("normalize_intensities");
+}
+
+int ffdp_jacobian_positive(const float* u, ffdp_dims d, double* fraction, void* stream) {
+    if (!u || !fraction) return set_error(FFDP_INVALID_ARGUMENT, "jacobian_positive_fraction: null pointer");
+    if (d.nx < 3 || d.ny < 3 || d.nz < 3)
+        return set_error(FFDP_INVALID_ARGUMENT, "jacobian_positive_fraction: lattice too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* cnt = (unsigned long long*)scratch_alloc(sizeof(unsigned long long), st);
+    if (!cnt) return set_error(FFDP_CUDA, "jacobian_positive_fraction: scratch allocation failed");
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st);
+    const int64_t n = (d.nx - 2) * (d.ny - 2) * (d.nz - 2);
+    rs::k_jacobian_positive<<<rs::grid_for(n), 256, 0, st>>>(u, d, cnt);
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st);
+    scratch_free(cnt, st);
+    FFDP_CHECK_CUDA(cudaStreamSynchronize(st));
+    *fraction = (double)h / (double)n;
+    return check_launch("jacobian_positive_fraction");
+}
+
+int ffdp_mse(const float* f, const float* m, int64_t n, int64_t n_total, float* grad, double* sum, void* stream) {
+    if (!f || !m || !sum || n < 1 || n_total < 1) return set_error(FFDP_INVALID_ARGUMENT, "dist_mse: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nb = rs::grid_for(n);
+    double* part = (double*)scratch_alloc(sizeof(double) * nb, st);
+    if (!part) return set_error(FFDP_CUDA, "dist_mse: scratch allocation failed");
+    rs::k_mse<<<nb, 256, 0, st>>>(f, m, n, 2.0 / (double)n_total, grad, part);
+    rs::k_sum_partials<<<1, 1, 0, st>>>(part, nb, sum);
+    scratch_free(part, st);
+    return check_launch("dist_mse");
 }
 
 }  // extern "C"

@@ -401,3 +401,62 @@ def sharded_warp_update(u_slab: torch.Tensor, g_u_slab: torch.Tensor, state, spe
     lib.ffdp_gp_convolve(V._ptr(u_h), V._ptr(out), V._dims(u_h.shape), slab, 3, V._taps_ptr(tw), len(tw), 1,
                          V._stream())
     return out
+
+
+def _gather_slabs(slab: torch.Tensor, spec: ShardSpec) -> torch.Tensor:
+    """gather_warp / gather_volume (fabric.hpp:108-132): the full field on every rank
+    (slabs padded to the thickest one for the equal-size all_gather, then trimmed)."""
+    if spec.world == 1:
+        return slab
+    ranges = shard_ranges(spec.global_shape[0], spec.world)
+    tmax = max(hi - lo for lo, hi in ranges)
+    src = torch.zeros((tmax,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=slab.device)
+    src[:slab.shape[0]].copy_(slab)
+    if _staged():
+        parts = [torch.empty_like(src, device="cpu") for _ in ranges]
+        dist.all_gather(parts, src.cpu())
+        parts = [p.to(slab.device) for p in parts]
+    else:
+        parts = [torch.empty_like(src) for _ in ranges]
+        dist.all_gather(parts, src)
+    return torch.cat([p[:hi - lo] for p, (lo, hi) in zip(parts, ranges)], 0)
+
+
+def sharded_deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine, schedule, trace=None,
+                             scale_index_base: int = 0, margin_planes: int = 8) -> torch.Tensor:
+    """deformable_stage (registration.hpp:230-331) with shards = world size, one rank per
+    GPU: every rank resamples the scale's F and M (the reference's workers do the same
+    from the shared volumes, 247-249) and keeps its z slab (make_shard_spec, 266-270);
+    per iteration ShardedStep (ring window, halo, allreduced loss / histogram) and
+    sharded_warp_update (halo-exchanged Sobolev + Adam + smoothing); the slabs are
+    gathered at the end of each scale (gather_warp, 323). Returns the full warp on every
+    rank; `trace` (rank-identical losses) gets one TraceEntry per iteration."""
+    from . import registration as R
+    from . import voxreg as V
+    schedule.validate()
+    rank, world = _world()
+    A, t = (np.eye(3), np.zeros(3)) if affine is None else (np.asarray(affine[0]), np.asarray(affine[1]))
+    warp = None
+    for s, step in enumerate(schedule.steps):
+        factor = 1.0 / step.downsample
+        f_s = fixed if factor == 1.0 else R.resample_scale(fixed, factor)
+        m_s = moving if factor == 1.0 else R.resample_scale(moving, factor)
+        shape = tuple(f_s.shape)
+        warp = R.resample_warp(warp, shape) if warp is not None else torch.zeros(shape + (3,), device=fixed.device)
+        spec = make_shard_spec(shape, world, rank)
+        sl = slice(spec.lo, spec.hi)
+        st = ShardedStep(f_s[sl], m_s[sl], spec, A, t, schedule.loss, margin_planes=margin_planes)
+        u = warp[sl].contiguous()
+        adam = V.AdamState.zeros(u)
+        lr_norm = V.deformable_lr_norm(shape, schedule.lr)
+        for it in range(step.iterations):
+            loss, g_u = st.step(u)
+            if not np.isfinite(loss):
+                raise R.NumericalError("deformable stage diverged (non-finite loss)", trace or [])
+            if trace is not None:
+                trace.append(R.TraceEntry(scale_index_base + s, it, loss))
+            u = sharded_warp_update(u, g_u, adam, spec, lr_norm, schedule.sigma_grad, schedule.sigma_warp)
+        warp = _gather_slabs(u, spec)
+    if tuple(warp.shape[:3]) != tuple(fixed.shape):
+        warp = R.resample_warp(warp, fixed.shape)
+    return warp

@@ -187,3 +187,115 @@ def deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine=None, sch
     if tuple(warp.shape[:3]) != tuple(fixed.shape):
         warp = resample_warp(warp, fixed.shape)
     return warp
+
+
+# ---------------------------------------------------------------- affine stage
+def _loss_and_grad(f_s: torch.Tensor, moved: torch.Tensor, p: V.LossParams):
+    """loss_and_grad (registration.hpp:123-173) through the operator kernels: MSE
+    (ffdp_mse), LNCC (lncc_forward_fused + lncc_backward_fused, upstream 1) or MI (exact or
+    approximate forward, mi_backward_impl with upstream -1, loss = -MI)."""
+    if p.kind == "mse":
+        grad = torch.empty_like(moved)
+        s = torch.zeros(1, dtype=torch.float64, device=moved.device)
+        lib.ffdp_mse(V._ptr(f_s), V._ptr(moved), moved.numel(), moved.numel(), V._ptr(grad), V._ptr(s), V._stream())
+        return float(s.item()) / moved.numel(), grad
+    if p.kind == "lncc":
+        res, state = V.lncc_forward_fused(f_s, moved, p.window, p.epsilon)
+        _, gm = V.lncc_backward_fused(1.0, state, f_s, moved, p.ants_approx)
+        return res.loss, gm
+    if p.kind == "mi":
+        k = p.make_kernel()
+        res = (V.mi_forward_approx if p.mi_approx_forward else V.mi_forward_exact)(f_s, moved, p.bins, k)
+        _, gm = V.mi_backward(-1.0, f_s, moved, res.hist, k, check_samples=False)
+        return -res.mi, gm
+    raise InvalidArgument(f"loss_and_grad: unknown loss kind {p.kind!r}")
+
+
+def _adam_host(params: np.ndarray, grad: np.ndarray, state: dict, lr: float):
+    """adam_step (adam.hpp:30-50) on the 12 affine parameters, fp64 (host control of a
+    12-number state; the volumes never leave the device)."""
+    state["step"] += 1
+    b1, b2, eps = 0.9, 0.999, 1e-8
+    c1 = 1.0 - b1 ** state["step"]
+    c2 = 1.0 - b2 ** state["step"]
+    state["m1"] = b1 * state["m1"] + (1.0 - b1) * grad
+    state["m2"] = b2 * state["m2"] + (1.0 - b2) * grad * grad
+    return params - lr * (state["m1"] / c1) / (np.sqrt(state["m2"] / c2) + eps)
+
+
+def affine_stage(fixed: torch.Tensor, moving: torch.Tensor, schedule: ScaleSchedule,
+                 trace: Optional[List[TraceEntry]] = None, scale_index_base: int = 0):
+    """affine_stage (registration.hpp:176-219): Adam on (A, t) from the identity; per
+    iteration moved = fused_sample(M_s, zero warp, A, t) on F_s's lattice, loss_and_grad,
+    fused_sample_backward(want affine + translation) -- the fp64 gA / gt reductions of
+    the sampler kernel. Returns (A 3x3, t 3)."""
+    schedule.validate()
+    fixed, moving = V._vol(fixed, "affine_stage"), V._vol(moving, "affine_stage")
+    params = np.concatenate([np.eye(3).ravel(), np.zeros(3)])
+    state = {"m1": np.zeros(12), "m2": np.zeros(12), "step": 0}
+    want = V.SamplerGradWant(image=False, warp=False, affine=True, translation=True)
+    for s, step in enumerate(schedule.steps):
+        factor = 1.0 / step.downsample
+        f_s = fixed if factor == 1.0 else resample_scale(fixed, factor)
+        m_s = moving if factor == 1.0 else resample_scale(moving, factor)
+        zero = torch.zeros(tuple(f_s.shape) + (3,), dtype=torch.float32, device=f_s.device)
+        for it in range(step.iterations):
+            args = V.SamplerArgs(A=params[:9].reshape(3, 3), t=params[9:])
+            moved = V.fused_sample(m_s, zero, args)
+            loss, gm = _loss_and_grad(f_s, moved, schedule.loss)
+            if not np.isfinite(loss):
+                raise NumericalError("affine stage diverged (non-finite loss)", trace or [])
+            if trace is not None:
+                trace.append(TraceEntry(scale_index_base + s, it, loss))
+            g = V.fused_sample_backward(gm, m_s, zero, args, want)
+            params = _adam_host(params, np.concatenate([g.affine.ravel(), g.translation]), state, schedule.lr)
+    return params[:9].reshape(3, 3).copy(), params[9:].copy()
+
+
+# ---------------------------------------------------------------- the pipeline
+def jacobian_positive_fraction(u: torch.Tensor) -> float:
+    """jacobian_positive_fraction (metrics.hpp:145-176): interior voxels with
+    det(I + du/dx) > 0 (central differences in normalized units)."""
+    u = V._warp(u, "jacobian_positive_fraction")
+    out = C.c_double()
+    lib.ffdp_jacobian_positive(V._ptr(u), V._dims(u.shape), C.byref(out), V._stream())
+    return out.value
+
+
+@dataclass
+class RegistrationConfig:
+    """RegistrationConfig (registration.hpp:333-338)."""
+    affine: ScaleSchedule = field(default_factory=lambda: ScaleSchedule(loss=V.LossParams(kind="mi")))
+    deformable: ScaleSchedule = field(default_factory=ScaleSchedule)
+    deformable_opts: DeformableOptions = field(default_factory=DeformableOptions)
+    skip_affine: bool = False
+
+
+@dataclass
+class RegistrationResult:
+    """RegistrationResult (registration.hpp:87-94); warp in fp32 on the device."""
+    affine: tuple
+    warp: torch.Tensor
+    trace: List[TraceEntry]
+    seconds: float
+    jacobian_positive_fraction: float
+
+
+def register_volumes(fixed: torch.Tensor, moving: torch.Tensor, config: RegistrationConfig) -> RegistrationResult:
+    """register_volumes (registration.hpp:340-368): intensity-normalised copies, the
+    affine stage (unless skipped), the deformable stage on top of it, the Jacobian
+    sign fraction of the warp (reported, not enforced)."""
+    import time
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f_n, m_n = normalize_intensities(fixed), normalize_intensities(moving)
+    trace: List[TraceEntry] = []
+    affine = (np.eye(3), np.zeros(3))
+    base = 0
+    if not config.skip_affine:
+        affine = affine_stage(f_n, m_n, config.affine, trace, 0)
+        base = len(config.affine.steps)
+    warp = deformable_stage(f_n, m_n, affine, config.deformable, config.deformable_opts, trace, base)
+    jac = jacobian_positive_fraction(warp) if min(warp.shape[:3]) >= 3 else 1.0
+    torch.cuda.synchronize()
+    return RegistrationResult(affine, warp, trace, time.perf_counter() - t0, jac)

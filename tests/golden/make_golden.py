@@ -162,6 +162,21 @@ def main():
         g["rs_warp_" + "x".join(map(str, sh))] = ref.resample_warp(rw, sh)
     g["rs_norm"] = ref.normalize(rv)
 
+    # --- affine stage (registration.hpp:176-219) and the deformable stage (230-331), H = 1
+    #     and H = 3, on the MI fixture; the Jacobian sign fraction (metrics.hpp:145-176)
+    si = step_inputs(orc, (18, 20, 22), seed=4242, loss="mi")
+    for loss in ("mse", "lncc", "mi"):
+        A, t, tr = ref.affine_stage(si.f, si.m, [(2, 3), (1, 3)], lr=0.01, loss=loss)
+        g.update({f"aff_{loss}_A": A, f"aff_{loss}_t": t, f"aff_{loss}_trace": tr})
+    for loss, kind in (("lncc", "gaussian"), ("mi", "bspline3"), ("mi", "gaussian")):
+        sl = step_inputs(orc, (18, 20, 22), seed=4242, loss=loss)
+        for world in (1, 3):
+            w, tr = ref.deformable_stage(sl.f, sl.m, [(2, 3), (1, 3)], sl.A, sl.t, loss=loss, mi_kind=kind,
+                                         world=world)
+            g.update({f"def_{loss}_{kind}_H{world}_warp": w, f"def_{loss}_{kind}_H{world}_trace": tr})
+    jw = orc.random_volume(orc.rng(901), (8, 9, 10, 3), -0.4, 0.4)
+    g.update({"jac_w": jw, "jac_frac": np.array(ref.jacobian_positive(jw))})
+
     path = os.path.join(OUT, "voxreg_golden.npz")
     np.savez_compressed(path, **g)
     print(f"wrote {path}: {len(g)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

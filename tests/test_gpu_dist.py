@@ -106,3 +106,49 @@ def test_sharded_warp_update_matches_single_gpu(world):
     m1 = np.concatenate([out[r][1] for r in range(world)], axis=0)
     assert np.array_equal(got, ref.cpu().numpy())
     assert np.array_equal(m1, st.m1.cpu().numpy())
+
+
+def w_stage(rank, world, loss):
+    """dist.sharded_deformable_stage over real ranks (every rank gets the full volumes)."""
+    import torch
+
+    from oracle import Oracle, step_inputs
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200 import registration as R
+    from paper_2509_25044_b200 import voxreg as V
+    si = step_inputs(Oracle(), (18, 20, 22), seed=4242, loss=loss)
+    dev = torch.device("cuda", 0)
+    f = torch.from_numpy(si.f.astype(np.float32)).to(dev)
+    m = torch.from_numpy(si.m.astype(np.float32)).to(dev)
+    sch = R.ScaleSchedule([R.ScaleStep(2, 3), R.ScaleStep(1, 3)],
+                          loss=V.LossParams(kind=loss, bins=32, mi_bspline_kernel=True))
+    trace = []
+    w = D.sharded_deformable_stage(f, m, (si.A, si.t), sch, trace, margin_planes=2)
+    return w.cpu().numpy(), [e.loss for e in trace]
+
+
+def w_stage_lncc(rank, world):
+    return w_stage(rank, world, "lncc")
+
+
+def w_stage_mi(rank, world):
+    return w_stage(rank, world, "mi")
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_sharded_deformable_stage_matches_oracle(orc, loss):
+    """deformable_stage with shards = 2 (registration.hpp:230-331) against the oracle's
+    single-rank stage (pinned to the reference at H = 1 and 3): same tolerances as the
+    single-GPU stage (trace 1e-5; warp l2 2e-4 and a tenth of one Adam step)."""
+    need_gpu()
+    from gpu_util import l2rel
+    from oracle import step_inputs
+    from paper_2509_25044_b200 import voxreg as V
+    si = step_inputs(orc, (18, 20, 22), seed=4242, loss=loss)
+    w_ref, tr_ref = orc.deformable_stage(si.f, si.m, [(2, 3), (1, 3)], si.A, si.t, loss=loss, mi_kind="bspline3")
+    out = spawn(w_stage_lncc if loss == "lncc" else w_stage_mi, 2)
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+    w, tr = out[0][0], np.array(out[0][1])
+    assert np.max(np.abs(tr - tr_ref) / np.abs(tr_ref)) <= 1e-5
+    assert l2rel(w, w_ref) <= 2e-4
+    assert np.max(np.abs(w - w_ref)) <= 0.1 * V.deformable_lr_norm(si.f.shape, 0.5)

@@ -110,3 +110,33 @@ def test_deformable_stage_gaussian_mi_first_iteration(R, orc):
     R.deformable_stage(dev(si.f), dev(si.m), (si.A, si.t), sch, trace=trace)
     assert trace[0].loss == pytest.approx(tr_ref[0], rel=1e-5)
     assert all(np.isfinite(e.loss) for e in trace) and trace[-1].loss < trace[0].loss
+
+
+@pytest.mark.parametrize("loss", ["mse", "lncc", "mi"])
+def test_affine_stage_matches_oracle(R, orc, loss):
+    """affine_stage (registration.hpp:176-219), two scales x 3 iterations: A, t to 1e-5
+    (the fp64 gA / gt reductions of the sampler over fp32 moved images), trace to 1e-5."""
+    from oracle import step_inputs
+    from paper_2509_25044_b200 import voxreg as V
+    si = step_inputs(orc, (18, 20, 22), seed=4242, loss="mi")
+    A_ref, t_ref, tr_ref = orc.affine_stage(si.f, si.m, [(2, 3), (1, 3)], lr=0.01, loss=loss)
+    sch = R.ScaleSchedule([R.ScaleStep(2, 3), R.ScaleStep(1, 3)], lr=0.01, loss=V.LossParams(kind=loss, bins=32))
+    trace = []
+    A, t = R.affine_stage(dev(si.f), dev(si.m), sch, trace)
+    tr = np.array([e.loss for e in trace])
+    assert np.max(np.abs(tr - tr_ref) / np.abs(tr_ref)) <= 1e-5
+    assert np.max(np.abs(A - A_ref)) <= 1e-5 and np.max(np.abs(t - t_ref)) <= 1e-5
+
+
+def test_jacobian_and_register_volumes(R, orc, golden):
+    assert R.jacobian_positive_fraction(dev(golden["jac_w"])) == pytest.approx(float(golden["jac_frac"]), abs=1e-12)
+    from oracle import step_inputs
+    from paper_2509_25044_b200 import voxreg as V
+    si = step_inputs(orc, (18, 20, 22), seed=4242, loss="mi")
+    cfg = R.RegistrationConfig(
+        affine=R.ScaleSchedule([R.ScaleStep(2, 2)], lr=0.01, loss=V.LossParams(kind="mi", bins=32)),
+        deformable=R.ScaleSchedule([R.ScaleStep(2, 2), R.ScaleStep(1, 2)], loss=V.LossParams(kind="lncc")))
+    res = R.register_volumes(dev(si.f * 3 + 1), dev(si.m * 2), cfg)
+    assert [(e.scale_index, e.iteration) for e in res.trace] == [(0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1)]
+    assert res.warp.shape == si.f.shape + (3,) and 0.0 <= res.jacobian_positive_fraction <= 1.0
+    assert all(np.isfinite(e.loss) for e in res.trace)

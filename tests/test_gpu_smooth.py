@@ -73,7 +73,7 @@ def test_gp_convolve_rejects(V):
     with pytest.raises(InvalidArgument):
         V.gp_convolve(x, np.ones(4) / 4)  # even kernel (distops.hpp:87,97)
     with pytest.raises(InvalidArgument):
-        V.gp_convolve(x, np.ones(11) / 11)  # radius above the kernel's limit
+        V.gp_convolve(x, np.ones(15) / 15)  # radius above the kernel's limit (6)
     with pytest.raises(InvalidArgument):
         # planes [2, 6) of a 12-plane lattice with only 1 halo plane for a radius-3 window
         V.gp_convolve(x[:6].contiguous(), np.full(7, 1 / 7), slab=Slab(1, 6, 2, 6, 12))

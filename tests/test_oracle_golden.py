@@ -153,3 +153,29 @@ def test_resample_and_normalize(orc, golden):
     for sh in ((13, 17, 19), (4, 5, 6), (1, 9, 11)):
         close(orc.resample_warp(golden["rs_w"], sh), golden["rs_warp_" + "x".join(map(str, sh))], tol=0.0)
     close(orc.normalize(v), golden["rs_norm"], tol=0.0)
+
+
+@pytest.mark.parametrize("loss", ["mse", "lncc", "mi"])
+def test_affine_stage(orc, golden, loss):
+    """affine_stage (registration.hpp:176-219): 12-parameter Adam over two scales."""
+    si = step_inputs(orc, (18, 20, 22), seed=4242, loss="mi")
+    A, t, tr = orc.affine_stage(si.f, si.m, [(2, 3), (1, 3)], lr=0.01, loss=loss)
+    close(A, golden[f"aff_{loss}_A"], tol=1e-12)
+    close(t, golden[f"aff_{loss}_t"], tol=1e-12)
+    close(tr, golden[f"aff_{loss}_trace"], tol=1e-12)
+
+
+@pytest.mark.parametrize("loss,kind", [("lncc", "gaussian"), ("mi", "bspline3"), ("mi", "gaussian")])
+def test_deformable_stage(orc, golden, loss, kind):
+    """deformable_stage (registration.hpp:230-331): the single-rank restatement equals the
+    reference at H = 1 and H = 3 (ring sampler + halos + allreduces)."""
+    si = step_inputs(orc, (18, 20, 22), seed=4242, loss=loss)
+    w, tr = orc.deformable_stage(si.f, si.m, [(2, 3), (1, 3)], si.A, si.t, loss=loss, mi_kind=kind)
+    for world in (1, 3):
+        close(tr, golden[f"def_{loss}_{kind}_H{world}_trace"], tol=1e-9)
+        close(w, golden[f"def_{loss}_{kind}_H{world}_warp"], tol=1e-8)
+
+
+def test_jacobian_positive(orc, golden):
+    assert orc.jacobian_positive(golden["jac_w"]) == float(golden["jac_frac"])
+    assert 0.0 < float(golden["jac_frac"]) < 1.0
