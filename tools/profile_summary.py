@@ -24,8 +24,9 @@ from collections import OrderedDict
 sys.path.insert(0, os.path.dirname(__file__))
 from ncu_raw_summary import WANT  # noqa: E402
 
-OURS = re.compile(r"k_step_|k_hist_to_raw|k_mi_finalize|k_zero|k_reduce|k_pad|k_sampler|k_lncc|k_mi_|k_conv|k_add_partials")
-VOXELS = {"mi256": 256 ** 3, "lncc720": 720 * 640 * 720}
+OURS = re.compile(r"k_step_|k_hist_to_raw|k_mi_finalize|k_zero|k_reduce|k_pad|k_sampler|k_lncc|k_mi_|k_conv|"
+                  r"k_add_partials|k_smooth|k_trilinear|k_normalize|k_mse|k_jacobian")
+VOXELS = {"mi256": 256 ** 3, "lncc720": 720 * 640 * 720, "wu720": 720 * 640 * 720}
 
 
 def short(name):
@@ -83,7 +84,8 @@ def full(rep, out, workload):
             nv = VOXELS[workload]
             fo.write(f"   traffic (dram read + write) per launch: {traffic:.4e} B = {traffic / nv:.2f} B/voxel "
                      f"over {nv} voxels\n")
-            res[name.split("<")[0]] = {"workload": workload, "dram_bytes_per_launch": traffic,
+            key = name.split("<")[0] if workload != "wu720" else name  # the two k_smooth kernels
+            res[key] = {"workload": workload, "dram_bytes_per_launch": traffic,
                                        "voxels": nv, "bytes_per_voxel": round(traffic / nv, 3)}
     return res
 
@@ -99,7 +101,7 @@ def main(tag, d):
         traffic = json.load(open(tp))
     for p in sorted(glob.glob(os.path.join(d, "full_*.ncu-rep"))):
         k = os.path.basename(p)[len("full_"):-len(".ncu-rep")]
-        wl = "lncc720" if "lncc" in k else "mi256"  # capture names: full_<kernel>
+        wl = "lncc720" if "lncc" in k else "wu720" if k.startswith("wu") else "mi256"  # full_<kernel>
         for name, v in full(p, f"profiles/{tag}_full_{k}.txt", wl).items():
             v["round"] = tag
             traffic[name] = v
