@@ -62,7 +62,9 @@ constexpr int NSTAGE = 3;  // input planes in flight (cp.async ring)
 
 template <int R, int CH>
 struct Smem {
-    static constexpr int HX = TX + 2 * R, HY = TY + 2 * R, ROW = CH * HX;
+    // ROW: floats per row, with room for the up-to-3-float shift that 16-byte aligns the
+    // row's first chunk (V16 loads); ROW is a multiple of 4 so every row starts aligned
+    static constexpr int HX = TX + 2 * R, HY = TY + 2 * R, ROW = (CH * HX + 3 + 3) / 4 * 4;
     float raw[NSTAGE][HY][ROW];  // haloed input planes, filled by cp.async (zero-fill outside)
     float X[HY][TX * CH];        // x-convolved rows (the top barrier of the next plane protects it)
 };
@@ -72,11 +74,18 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, int src_bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int R, int CH, bool ADAM>
+// V16: rows of CH * nx floats start 16-byte aligned, so the haloed tile row moves in
+// 16-byte cp.async chunks (the row's first element sits `sh` floats into the stage row;
+// chunks left of the lattice or past its end are zero-filled by src_bytes).
+template <int R, int CH, bool ADAM, bool V16>
 __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
     using S = Smem<R, CH>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -104,18 +113,34 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
 
     // The haloed tile of plane p, as rows of CH * HX consecutive floats, copied
     // asynchronously (zero outside the lattice and for planes outside the volume). A
-    // thread's tile elements are fixed for the whole z march: their in-plane source
-    // offsets (-1 outside the lattice) are computed once. Each thread always commits one
-    // group per plane (possibly empty) so the wait counts line up.
-    constexpr int NEL = S::HY * S::ROW, KL = (NEL + NT - 1) / NT;
+    // thread's tile elements (or 16-byte chunks) are fixed for the whole z march: their
+    // in-plane source offsets and byte counts are computed once. Each thread always
+    // commits one group per plane (possibly empty) so the wait counts line up.
+    const int e0 = (x0 - R) * CH;                 // the tile row's first element in the lattice row
+    const int sh = V16 ? e0 - ((e0 >> 2) << 2) : 0;  // its float offset in the stage row
+    constexpr int NCH = (S::ROW) / 4;              // chunks per stage row (V16)
+    constexpr int NEL = V16 ? S::HY * NCH : S::HY * (CH * S::HX);
+    constexpr int KL = (NEL + NT - 1) / NT;
     int32_t src_off[KL];
+    int8_t src_bytes[KL];
 #pragma unroll
     for (int k = 0; k < KL; ++k) {
         const int q = t + k * NT;
-        const int r = q / S::ROW, e = q - r * S::ROW;
-        const int yy = y0 - R + r;
-        const int xe = (x0 - R) * CH + e;
-        src_off[k] = (q < NEL && yy >= 0 && yy < P.ny && xe >= 0 && xe < P.nx * CH) ? yy * P.nx * CH + xe : -1;
+        if (V16) {
+            const int r = q / NCH, c = q - r * NCH;
+            const int yy = y0 - R + r;
+            const int a = ((e0 >> 2) << 2) + 4 * c;  // chunk start, a multiple of 4 (>= 0 or all left)
+            const int nb = (q < NEL && yy >= 0 && yy < P.ny && a >= 0) ? min(max(P.nx * CH - a, 0), 4) * 4 : 0;
+            src_off[k] = nb ? yy * P.nx * CH + a : 0;
+            src_bytes[k] = (int8_t)nb;
+        } else {
+            const int r = q / (CH * S::HX), e = q - r * (CH * S::HX);
+            const int yy = y0 - R + r;
+            const int xe = e0 + e;
+            const bool ok = q < NEL && yy >= 0 && yy < P.ny && xe >= 0 && xe < P.nx * CH;
+            src_off[k] = ok ? yy * P.nx * CH + xe : 0;
+            src_bytes[k] = ok ? 4 : 0;
+        }
     }
     auto issue = [&](int64_t p, int stage) {
         const bool pin = p >= 0 && p < P.nz_global;
@@ -125,8 +150,14 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
         for (int k = 0; k < KL; ++k) {
             const int q = t + k * NT;
             if (q < NEL) {
-                const bool ok = pin && src_off[k] >= 0;
-                cp_async4(dst + q, ok ? src + src_off[k] : P.in, ok ? 4 : 0);
+                const int nb = pin ? src_bytes[k] : 0;
+                if (V16) {
+                    const int r = q / NCH, c = q - r * NCH;
+                    cp_async16(dst + r * S::ROW + 4 * c, nb ? src + src_off[k] : P.in, nb);
+                } else {
+                    const int r = q / (CH * S::HX), e = q - r * (CH * S::HX);
+                    cp_async4(dst + r * S::ROW + e, nb ? src + src_off[k] : P.in, nb);
+                }
             }
         }
         cp_async_commit();
@@ -140,8 +171,10 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
     }
     // Adam operands of the next output voxel, loaded one plane ahead
     float pu[CH], pm1[CH], pm2[CH];
-    auto fetch = [&](int64_t q) {
-        const int64_t o = ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx) * CH;
+    // element offset of the thread's output voxel in plane zc0; + plane * CH per plane
+    const int64_t pstride = P.plane * CH;
+    int64_t o_next = ((zc0 - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx) * CH;
+    auto fetch = [&](int64_t o) {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             pu[c] = P.u[o + c];
@@ -149,7 +182,7 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
             pm2[c] = P.m2[o + c];
         }
     };
-    if (ADAM && own) fetch(zc0);
+    if (ADAM && own) fetch(o_next);
     int stage = 0;
     for (int64_t p = pstart; p < pend; ++p) {
         // plane p + NSTAGE - 1 goes into the stage read two planes ago (freed by the
@@ -166,7 +199,7 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
         for (int j = t; j < S::HY * CH * (TX / XR); j += NT) {
             const int r = j / (CH * (TX / XR)), rc = j - r * (CH * (TX / XR));
             const int m = rc / CH, c = rc - m * CH;
-            const float* in = &sm.raw[stage][r][XR * m * CH + c];
+            const float* in = &sm.raw[stage][r][sh + XR * m * CH + c];
             float w_[XR + 2 * R];
 #pragma unroll
             for (int i = 0; i < XR + 2 * R; ++i) w_[i] = in[i * CH];
@@ -199,7 +232,8 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
         const float inv = !P.renorm ? 1.0f
                           : (q >= R && q + R < P.nz_global) ? inv_xy_full
                                                             : 1.0f / (wxy * wsum<R>(P, q, P.nz_global));
-        const int64_t o = ((q - P.z_begin) * P.plane + (int64_t)gy * P.nx + gx) * CH;
+        const int64_t o = o_next;
+        o_next += pstride;
         float v[CH];
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
@@ -212,14 +246,15 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
             float cu[CH], c1[CH], c2[CH];
 #pragma unroll
             for (int c = 0; c < CH; ++c) cu[c] = pu[c], c1[c] = pm1[c], c2[c] = pm2[c];
-            if (q + 1 < zc1) fetch(q + 1);
+            if (q + 1 < zc1) fetch(o_next);
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 const float m = fmaf(P.b1, c1[c], P.omb1 * v[c]);
                 const float s2 = fmaf(P.b2, c2[c], P.omb2 * v[c] * v[c]);
                 P.m1[o + c] = m;
                 P.m2[o + c] = s2;
-                P.u[o + c] = cu[c] - P.lr_c1 * m / (sqrtf(s2 * P.inv_c2) + P.eps);
+                // fast (2-ulp) division: well inside the fp32 budget of the update
+                P.u[o + c] = cu[c] - P.lr_c1 * __fdividef(m, sqrtf(s2 * P.inv_c2) + P.eps);
             }
         } else {
 #pragma unroll
@@ -247,16 +282,22 @@ int launch(Params P, cudaStream_t st) {
     const size_t smem = sizeof(Smem<R, CH>);
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(k_smooth<R, CH, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smooth<R, CH, ADAM>, NT, smem);
+        for (auto fn : {k_smooth<R, CH, ADAM, true>, k_smooth<R, CH, ADAM, false>})
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smooth<R, CH, ADAM, true>, NT, smem);
         per_sm = std::max(per_sm, 1);
     }
+    const bool v16 = ((uintptr_t)P.in & 15) == 0 && (P.nx * CH) % 4 == 0;
     const int64_t tx = (P.nx + TX - 1) / TX, ty = (P.ny + TY - 1) / TY;
     const int64_t nzs = P.z_end - P.z_begin;
     P.zchunk = pick_zchunk(tx * ty, nzs, (int64_t)per_sm * num_sms(), R);
     const int64_t chunks = (nzs + P.zchunk - 1) / P.zchunk;
     if (ty > 65535 || chunks > 65535) return set_error(FFDP_INVALID_ARGUMENT, "gp_convolve: grid too large");
-    k_smooth<R, CH, ADAM><<<dim3((unsigned)tx, (unsigned)ty, (unsigned)chunks), NT, smem, st>>>(P);
+    const dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)chunks);
+    if (v16)
+        k_smooth<R, CH, ADAM, true><<<grid, NT, smem, st>>>(P);
+    else
+        k_smooth<R, CH, ADAM, false><<<grid, NT, smem, st>>>(P);
     return check_launch(ADAM ? "sobolev_adam" : "gp_convolve");
 }
 
