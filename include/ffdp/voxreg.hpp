@@ -66,6 +66,7 @@ struct Dims3 {
     std::int64_t nx = 0, ny = 0, nz = 0;
     std::int64_t voxels() const { return nx * ny * nz; }
     bool positive() const { return nx > 0 && ny > 0 && nz > 0; }
+    std::int64_t operator[](int c) const { return c == 0 ? nx : c == 1 ? ny : nz; }
     bool operator==(const Dims3& o) const { return nx == o.nx && ny == o.ny && nz == o.nz; }
     bool operator!=(const Dims3& o) const { return !(*this == o); }
     ffdp_dims c() const { return ffdp_dims{nx, ny, nz}; }
@@ -618,6 +619,233 @@ class DeformableStep {
     std::optional<ParzenKernel> kernel_;
     float shift_f_ = 0, shift_m_ = 0;
 };
+
+
+// ------------------------------------------------------------------ smoothing (smoothing.hpp:25-125)
+enum class EdgeMode { zero_pad, renormalize };
+
+// gaussian_taps (smoothing.hpp:25-39): truncated at ceil(3 sigma), normalized to sum 1.
+inline std::vector<double> gaussian_taps(double sigma) {
+    if (!std::isfinite(sigma) || sigma < 0) throw std::invalid_argument("gaussian_taps: sigma must be finite and >= 0");
+    if (sigma == 0) return {1.0};
+    const auto radius = static_cast<std::int64_t>(std::ceil(3.0 * sigma));
+    std::vector<double> taps(static_cast<std::size_t>(2 * radius + 1));
+    double sum = 0;
+    for (std::int64_t k = -radius; k <= radius; ++k) {
+        const double w = std::exp(-0.5 * (static_cast<double>(k) / sigma) * (static_cast<double>(k) / sigma));
+        taps[static_cast<std::size_t>(k + radius)] = w;
+        sum += w;
+    }
+    for (auto& w : taps) w /= sum;
+    return taps;
+}
+
+// box_taps (smoothing.hpp:42-46).
+inline std::vector<double> box_taps(int window) {
+    if (window < 1 || window % 2 == 0) throw std::invalid_argument("box_taps: window must be odd and >= 1");
+    return std::vector<double>(static_cast<std::size_t>(window), 1.0 / window);
+}
+
+// gp_convolve / separable_convolve (distops.hpp:84-101, smoothing.hpp:98-105) of a whole
+// volume or warp field on one GPU: one z-marching kernel (ffdp_gp_convolve).
+inline Volume3 gp_convolve(const Volume3& v, const std::vector<double>& taps, EdgeMode mode = EdgeMode::zero_pad,
+                           cudaStream_t s = nullptr) {
+    if (taps.size() % 2 == 0) throw std::invalid_argument("gp_convolve: kernel must be odd");
+    Volume3 out = Volume3::uninitialized(v.dims);
+    out.spacing = v.spacing;
+    out.origin = v.origin;
+    check(ffdp_gp_convolve(v.data.data(), out.data.data(), v.dims.c(), full_slab(v.dims.nz), 1, taps.data(),
+                           static_cast<int>(taps.size()), mode == EdgeMode::renormalize ? 1 : 0, s));
+    return out;
+}
+
+inline WarpField gp_convolve(const WarpField& w, const std::vector<double>& taps, EdgeMode mode = EdgeMode::zero_pad,
+                             cudaStream_t s = nullptr) {
+    if (taps.size() % 2 == 0) throw std::invalid_argument("gp_convolve: kernel must be odd");
+    WarpField out = WarpField::uninitialized(w.dims);
+    check(ffdp_gp_convolve(w.data.data(), out.data.data(), w.dims.c(), full_slab(w.dims.nz), 3, taps.data(),
+                           static_cast<int>(taps.size()), mode == EdgeMode::renormalize ? 1 : 0, s));
+    return out;
+}
+
+// ------------------------------------------------------------------ Adam (adam.hpp:14-50)
+// AdamState of a warp field: moments on the device (fp32, the reference's T storage).
+struct AdamState {
+    DeviceArray<float> m1, m2;
+    std::int64_t step = 0;
+    double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+
+    static AdamState zeros(std::size_t n, cudaStream_t s = nullptr) {
+        AdamState a;
+        a.m1 = DeviceArray<float>(n);
+        a.m2 = DeviceArray<float>(n);
+        a.m1.zero(s);
+        a.m2.zero(s);
+        return a;
+    }
+};
+
+// adam_step (adam.hpp:30-50) on a warp field, in place (the Adam epilogue of
+// ffdp_sobolev_adam with a single unit tap).
+inline void adam_step(WarpField& param, const WarpField& grad, AdamState& st, double lr, cudaStream_t s = nullptr) {
+    if (param.dims != grad.dims || param.data.size() != st.m1.size() || param.data.size() != st.m2.size())
+        throw std::invalid_argument("adam_step: shape mismatch");
+    st.step += 1;
+    const double one = 1.0;
+    check(ffdp_sobolev_adam(grad.data.data(), param.data.data(), st.m1.data(), st.m2.data(), param.dims.c(),
+                            full_slab(param.dims.nz), &one, 1, lr, st.beta1, st.beta2, st.eps, st.step, s));
+}
+
+// The warp update of one deformable iteration (registration.hpp:313-317): gp_convolve(g_u,
+// gaussian(sigma_grad), renormalize) fused with adam_step (u, st updated in place), then
+// `out` = gp_convolve(u, gaussian(sigma_warp), renormalize).
+inline void warp_update(WarpField& u, const WarpField& g_u, AdamState& st, double lr_norm, WarpField& out,
+                        double sigma_grad = 1.0, double sigma_warp = 0.5, cudaStream_t s = nullptr) {
+    if (u.dims != g_u.dims || u.dims != out.dims || u.data.size() != st.m1.size())
+        throw std::invalid_argument("adam_step: shape mismatch");
+    const auto tg = gaussian_taps(sigma_grad), tw = gaussian_taps(sigma_warp);
+    st.step += 1;
+    check(ffdp_sobolev_adam(g_u.data.data(), u.data.data(), st.m1.data(), st.m2.data(), u.dims.c(),
+                            full_slab(u.dims.nz), tg.data(), static_cast<int>(tg.size()), lr_norm, st.beta1,
+                            st.beta2, st.eps, st.step, s));
+    check(ffdp_gp_convolve(u.data.data(), out.data.data(), u.dims.c(), full_slab(u.dims.nz), 3, tw.data(),
+                           static_cast<int>(tw.size()), 1, s));
+}
+
+// ------------------------------------------------------------------ multi-scale (resample.hpp:48-146)
+inline Dims3 resample_dims(Dims3 d, double factor) {
+    ffdp_dims o;
+    check(ffdp_resample_dims(d.c(), factor, &o));
+    return Dims3{o.nx, o.ny, o.nz};
+}
+
+// resample_scale (resample.hpp:48-103): anti-alias (factor < 1) + trilinear onto
+// ceil(n * factor), first / last voxel centres kept (spacing rescaled like the reference).
+inline Volume3 resample_scale(const Volume3& v, double factor, cudaStream_t s = nullptr) {
+    const Dims3 nd = resample_dims(v.dims, factor);
+    Volume3 out = Volume3::uninitialized(nd);
+    for (int c = 0; c < 3; ++c) {
+        const double ratio = static_cast<double>(v.dims[c] - 1) / static_cast<double>(nd[c] - 1);
+        out.spacing[c] = v.dims[c] > 1 ? v.spacing[c] * ratio : v.spacing[c];
+    }
+    out.origin = v.origin;
+    check(ffdp_resample_scale(v.data.data(), v.dims.c(), factor, out.data.data(), nullptr, s));
+    return out;
+}
+
+// resample_warp (resample.hpp:108-146).
+inline WarpField resample_warp(const WarpField& w, Dims3 nd, cudaStream_t s = nullptr) {
+    if (!nd.positive()) throw std::invalid_argument("resample_warp: dims must be positive");
+    WarpField out = WarpField::uninitialized(nd);
+    check(ffdp_resample_warp(w.data.data(), w.dims.c(), out.data.data(), nd.c(), s));
+    return out;
+}
+
+// normalize_intensities (registration.hpp:100-115).
+inline Volume3 normalize_intensities(const Volume3& v, cudaStream_t s = nullptr) {
+    Volume3 out = Volume3::uninitialized(v.dims);
+    out.spacing = v.spacing;
+    out.origin = v.origin;
+    check(ffdp_normalize(v.data.data(), v.dims.voxels(), out.data.data(), s));
+    return out;
+}
+
+// jacobian_positive_fraction (metrics.hpp:145-176).
+inline double jacobian_positive_fraction(const WarpField& u, cudaStream_t s = nullptr) {
+    double f = 0;
+    check(ffdp_jacobian_positive(u.data.data(), u.dims.c(), &f, s));
+    return f;
+}
+
+// ------------------------------------------------------------------ the driver (registration.hpp:48-331)
+struct AffineMap {
+    Mat3 matrix = Mat3::identity();
+    Vec3 translation{{0, 0, 0}};
+};
+
+struct ScaleStep {
+    double downsample = 1;  // 4 means quarter resolution
+    int iterations = 0;
+};
+
+struct ScaleSchedule {
+    std::vector<ScaleStep> steps;
+    double lr = 0.5;
+    double sigma_grad = 1.0;
+    double sigma_warp = 0.5;
+    LossParams loss;
+
+    void validate() const {
+        if (steps.empty()) throw std::invalid_argument("schedule: no scale steps");
+        for (std::size_t i = 0; i < steps.size(); ++i) {
+            if (!(steps[i].downsample >= 1)) throw std::invalid_argument("schedule: downsample factors must be >= 1");
+            if (steps[i].iterations < 0) throw std::invalid_argument("schedule: iterations must be >= 0");
+            if (i > 0 && steps[i].downsample > steps[i - 1].downsample)
+                throw std::invalid_argument("schedule: factors must be non-increasing toward 1");
+        }
+        if (!(lr > 0) || !(sigma_grad >= 0) || !(sigma_warp >= 0))
+            throw std::invalid_argument("schedule: bad lr/sigma");
+    }
+};
+
+struct TraceEntry {
+    int scale_index = 0;
+    int iteration = 0;
+    double loss = 0;
+};
+
+struct NumericalError : std::runtime_error {
+    std::vector<TraceEntry> trace;
+    NumericalError(const std::string& what, std::vector<TraceEntry> t)
+        : std::runtime_error(what), trace(std::move(t)) {}
+};
+
+// deformable_stage (registration.hpp:230-331) on one GPU: per scale resample F and M on
+// the device, carry the warp over (resample_warp), build the fused step once (zero-
+// bordered M + workspace) and iterate step -> warp_update. The loss is read every
+// iteration (the reference's non-finite check and trace, 290-296).
+inline WarpField deformable_stage(const Volume3& fixed, const Volume3& moving, const AffineMap& affine,
+                                  const ScaleSchedule& schedule, std::vector<TraceEntry>* trace = nullptr,
+                                  int scale_index_base = 0, cudaStream_t s = nullptr) {
+    schedule.validate();
+    if (!fixed.same_lattice(moving))
+        throw std::invalid_argument("deformable_stage: F and M must share a lattice (registration.hpp:268-270)");
+    SamplerArgs args;
+    args.A = affine.matrix;
+    args.t = affine.translation;
+    std::optional<WarpField> warp;
+    for (std::size_t sc = 0; sc < schedule.steps.size(); ++sc) {
+        const auto& step = schedule.steps[sc];
+        const double factor = 1.0 / step.downsample;
+        std::optional<Volume3> fr, mr;
+        if (factor != 1.0) {
+            fr.emplace(resample_scale(fixed, factor, s));
+            mr.emplace(resample_scale(moving, factor, s));
+        }
+        const Volume3& f_s = fr ? *fr : fixed;
+        const Volume3& m_s = mr ? *mr : moving;
+        warp = warp ? resample_warp(*warp, f_s.dims, s) : WarpField::zeros(f_s.dims, s);
+        // registration.hpp:257-264: lr in voxels of the level -> normalized units
+        const Dims3 d = f_s.dims;
+        const double pitch = (2.0 / static_cast<double>(d.nx - 1) + 2.0 / static_cast<double>(d.ny - 1) +
+                              2.0 / static_cast<double>(d.nz - 1)) / 3.0;
+        const double lr_norm = schedule.lr * pitch;
+        DeformableStep st(f_s, m_s, schedule.loss, s);
+        AdamState adam = AdamState::zeros(warp->data.size(), s);
+        WarpField g = WarpField::uninitialized(d), spare = WarpField::uninitialized(d);
+        for (int it = 0; it < step.iterations; ++it) {
+            const StepResult r = st.step(*warp, args, g, true);
+            if (!std::isfinite(r.loss))
+                throw NumericalError("deformable stage diverged (non-finite loss)",
+                                     trace ? *trace : std::vector<TraceEntry>{});
+            if (trace) trace->push_back({scale_index_base + static_cast<int>(sc), it, r.loss});
+            warp_update(*warp, g, adam, lr_norm, spare, schedule.sigma_grad, schedule.sigma_warp, s);
+            std::swap(*warp, spare);
+        }
+    }
+    if (warp->dims != fixed.dims) warp = resample_warp(*warp, fixed.dims, s);
+    return std::move(*warp);
+}
 
 }  // namespace voxreg
 }  // namespace ffdp

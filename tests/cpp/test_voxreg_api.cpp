@@ -49,6 +49,14 @@ void or_mi_backward(const double* vi, const double* vj, int64_t n, const or_parz
 int or_synth_pair(uint64_t seed, or_dims d, int k, double max_disp, double* fixed, double* moving,
                   double* true_warp);
 void or_normalize_intensities(double* v, int64_t n);
+void or_separable_convolve(double* data, or_dims dims, int channels, const double* taps, int ntaps, int mode);
+void or_adam_step(double* param, const double* grad, double* m1, double* m2, int64_t n, double lr, double beta1,
+                  double beta2, double eps, int64_t step);
+int or_resample_scale(const double* in, or_dims d, double factor, double* out, or_dims* out_dims);
+int or_deformable_stage(const double* fixed, const double* moving, or_dims d, const double* A, const double* t,
+                        int nsteps, const double* downsample, const int* iterations, double lr, double sigma_grad,
+                        double sigma_warp, int loss_kind, int window, double eps, int ants, int bins, int mi_kind,
+                        double* warp_out, double* trace);
 double or_step_lncc(const double* f, const double* m, or_dims d, const double* u, const double* A, const double* t,
                     int window, double eps, int ants, double* g_u, double* moved_out, double* grad_moved_out);
 double or_step_mi(const double* f, const double* m, or_dims d, const double* u, const double* A, const double* t,
@@ -357,6 +365,127 @@ static void step_tests() {
     });
 }
 
+// ---------------------------------------------------------------- the warp update and the driver
+static std::vector<float> uniform_f32(uint64_t seed, size_t n, double lo, double hi) {
+    or_rng r;
+    or_rng_init(&r, seed);
+    std::vector<float> v(n);
+    for (auto& x : v) x = float(lo + (hi - lo) * or_rng_uniform(&r));
+    return v;
+}
+
+static void driver_tests() {
+    run("smoothing: gp_convolve (box zero_pad, gaussian renormalize) matches the oracle", [] {
+        const or_dims d{37, 19, 11};
+        const size_t n = size_t(d.nx * d.ny * d.nz);
+        for (int ch : {1, 3}) {
+            auto h = uniform_f32(901 + ch, n * ch, -1, 1);
+            for (int mode = 0; mode < 2; ++mode) {
+                const auto taps = mode ? V::gaussian_taps(1.0) : V::box_taps(7);
+                std::vector<double> ref = widen(h);
+                or_separable_convolve(ref.data(), d, ch, taps.data(), int(taps.size()), mode);
+                const auto em = mode ? V::EdgeMode::renormalize : V::EdgeMode::zero_pad;
+                std::vector<float> got;
+                if (ch == 1)
+                    got = V::gp_convolve(V::Volume3::from_host(dims(d), h.data()), taps, em).to_host();
+                else
+                    got = V::gp_convolve(V::WarpField::from_host(dims(d), h.data()), taps, em).to_host();
+                EXPECT_TRUE(maxrel(got, ref) <= 1e-6);
+            }
+        }
+        EXPECT_THROW(V::box_taps(4), std::invalid_argument);
+        EXPECT_THROW(V::gaussian_taps(-1.0), std::invalid_argument);
+    });
+    run("adam: adam_step (adam.hpp:30-50) matches the oracle over 3 steps", [] {
+        const or_dims d{34, 9, 5};
+        const size_t n = size_t(3 * d.nx * d.ny * d.nz);
+        auto p = uniform_f32(911, n, -1, 1);
+        std::vector<double> pr = widen(p), ar(n, 0.0), br(n, 0.0);
+        auto param = V::WarpField::from_host(dims(d), p.data());
+        auto st = V::AdamState::zeros(n);
+        for (int k = 1; k <= 3; ++k) {
+            auto g = uniform_f32(920 + k, n, -1, 1);
+            std::vector<double> gd = widen(g);
+            or_adam_step(pr.data(), gd.data(), ar.data(), br.data(), int64_t(n), 0.01, 0.9, 0.999, 1e-8, k);
+            V::adam_step(param, V::WarpField::from_host(dims(d), g.data()), st, 0.01);
+        }
+        EXPECT_TRUE(st.step == 3);
+        EXPECT_TRUE(maxrel(param.to_host(), pr) <= 1e-6);
+        EXPECT_TRUE(maxrel(st.m1.download(), ar) <= 1e-6 && maxrel(st.m2.download(), br) <= 1e-6);
+    });
+    run("multi-scale: resample_scale (resample.hpp:48-103) matches the oracle", [] {
+        const or_dims d{45, 34, 21};
+        auto h = uniform_f32(931, size_t(d.nx * d.ny * d.nz), 0, 1);
+        std::vector<double> hd = widen(h);
+        for (double f : {0.5, 0.25, 2.0}) {
+            or_dims od;
+            or_resample_scale(hd.data(), d, f, nullptr, &od);
+            std::vector<double> ref(size_t(od.nx * od.ny * od.nz));
+            or_resample_scale(hd.data(), d, f, ref.data(), &od);
+            auto got = V::resample_scale(V::Volume3::from_host(dims(d), h.data()), f);
+            EXPECT_TRUE(got.dims == dims(od));
+            EXPECT_TRUE(maxrel(got.to_host(), ref) <= 2e-6);
+        }
+        EXPECT_THROW(V::resample_scale(V::Volume3::zeros(dims(d)), 0.0), std::invalid_argument);
+    });
+    for (int mi = 0; mi < 2; ++mi) {
+        run(mi ? "driver: deformable_stage MI (B-spline) matches the oracle stage"
+               : "driver: deformable_stage LNCC matches the oracle stage",
+            [mi] {
+                Pair p = make_pair(22, 20, 18, 4242, mi == 1);
+                const int64_t n = p.d.nx * p.d.ny * p.d.nz;
+                const double ds[2] = {2, 1};
+                const int its[2] = {3, 3};
+                std::vector<double> wref(size_t(3 * n)), tref(6);
+                // lr 0.5 voxels overshoots on this MI pair (the MI falls after the first update
+                // and oscillates -- the reference does the same); 0.1 keeps the dynamics
+                // non-chaotic so fp32 vs fp64 stays comparable over the iterations
+                const double lr = mi ? 0.1 : 0.5;
+                const int rc = or_deformable_stage(p.fd.data(), p.md.data(), p.d, p.A, p.t, 2, ds, its, lr, 1.0, 0.5,
+                                                   mi, 7, 1e-5, 1, 32, 1, wref.data(), tref.data());
+                EXPECT_TRUE(rc == 0);
+                V::ScaleSchedule sch;
+                sch.steps = {V::ScaleStep{2, 3}, V::ScaleStep{1, 3}};
+                sch.loss.kind = mi ? V::LossKind::mi : V::LossKind::lncc;
+                sch.loss.mi_bspline_kernel = true;
+                sch.lr = lr;
+                V::AffineMap aff;
+                for (int i = 0; i < 9; ++i) aff.matrix.m[i] = p.A[i];
+                for (int i = 0; i < 3; ++i) aff.translation[i] = p.t[i];
+                std::vector<V::TraceEntry> trace;
+                auto w = V::deformable_stage(V::Volume3::from_host(dims(p.d), p.f.data()),
+                                             V::Volume3::from_host(dims(p.d), p.m.data()), aff, sch, &trace);
+                EXPECT_TRUE(trace.size() == 6);
+                double tr = 0;
+                for (size_t i = 0; i < trace.size() && i < 6; ++i) tr = std::max(tr, rel(trace[i].loss, tref[i]));
+                EXPECT_TRUE(tr <= 1e-5);
+                // warp: l2 to 2e-4 and every voxel within a tenth of one Adam step
+                const auto wh = w.to_host();
+                double num = 0, den = 0, mx = 0;
+                for (size_t i = 0; i < wref.size(); ++i) {
+                    const double dd = double(wh[i]) - wref[i];
+                    num += dd * dd;
+                    den += wref[i] * wref[i];
+                    mx = std::max(mx, std::fabs(dd));
+                }
+                const double step = lr * (2.0 / 21 + 2.0 / 19 + 2.0 / 17) / 3.0;
+                std::printf("  stage %s: trace rel %.3g, warp l2 %.3g, max/step %.3g\n", mi ? "mi" : "lncc", tr,
+                            std::sqrt(num / den), mx / step);
+                EXPECT_TRUE(std::sqrt(num / den) <= 2e-4);
+                EXPECT_TRUE(mx <= 0.1 * step);
+            });
+    }
+    run("driver: schedule rejects (registration.hpp:60-72)", [] {
+        V::ScaleSchedule sch;
+        EXPECT_THROW(sch.validate(), std::invalid_argument);
+        sch.steps = {V::ScaleStep{1, 2}, V::ScaleStep{2, 2}};
+        EXPECT_THROW(sch.validate(), std::invalid_argument);
+        sch.steps = {V::ScaleStep{1, 2}};
+        sch.lr = 0;
+        EXPECT_THROW(sch.validate(), std::invalid_argument);
+    });
+}
+
 int main() {
     if (ffdp_device_check() != FFDP_OK) {
         std::printf("no usable sm_100 device: %s\n", ffdp_last_error());
@@ -366,6 +495,7 @@ int main() {
     lncc_tests();
     mi_tests();
     step_tests();
+    driver_tests();
     std::printf("%d checks, %d failed\n", g_checks, g_failed);
     return g_failed ? 1 : 0;
 }
