@@ -612,8 +612,29 @@ __global__ void __launch_bounds__(NT, 3) k_step_mi_grad(const Params P) {
 // in flight per iteration.
 __host__ __device__ constexpr int grad_tab_floats(int B) { return 4 * (B + 2 * PAD) * ((B + 2 * PAD + 3) / 4 * 4); }
 
+#ifndef FFDP_GR_HINT
+#define FFDP_GR_HINT 0
+#endif
+#ifndef FFDP_GR_MINB
+#define FFDP_GR_MINB 2
+#endif
+#ifndef FFDP_GR_CTAS
+#define FFDP_GR_CTAS 2
+#endif
+#ifndef FFDP_GR_UNROLL
+#define FFDP_GR_UNROLL 2
+#endif
+// streaming (read-once / write-once) cache hints for the records, F and g_u (FFDP_GR_HINT)
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return FFDP_GR_HINT ? __ldcs(p) : __ldg(p); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+    if (FFDP_GR_HINT)
+        __stcs(p, v);
+    else
+        *p = v;
+}
+
 template <bool VEC>
-__global__ void __launch_bounds__(256) k_step_mi_grad_rec(const float* __restrict__ f, const float4* __restrict__ rec,
+__global__ void __launch_bounds__(256, FFDP_GR_MINB) k_step_mi_grad_rec(const float* __restrict__ f, const float4* __restrict__ rec,
                                                           float* __restrict__ g_u, int64_t n, const double* table,
                                                           int B) {
     extern __shared__ __align__(16) float sg[];
@@ -655,19 +676,33 @@ __global__ void __launch_bounds__(256) k_step_mi_grad_rec(const float* __restric
                          int64_t i) {
             const float g0 = dl(fv.x, r0.x), g1 = dl(fv.y, r1.x), g2 = dl(fv.z, r2.x), g3 = dl(fv.w, r3.x);
             float4* o = reinterpret_cast<float4*>(g_u + 12 * i);
-            o[0] = make_float4(r0.y * g0, r0.z * g0, r0.w * g0, r1.y * g1);
-            o[1] = make_float4(r1.z * g1, r1.w * g1, r2.y * g2, r2.z * g2);
-            o[2] = make_float4(r2.w * g2, r3.y * g3, r3.z * g3, r3.w * g3);
+            st_stream(o, make_float4(r0.y * g0, r0.z * g0, r0.w * g0, r1.y * g1));
+            st_stream(o + 1, make_float4(r1.z * g1, r1.w * g1, r2.y * g2, r2.z * g2));
+            st_stream(o + 2, make_float4(r2.w * g2, r3.y * g3, r3.z * g3, r3.w * g3));
         };
         int64_t i = tid;
+#if FFDP_GR_UNROLL == 4
+        for (; i + 3 * stride < n4; i += 4 * stride) {
+            float4 fv[4], r[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t k = i + q * stride;
+                fv[q] = ld_stream(reinterpret_cast<const float4*>(f) + k);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) r[q][e] = ld_stream(rec + 4 * k + e);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) group(fv[q], r[q][0], r[q][1], r[q][2], r[q][3], i + q * stride);
+        }
+#endif
         for (; i + stride < n4; i += 2 * stride) {
             const int64_t j = i + stride;
-            const float4 fa = __ldg(reinterpret_cast<const float4*>(f) + i);
-            const float4 fb = __ldg(reinterpret_cast<const float4*>(f) + j);
-            const float4 a0 = __ldg(rec + 4 * i), a1 = __ldg(rec + 4 * i + 1), a2 = __ldg(rec + 4 * i + 2),
-                         a3 = __ldg(rec + 4 * i + 3);
-            const float4 b0 = __ldg(rec + 4 * j), b1 = __ldg(rec + 4 * j + 1), b2 = __ldg(rec + 4 * j + 2),
-                         b3 = __ldg(rec + 4 * j + 3);
+            const float4 fa = ld_stream(reinterpret_cast<const float4*>(f) + i);
+            const float4 fb = ld_stream(reinterpret_cast<const float4*>(f) + j);
+            const float4 a0 = ld_stream(rec + 4 * i), a1 = ld_stream(rec + 4 * i + 1), a2 = ld_stream(rec + 4 * i + 2),
+                         a3 = ld_stream(rec + 4 * i + 3);
+            const float4 b0 = ld_stream(rec + 4 * j), b1 = ld_stream(rec + 4 * j + 1), b2 = ld_stream(rec + 4 * j + 2),
+                         b3 = ld_stream(rec + 4 * j + 3);
             group(fa, a0, a1, a2, a3, i);
             group(fb, b0, b1, b2, b3, j);
         }
@@ -846,7 +881,7 @@ int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ff
     }
     const bool vec = (((uintptr_t)fi | (uintptr_t)rec | (uintptr_t)g_u) & 15) == 0;
     const int64_t work = vec ? n / 4 : n;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8LL * num_sms()));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)FFDP_GR_CTAS * num_sms()));
     if (vec)
         k_step_mi_grad_rec<true><<<grid, 256, smem, st>>>(fi, reinterpret_cast<const float4*>(rec), g_u, n, table, B);
     else
