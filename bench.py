@@ -551,7 +551,12 @@ def run_registration(shape, schedule_spec):
             "schedule": [{"downsample": d, "iterations": n} for d, n in schedule_spec],
             "seconds": round(ms / 1e3, 4), "voxel_iterations": vox_iters,
             "gvoxel_iterations_per_s": round(vox_iters / (ms * 1e-3) / 1e9, 3),
-            "loss_first": trace[0].loss, "loss_last": trace[-1].loss,
+            # per scale: the loss falls within a scale; across scales it is not comparable
+            # (a 7^3 window sees less structure at full resolution than at 1/4)
+            "loss_per_scale": [{"downsample": d, "first": round(min(e.loss for e in trace if e.scale_index == i and
+                                                                    e.iteration == 0), 6),
+                                "last": round([e.loss for e in trace if e.scale_index == i][-1], 6)}
+                               for i, (d, _) in enumerate(schedule_spec)],
             "per_iteration": "fused warp+LNCC step (2 kernels + reduction), ffdp_sobolev_adam, ffdp_gp_convolve"}
 
 
