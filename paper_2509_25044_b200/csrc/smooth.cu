@@ -122,12 +122,14 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
     constexpr int NEL = V16 ? S::HY * NCH : S::HY * (CH * S::HX);
     constexpr int KL = (NEL + NT - 1) / NT;
     int32_t src_off[KL];
+    int16_t dst_off[KL];  // float offset in a stage (-1: no element)
     int8_t src_bytes[KL];
 #pragma unroll
     for (int k = 0; k < KL; ++k) {
         const int q = t + k * NT;
         if (V16) {
             const int r = q / NCH, c = q - r * NCH;
+            dst_off[k] = (int16_t)(q < NEL ? r * S::ROW + 4 * c : -1);
             const int yy = y0 - R + r;
             const int a = ((e0 >> 2) << 2) + 4 * c;  // chunk start, a multiple of 4 (>= 0 or all left)
             const int nb = (q < NEL && yy >= 0 && yy < P.ny && a >= 0) ? min(max(P.nx * CH - a, 0), 4) * 4 : 0;
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
             src_bytes[k] = (int8_t)nb;
         } else {
             const int r = q / (CH * S::HX), e = q - r * (CH * S::HX);
+            dst_off[k] = (int16_t)(q < NEL ? r * S::ROW + e : -1);
             const int yy = y0 - R + r;
             const int xe = e0 + e;
             const bool ok = q < NEL && yy >= 0 && yy < P.ny && xe >= 0 && xe < P.nx * CH;
@@ -145,23 +148,36 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
     auto issue = [&](int64_t p, int stage) {
         const bool pin = p >= 0 && p < P.nz_global;
         const float* src = P.in + (pin ? (p - P.buf_z0) * P.plane * CH : 0);
+        asm("" : "+l"(src));  // one plane base; each copy is then one wide add of its offset
         float* dst = &sm.raw[stage][0][0];
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
-            const int q = t + k * NT;
-            if (q < NEL) {
+            if (dst_off[k] >= 0) {
                 const int nb = pin ? src_bytes[k] : 0;
-                if (V16) {
-                    const int r = q / NCH, c = q - r * NCH;
-                    cp_async16(dst + r * S::ROW + 4 * c, nb ? src + src_off[k] : P.in, nb);
-                } else {
-                    const int r = q / (CH * S::HX), e = q - r * (CH * S::HX);
-                    cp_async4(dst + r * S::ROW + e, nb ? src + src_off[k] : P.in, nb);
-                }
+                const float* sp = src + (uint32_t)src_off[k];
+                if (V16)
+                    cp_async16(dst + dst_off[k], sp, nb);
+                else
+                    cp_async4(dst + dst_off[k], sp, nb);
             }
         }
         cp_async_commit();
     };
+
+    // x taps: a job is a run of XR outputs of one channel of one row, sliding over the
+    // XR + 2R inputs in registers (runs of 8 measured no faster for R = 3); job order
+    // (run, channel) inside a row keeps a row's lanes on distinct banks. A thread's jobs
+    // are the same every plane: their stage / X offsets are computed once.
+    constexpr int XR = 4, NJ = S::HY * CH * (TX / XR), XJ = (NJ + NT - 1) / NT;
+    int32_t xj_in[XJ], xj_out[XJ];
+#pragma unroll
+    for (int jj = 0; jj < XJ; ++jj) {
+        const int j = t + jj * NT;
+        const int r = j / (CH * (TX / XR)), rc = j - r * (CH * (TX / XR));
+        const int m = rc / CH, c = rc - m * CH;
+        xj_in[jj] = j < NJ ? r * S::ROW + sh + XR * m * CH + c : -1;
+        xj_out[jj] = r * (TX * CH) + XR * m * CH + c;
+    }
 
     const int64_t pstart = zc0 - R, pend = zc1 + R;  // input planes of this chunk
 #pragma unroll
@@ -192,23 +208,20 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
         else cp_async_commit();
         cp_async_wait<NSTAGE - 1>();  // this thread's copies of plane p have landed
         __syncthreads();             // everyone's have; X is free
-        // x taps: a job is a run of XR outputs of one channel of one row, sliding over the
-        // XR + 2R inputs in registers (runs of 8 measured no faster for R = 3); job order
-        // (run, channel) inside a row keeps a row's lanes on distinct banks
-        constexpr int XR = 4;
-        for (int j = t; j < S::HY * CH * (TX / XR); j += NT) {
-            const int r = j / (CH * (TX / XR)), rc = j - r * (CH * (TX / XR));
-            const int m = rc / CH, c = rc - m * CH;
-            const float* in = &sm.raw[stage][r][sh + XR * m * CH + c];
+#pragma unroll
+        for (int jj = 0; jj < XJ; ++jj) {
+            if (xj_in[jj] < 0) continue;
+            const float* in = &sm.raw[stage][0][0] + xj_in[jj];
             float w_[XR + 2 * R];
 #pragma unroll
             for (int i = 0; i < XR + 2 * R; ++i) w_[i] = in[i * CH];
+            float* xo = &sm.X[0][0] + xj_out[jj];
 #pragma unroll
             for (int o = 0; o < XR; ++o) {
                 float acc = 0.0f;
 #pragma unroll
                 for (int k = 0; k <= 2 * R; ++k) acc = fmaf(P.w[k], w_[o + k], acc);
-                sm.X[r][(XR * m + o) * CH + c] = acc;
+                xo[o * CH] = acc;
             }
         }
         __syncthreads();
@@ -253,8 +266,11 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
                 const float s2 = fmaf(P.b2, c2[c], P.omb2 * v[c] * v[c]);
                 P.m1[o + c] = m;
                 P.m2[o + c] = s2;
-                // fast (2-ulp) division: well inside the fp32 budget of the update
-                P.u[o + c] = cu[c] - P.lr_c1 * __fdividef(m, sqrtf(s2 * P.inv_c2) + P.eps);
+                // sqrt(v / c2) as v * rsqrt(v) (approximate MUFU, v = 0 -> 0) and a fast
+                // division: a few ulp, well inside the fp32 budget of the update
+                const float vv = s2 * P.inv_c2;
+                const float sq = vv * rsqrtf(fmaxf(vv, 1e-37f));
+                P.u[o + c] = cu[c] - P.lr_c1 * __fdividef(m, sq + P.eps);
             }
         } else {
 #pragma unroll
