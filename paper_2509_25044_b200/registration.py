@@ -123,12 +123,19 @@ class _Scale:
         self.m = V.MovingImage(m_s)
         self.params = params
         self.ws = V.StepWorkspace(f_s.device, params.bins)
-        self.shifts = (V.intensity_shift(f_s), V.intensity_shift(m_s)) if params.kind == "lncc" else None
+        self.shifts = ((V.intensity_shift(f_s), V.intensity_shift(m_s)) if params.kind == "lncc" and params.ants_approx
+                       else None)
         self.g_u = torch.empty(tuple(f_s.shape) + (3,), dtype=torch.float32, device=f_s.device)
         self.trace = torch.zeros(max(1, iterations), dtype=torch.float64, device=f_s.device)
         self.n = f_s.numel()
 
     def step(self, u, A, t, it):
+        p = self.params
+        if p.kind == "mse" or (p.kind == "lncc" and not p.ants_approx) or (p.kind == "mi" and p.mi_approx_forward):
+            # operator-kernel composition (voxreg._composite_step): the loss comes back on the host
+            r = V.warp_loss_step(self.f, self.m, u, A, t, p, g_u=self.g_u, ws=self.ws)
+            self.trace[it] = r.loss
+            return self.g_u
         V.warp_loss_step(self.f, self.m, u, A, t, self.params, g_u=self.g_u, ws=self.ws, shifts=self.shifts,
                          sync=False)
         if self.params.kind == "lncc":

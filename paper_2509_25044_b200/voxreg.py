@@ -548,8 +548,10 @@ def mi_backward(upstream: float, img_i, img_j, hist: JointHistogram, kernel: Par
 # ---------------------------------------------------------------- the fused step
 @dataclass
 class LossParams:
-    """LossParams (registration.hpp:33-46), restricted to the fused step's losses."""
-    kind: str = "lncc"  # "lncc" | "mi"
+    """LossParams (registration.hpp:33-46). The fused step kernels cover LNCC (ANTs) and
+    exact-forward MI; MSE, exact-mode LNCC and approximate-forward MI run through the
+    operator kernels (warp_loss_step composes them)."""
+    kind: str = "lncc"  # "lncc" | "mi" | "mse"
     window: int = 7
     epsilon: float = 1e-5
     ants_approx: bool = True
@@ -635,10 +637,10 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
         raise InvalidArgument("warp_loss_step: F and M must share a lattice (registration.hpp:268-270)")
     win = mi.window()
     ws.miss.zero_()
+    if params.kind == "mse" or (params.kind == "lncc" and not params.ants_approx) or \
+            (params.kind == "mi" and params.mi_approx_forward):
+        return _composite_step(f, win, u, ca, params, g_u, ws, sync)
     if params.kind == "lncc":
-        if not params.ants_approx:
-            raise InvalidArgument("warp_loss_step: the fused LNCC step implements the ANTs backward "
-                                  "(use lncc_forward_fused / lncc_backward_fused for exact mode)")
         if shifts is None:
             shifts = (intensity_shift(f), intensity_shift(mi.interior.contiguous()))
         ws.sum_n.zero_()
@@ -651,8 +653,6 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
         loss = 1.0 - float(ws.sum_n.item()) / n
     elif params.kind == "mi":
         k = params.make_kernel()
-        if params.mi_approx_forward:
-            raise InvalidArgument("warp_loss_step: the fused MI step uses the exact Parzen forward")
         if ws.bins != params.bins:
             raise InvalidArgument("warp_loss_step: workspace built for a different bin count")
         rec = ws.records(_dims(f.shape), slab) if k.kind == PARZEN_BSPLINE3 else None
@@ -665,3 +665,35 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
     else:
         raise InvalidArgument(f"warp_loss_step: unknown loss kind {params.kind!r}")
     return StepResult(loss, g_u, int(ws.miss.item()))
+
+
+def _composite_step(f, win, u, ca, params: LossParams, g_u, ws: StepWorkspace, sync: bool) -> StepResult:
+    """The deformable step for the losses the fused kernels do not cover, composed from the
+    operator kernels exactly as the reference composes it (registration.hpp:277-312 at
+    H = 1): moved = fused_sample(M, u) -> dist_mse (distops.hpp:260-282) / LNCC exact
+    backward (lncc.hpp:226-280, upstream 1) / MI with the approximate forward
+    (mi.hpp:275-354) and mi_backward_impl (upstream -1) -> fused_sample_backward(want
+    warp)."""
+    n = f.numel()
+    dims = _dims(f.shape)
+    moved = torch.empty(f.shape, dtype=torch.float32, device=f.device)
+    lib.ffdp_sampler_fwd(win, _ptr(u), dims, C.byref(ca), _ptr(moved), 0, None, _ptr(ws.miss), _stream())
+    if params.kind == "mse":
+        ws.sum_n.zero_()
+        gm = torch.empty_like(moved)
+        lib.ffdp_mse(_ptr(f), _ptr(moved), n, n, _ptr(gm), _ptr(ws.sum_n), _stream())
+        loss = (ws.sum_n / n) if not sync else float(ws.sum_n.item()) / n
+    elif params.kind == "lncc":
+        res, state = lncc_forward_fused(f, moved, params.window, params.epsilon)
+        _, gm = lncc_backward_fused(1.0, state, f, moved, params.ants_approx)
+        loss = res.loss
+    else:
+        k = params.make_kernel()
+        res = (mi_forward_approx if params.mi_approx_forward else mi_forward_exact)(f, moved, params.bins, k)
+        _, gm = mi_backward(-1.0, f, moved, res.hist, k, check_samples=False)
+        loss = -res.mi
+    lib.ffdp_sampler_bwd(_ptr(gm), win, _ptr(u), dims, C.byref(ca), WANT_WARP, None, _ptr(g_u), None, _ptr(ws.miss),
+                         _stream())
+    if not sync:
+        return StepResult(float("nan"), g_u)
+    return StepResult(float(loss), g_u, int(ws.miss.item()))

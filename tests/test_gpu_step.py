@@ -117,3 +117,35 @@ def test_step_mi_sparse_histogram(V, orc, shape, seed):
     res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="mi", bins=32, mi_bspline_kernel=True))
     assert res.loss == pytest.approx(ref["loss"], rel=LOSS_RTOL)
     assert maxrel(host(res.g_u), ref["g_u"]) <= GRAD_MAXREL
+
+
+@pytest.mark.parametrize("mode", ["mse", "lncc_exact", "mi_approx", "mi_gaussian"])
+def test_step_operator_composed_losses(V, orc, mode):
+    """The step for the losses outside the fused kernels (registration.hpp:277-312 with
+    dist_mse distops.hpp:260-282, LNCC exact backward lncc.hpp:226-280, MI approximate
+    forward mi.hpp:275-354) and the Gaussian-Parzen fused MI step, against the oracle."""
+    from gpu_util import dev, host, maxrel
+    from oracle import step_inputs
+    loss_kind = "lncc" if mode.startswith("lncc") or mode == "mse" else "mi"
+    si = step_inputs(orc, (17, 19, 23), seed=4242, loss=loss_kind)
+    if mode == "mse":
+        moved = orc.sample(si.m, si.u, si.A, si.t)["out"]
+        n = moved.size
+        ref_loss = float(np.sum((moved - si.f) ** 2) / n)
+        ref_gu = orc.sample(si.m, si.u, si.A, si.t, upstream=2.0 * (moved - si.f) / n)["warp"]
+        p = V.LossParams(kind="mse")
+    elif mode == "lncc_exact":
+        r = orc.step_lncc(si.f, si.m, si.u, si.A, si.t, ants=False)
+        ref_loss, ref_gu = r["loss"], r["g_u"]
+        p = V.LossParams(kind="lncc", ants_approx=False)
+    elif mode == "mi_approx":
+        r = orc.step_mi(si.f, si.m, si.u, orc.parzen("gaussian", 32), si.A, si.t, approx=True)
+        ref_loss, ref_gu = r["loss"], r["g_u"]
+        p = V.LossParams(kind="mi", bins=32, mi_approx_forward=True)
+    else:
+        r = orc.step_mi(si.f, si.m, si.u, orc.parzen("gaussian", 32), si.A, si.t)
+        ref_loss, ref_gu = r["loss"], r["g_u"]
+        p = V.LossParams(kind="mi", bins=32)
+    res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, p)
+    assert res.loss == pytest.approx(ref_loss, rel=1e-5)
+    assert maxrel(host(res.g_u), ref_gu) <= 1e-4
