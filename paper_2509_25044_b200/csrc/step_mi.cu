@@ -300,9 +300,6 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
 #ifndef FFDP_MI_HPAD
 #define FFDP_MI_HPAD 2
 #endif
-#ifndef FFDP_MI_L2PF
-#define FFDP_MI_L2PF 0
-#endif
 constexpr int HPAD = FFDP_MI_HPAD;
 constexpr int HDUMMY = HPAD == 2 ? 4 : 0;  // dummy rows per copy (HPAD 2)
 // Fixed-point scale 2^S (S = FFDP_MI_BS_LOG2, odd):
@@ -434,19 +431,6 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
             const float(&ff)[4] = L.ff;
             const bool(&ok)[4] = L.ok;
             float4* rp = P.rec + (w.bi - zrec);
-            if (FFDP_MI_L2PF > 0 && lane < 16) {
-                // pull the F and u lines of the unit FFDP_MI_L2PF iterations ahead into L2:
-                // lanes 0-11 take the 4 x 3 lines of u, lanes 12-15 the 4 lines of F
-                const int64_t ahead = unit + FFDP_MI_L2PF * stride;
-                if (ahead < P.nunits) {
-                    const Unit wa = unit_coords(P, (uint32_t)ahead, 0);
-                    const int row = lane < 12 ? lane / 3 : lane - 12;
-                    const char* a = lane < 12 ? reinterpret_cast<const char*>(P.u + 3 * (wa.bi + (int64_t)row * P.nx)) +
-                                                    128 * (lane % 3)
-                                              : reinterpret_cast<const char*>(P.f + wa.bi + (int64_t)row * P.nx);
-                    if (wa.y0 + row < P.ny) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-                }
-            }
             Cell c[4];
             unit_cells(P, w, L.uu, c);
             Corners cr[4];
@@ -461,11 +445,7 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
                 if (REC) {
                     float d[3];
                     mw = interp_grad(cr[k], c[k], d);
-#ifdef FFDP_EXP_NOREC
-                    if (ok[k] && d[0] == 1234.5f) *rp = make_float4(mw, d[0], d[1], d[2]);
-#else
                     if (ok[k]) *rp = make_float4(mw, P.g.dscale[0] * d[0], P.g.dscale[1] * d[1], P.g.dscale[2] * d[2]);
-#endif
                     rp += P.nx;
                 } else {
                     mw = interp(cr[k], c[k]);
@@ -475,20 +455,11 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
                 const int32_t mj = bspline_scaled<BC>(mw, B, BS_WSCALE, kJ);
                 // HPAD 2: voxels outside the lattice add into the copy's dummy rows
                 uint32_t* h = (HPAD == 2 && !ok[k]) ? mine - HPAD * LD - HPAD + LD * LD : mine + mi * LD + mj;
-#ifdef FFDP_EXP_NOATOM
-                uint32_t x = 0;
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) x += __float_as_uint(kI[a] * kJ[b]);
-                if (x == 0x12345) h[0] = x;
-#else
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
                     for (int b = 0; b < 4; ++b)
                         atomicAdd(h + a * LD + b, __float_as_uint(kI[a] * kJ[b]));
-#endif
             }
         }
         if (++iter == BS_FOLD_ITERS || base + stride >= P.nunits) {
