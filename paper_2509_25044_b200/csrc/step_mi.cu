@@ -24,13 +24,6 @@
 namespace ffdp {
 namespace mstep {
 
-// 4-byte asynchronous global -> shared copy; src_bytes = 0 writes a zero (no global read).
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 constexpr int NT = 256;  // pass 2: 8 warps x 128 voxels per CTA iteration
 
@@ -288,11 +281,6 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
 //    masking gone the fixed-point scales fold into the B-spline coefficients;
 //  * per-unit row pointers for F, u and the records (one 64-bit add per row);
 //  * with BC > 0 every counter offset of the 4 x 4 footprint is an immediate.
-// FFDP_MI_CPA = 1 stages the next unit's F and u rows in shared memory by cp.async:
-// measured slower (0.200 vs 0.177 ms at 256^3) -- the 64 KB stage takes L1 from the gather.
-#ifndef FFDP_MI_CPA
-#define FFDP_MI_CPA 0
-#endif
 // Histogram pad: 4 (out-of-lattice voxels get intensity -1, all of whose bins land in the
 // pad) or 2 (the minimum for in-range intensities; out-of-lattice voxels are redirected
 // to 4 dummy rows after the table). 2 keeps the shared footprint under the 100 KB
@@ -320,9 +308,7 @@ __host__ __device__ constexpr int bs_stride(int B) {
     return ((bs_ld(B) * (bs_ld(B) + HDUMMY) + 31) / 32) * 32 + (32 / HCOPY);
 }
 inline size_t bs_smem_bytes(int B) {
-    // + the cp.async stage of each warp: F (4 x 32) and u (4 x 96) floats of one unit
-    return sizeof(unsigned long long) * B * B + sizeof(uint32_t) * (size_t)HCOPY * bs_stride(B) +
-           (FFDP_MI_CPA ? sizeof(float) * 512 * (HNT / 32) : 0);
+    return sizeof(unsigned long long) * B * B + sizeof(uint32_t) * (size_t)HCOPY * bs_stride(B);
 }
 
 // Cubic B-spline weights of the 4 bins m_lo..m_lo+3 scaled by C (mi.hpp:28-140, bspline3),
@@ -359,58 +345,23 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
     uint32_t* mine = s32 + (lane % HCOPY) * CS + HPAD * LD + HPAD;
     const int64_t stride = (int64_t)gridDim.x * (HNT / 32);
     const int64_t zrec = (P.z_begin - P.buf_z0) * P.plane;  // records cover the interior planes
-    // The unit's F and u rows. With FFDP_MI_CPA they are staged in shared memory by
-    // cp.async one unit ahead (the copies need no registers, so the next unit's loads are
-    // in flight during this unit's gathers and histogram updates); otherwise they are
-    // loaded at the top of the unit.
+    // The unit's F and u rows. (Loading them one unit ahead -- in registers after the
+    // interpolation, or staged in shared memory by cp.async -- measured slower: 0.206 and
+    // 0.200 vs 0.177 ms at 256^3; the first spills at 64 registers, the second takes L1
+    // from the gather.)
     struct Ld {
         Unit w;
         float ff[4], uu[12];
         bool ok[4];
     };
-    float* stage = reinterpret_cast<float*>(smem + sizeof(unsigned long long) * B * B +
-                                            sizeof(uint32_t) * (size_t)HCOPY * CS) + warp * 512;
-    auto issue = [&](int64_t unit) {
-        const Unit wu = unit_coords(P, (uint32_t)unit, lane);
-        const int32_t x0 = wu.x - lane;
-        const float* fr = P.f + (wu.bi - (wu.vx ? wu.x : 0)) + x0;          // row y0, x0
-        const float* ur = P.u + 3 * ((wu.bi - (wu.vx ? wu.x : 0)) + x0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool row = wu.y0 + k < P.ny;
-            cp_async4(stage + k * 32 + lane, row && wu.vx ? fr + lane : P.f, row && wu.vx ? 4 : 0);
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const int e = lane + 32 * j;                    // element of the row's 96 floats
-                const bool ok = row && x0 + e / 3 < P.nx;
-                cp_async4(stage + 128 + k * 96 + e, ok ? ur + e : P.u, ok ? 4 : 0);
-            }
-            fr += P.nx;
-            ur += 3 * P.nx;
-        }
-        cp_async_commit();
-    };
     auto load = [&](int64_t unit, Ld& L) {
         L.w = unit_coords(P, (uint32_t)unit, lane);
-        if (FFDP_MI_CPA) {
-            cp_async_wait_all();
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                L.ok[k] = L.w.vx && (L.w.y0 + k) < P.ny;
-                L.ff[k] = L.ok[k] ? stage[k * 32 + lane] : -1.0f;  // -1: every bin in the pad rows
-#pragma unroll
-                for (int c = 0; c < 3; ++c) L.uu[3 * k + c] = stage[128 + k * 96 + 3 * lane + c];
-            }
-            __syncwarp();  // the stage is read: the next unit's copies may land
-            return;
-        }
         const float* fp = P.f + L.w.bi;
         const float* up = P.u + 3 * L.w.bi;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             L.ok[k] = L.w.vx && (L.w.y0 + k) < P.ny;
-            L.ff[k] = L.ok[k] ? __ldg(fp) : -1.0f;  // -1: every bin in the pad rows
+            L.ff[k] = L.ok[k] ? __ldg(fp) : -1.0f;  // -1: every bin in the pad rows (HPAD 4)
             L.uu[3 * k] = L.ok[k] ? __ldg(up) : 0.0f;
             L.uu[3 * k + 1] = L.ok[k] ? __ldg(up + 1) : 0.0f;
             L.uu[3 * k + 2] = L.ok[k] ? __ldg(up + 2) : 0.0f;
@@ -418,15 +369,12 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
             up += 3 * P.nx;
         }
     };
-    if (FFDP_MI_CPA && (int64_t)blockIdx.x * (HNT / 32) + warp < P.nunits)
-        issue((int64_t)blockIdx.x * (HNT / 32) + warp);
     int iter = 0;
     for (int64_t base = (int64_t)blockIdx.x * (HNT / 32); base < P.nunits; base += stride) {
         const int64_t unit = base + warp;
         if (unit < P.nunits) {
             Ld L;
             load(unit, L);
-            if (FFDP_MI_CPA && unit + stride < P.nunits) issue(unit + stride);
             const Unit& w = L.w;
             const float(&ff)[4] = L.ff;
             const bool(&ok)[4] = L.ok;
