@@ -505,9 +505,10 @@ inline std::pair<Volume3, Volume3> mi_backward(double upstream, const Volume3& i
 }
 
 // ------------------------------------------------------------------ the fused deformable step
-enum class LossKind { lncc, mi };
+enum class LossKind { mse, lncc, mi };
 
-// LossParams (registration.hpp:33-46) restricted to the fused step's losses.
+// LossParams (registration.hpp:33-46). DeformableStep fuses LNCC (ANTs) and exact-forward
+// MI; the other combinations run through loss_and_grad (deformable_stage composes them).
 struct LossParams {
     LossKind kind = LossKind::lncc;
     int window = 7;
@@ -535,6 +536,7 @@ class DeformableStep {
         : f_(fixed.data.data()), dims_(fixed.dims), p_(p), stream_(s) {
         if (!fixed.same_lattice(moving))
             throw std::invalid_argument("DeformableStep: F and M must share a lattice (registration.hpp:268-270)");
+        if (p.kind == LossKind::mse) throw std::invalid_argument("DeformableStep: MSE runs through loss_and_grad");
         if (p.kind == LossKind::lncc && !p.ants_approx)
             throw std::invalid_argument("DeformableStep: the fused LNCC step implements the ANTs backward");
         if (p.kind == LossKind::mi && p.mi_approx_forward)
@@ -800,6 +802,38 @@ struct NumericalError : std::runtime_error {
         : std::runtime_error(what), trace(std::move(t)) {}
 };
 
+// loss_and_grad (registration.hpp:123-173) through the operator kernels: MSE (dist_mse),
+// LNCC (lncc_forward_fused + lncc_backward_fused, upstream 1) or MI (exact / approximate
+// forward + mi_backward_impl, upstream -1, loss = -MI). Returns the loss and dL/dmoved.
+inline std::pair<double, Volume3> loss_and_grad(const Volume3& f, const Volume3& moved, const LossParams& p,
+                                                cudaStream_t s = nullptr) {
+    if (!f.same_lattice(moved)) throw std::invalid_argument("loss_and_grad: lattices differ");
+    if (p.kind == LossKind::mse) {
+        Volume3 g = Volume3::uninitialized(f.dims);
+        DeviceArray<double> sum(1);
+        sum.zero(s);
+        check(ffdp_mse(f.data.data(), moved.data.data(), f.dims.voxels(), f.dims.voxels(), g.data.data(),
+                       sum.data(), s));
+        return {sum.download(s)[0] / static_cast<double>(f.dims.voxels()), std::move(g)};
+    }
+    if (p.kind == LossKind::lncc) {
+        auto fw = lncc_forward_fused(f, moved, p.window, p.epsilon, false, s);
+        auto bw = lncc_backward_fused(1.0, fw.second, f, moved, p.ants_approx, s);
+        return {fw.first.loss, std::move(bw.second)};
+    }
+    const ParzenKernel k = p.mi_bspline_kernel ? ParzenKernel::bspline3(p.bins) : ParzenKernel::gaussian(p.bins);
+    const MiResult r = p.mi_approx_forward ? mi_forward_approx(f, moved, p.bins, k, s)
+                                           : mi_forward_exact(f, moved, p.bins, k, s);
+    auto bw = detail::mi_backward_impl(-1.0, f, moved, r.hist, k, s);
+    return {-r.mi, std::move(bw.second)};
+}
+
+// Whether DeformableStep's fused kernels cover the loss (else deformable_stage composes
+// fused_sample -> loss_and_grad -> fused_sample_backward).
+inline bool fused_loss(const LossParams& p) {
+    return (p.kind == LossKind::lncc && p.ants_approx) || (p.kind == LossKind::mi && !p.mi_approx_forward);
+}
+
 // deformable_stage (registration.hpp:230-331) on one GPU: per scale resample F and M on
 // the device, carry the warp over (resample_warp), build the fused step once (zero-
 // bordered M + workspace) and iterate step -> warp_update. The loss is read every
@@ -830,11 +864,23 @@ inline WarpField deformable_stage(const Volume3& fixed, const Volume3& moving, c
         const double pitch = (2.0 / static_cast<double>(d.nx - 1) + 2.0 / static_cast<double>(d.ny - 1) +
                               2.0 / static_cast<double>(d.nz - 1)) / 3.0;
         const double lr_norm = schedule.lr * pitch;
-        DeformableStep st(f_s, m_s, schedule.loss, s);
+        std::optional<DeformableStep> st;
+        if (fused_loss(schedule.loss)) st.emplace(f_s, m_s, schedule.loss, s);
         AdamState adam = AdamState::zeros(warp->data.size(), s);
         WarpField g = WarpField::uninitialized(d), spare = WarpField::uninitialized(d);
         for (int it = 0; it < step.iterations; ++it) {
-            const StepResult r = st.step(*warp, args, g, true);
+            StepResult r;
+            if (st) {
+                r = st->step(*warp, args, g, true);
+            } else {
+                // ring_sample -> loss -> ring_sample_backward(want warp) through the operators
+                const Volume3 moved = fused_sample(m_s, &*warp, args, s);
+                auto lg = loss_and_grad(f_s, moved, schedule.loss, s);
+                r.loss = lg.first;
+                SamplerGradWant want;
+                want.warp = true;
+                g = std::move(*fused_sample_backward(lg.second, m_s, &*warp, args, want, s).warp);
+            }
             if (!std::isfinite(r.loss))
                 throw NumericalError("deformable stage diverged (non-finite loss)",
                                      trace ? *trace : std::vector<TraceEntry>{});
@@ -845,6 +891,89 @@ inline WarpField deformable_stage(const Volume3& fixed, const Volume3& moving, c
     }
     if (warp->dims != fixed.dims) warp = resample_warp(*warp, fixed.dims, s);
     return std::move(*warp);
+}
+
+// affine_stage (registration.hpp:176-219): Adam on the 12 affine parameters from the
+// identity (state shared by all scales); per iteration moved = fused_sample(M_s, zero warp,
+// A, t) on F_s's lattice, loss_and_grad, fused_sample_backward(want affine + translation).
+inline AffineMap affine_stage(const Volume3& fixed, const Volume3& moving, const ScaleSchedule& schedule,
+                              std::vector<TraceEntry>* trace = nullptr, int scale_index_base = 0,
+                              cudaStream_t s = nullptr) {
+    schedule.validate();
+    AffineMap map;
+    double m1[12] = {0}, m2[12] = {0};
+    std::int64_t step_count = 0;
+    for (std::size_t sc = 0; sc < schedule.steps.size(); ++sc) {
+        const auto& step = schedule.steps[sc];
+        const double factor = 1.0 / step.downsample;
+        std::optional<Volume3> fr, mr;
+        if (factor != 1.0) {
+            fr.emplace(resample_scale(fixed, factor, s));
+            mr.emplace(resample_scale(moving, factor, s));
+        }
+        const Volume3& f_s = fr ? *fr : fixed;
+        const Volume3& m_s = mr ? *mr : moving;
+        const WarpField zero = WarpField::zeros(f_s.dims, s);  // outputs on F's lattice
+        for (int it = 0; it < step.iterations; ++it) {
+            SamplerArgs args;
+            args.A = map.matrix;
+            args.t = map.translation;
+            const Volume3 moved = fused_sample(m_s, &zero, args, s);
+            auto lg = loss_and_grad(f_s, moved, schedule.loss, s);
+            if (!std::isfinite(lg.first))
+                throw NumericalError("affine stage diverged (non-finite loss)",
+                                     trace ? *trace : std::vector<TraceEntry>{});
+            if (trace) trace->push_back({scale_index_base + static_cast<int>(sc), it, lg.first});
+            SamplerGradWant want;
+            want.affine = want.translation = true;
+            const SamplerGrads gr = fused_sample_backward(lg.second, m_s, &zero, args, want, s);
+            // adam_step<double> on the 12 parameters (adam.hpp:30-50)
+            double params[12], grad[12];
+            for (int i = 0; i < 9; ++i) params[i] = map.matrix.m[i], grad[i] = gr.affine->m[i];
+            for (int i = 0; i < 3; ++i) params[9 + i] = map.translation[i], grad[9 + i] = (*gr.translation)[i];
+            ++step_count;
+            const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+            const double c1 = 1.0 - std::pow(b1, static_cast<double>(step_count));
+            const double c2 = 1.0 - std::pow(b2, static_cast<double>(step_count));
+            for (int i = 0; i < 12; ++i) {
+                m1[i] = b1 * m1[i] + (1.0 - b1) * grad[i];
+                m2[i] = b2 * m2[i] + (1.0 - b2) * grad[i] * grad[i];
+                params[i] -= schedule.lr * (m1[i] / c1) / (std::sqrt(m2[i] / c2) + eps);
+            }
+            for (int i = 0; i < 9; ++i) map.matrix.m[i] = params[i];
+            for (int i = 0; i < 3; ++i) map.translation[i] = params[9 + i];
+        }
+    }
+    return map;
+}
+
+// RegistrationConfig / RegistrationResult / register_volumes (registration.hpp:333-368).
+struct RegistrationConfig {
+    ScaleSchedule affine;
+    ScaleSchedule deformable;
+    bool skip_affine = false;
+};
+
+struct RegistrationResult {
+    AffineMap affine;
+    WarpField warp;
+    std::vector<TraceEntry> trace;
+    double jacobian_positive_fraction = 1.0;
+};
+
+inline RegistrationResult register_volumes(const Volume3& fixed, const Volume3& moving,
+                                           const RegistrationConfig& config, cudaStream_t s = nullptr) {
+    RegistrationResult res;
+    const Volume3 f_n = normalize_intensities(fixed, s), m_n = normalize_intensities(moving, s);
+    int base = 0;
+    if (!config.skip_affine) {
+        res.affine = affine_stage(f_n, m_n, config.affine, &res.trace, 0, s);
+        base = static_cast<int>(config.affine.steps.size());
+    }
+    res.warp = deformable_stage(f_n, m_n, res.affine, config.deformable, &res.trace, base, s);
+    const Dims3 d = res.warp.dims;
+    if (d.nx >= 3 && d.ny >= 3 && d.nz >= 3) res.jacobian_positive_fraction = jacobian_positive_fraction(res.warp, s);
+    return res;
 }
 
 }  // namespace voxreg

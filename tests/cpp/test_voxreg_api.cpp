@@ -53,6 +53,9 @@ void or_separable_convolve(double* data, or_dims dims, int channels, const doubl
 void or_adam_step(double* param, const double* grad, double* m1, double* m2, int64_t n, double lr, double beta1,
                   double beta2, double eps, int64_t step);
 int or_resample_scale(const double* in, or_dims d, double factor, double* out, or_dims* out_dims);
+int or_affine_stage(const double* fixed, const double* moving, or_dims d, int nsteps, const double* downsample,
+                    const int* iterations, double lr, int loss_kind, int window, double eps, int ants, int bins,
+                    int mi_kind, double* A_out, double* t_out, double* trace);
 int or_deformable_stage(const double* fixed, const double* moving, or_dims d, const double* A, const double* t,
                         int nsteps, const double* downsample, const int* iterations, double lr, double sigma_grad,
                         double sigma_warp, int loss_kind, int window, double eps, int ants, int bins, int mi_kind,
@@ -475,6 +478,50 @@ static void driver_tests() {
                 EXPECT_TRUE(mx <= 0.1 * step);
             });
     }
+    for (int kind = 0; kind < 3; ++kind) {
+        run(kind == 0 ? "driver: affine_stage MSE matches the oracle"
+                      : kind == 1 ? "driver: affine_stage LNCC matches the oracle" : "driver: affine_stage MI matches the oracle",
+            [kind] {
+                Pair p = make_pair(22, 20, 18, 4242, true);
+                const double ds[2] = {2, 1};
+                const int its[2] = {3, 3};
+                double A[9], t[3], tr[6];
+                EXPECT_TRUE(or_affine_stage(p.fd.data(), p.md.data(), p.d, 2, ds, its, 0.01, kind, 7, 1e-5, 1, 32, 0, A,
+                                            t, tr) == 0);
+                V::ScaleSchedule sch;
+                sch.steps = {V::ScaleStep{2, 3}, V::ScaleStep{1, 3}};
+                sch.lr = 0.01;
+                sch.loss.kind = kind == 0 ? V::LossKind::mse : kind == 1 ? V::LossKind::lncc : V::LossKind::mi;
+                std::vector<V::TraceEntry> trace;
+                const V::AffineMap a = V::affine_stage(V::Volume3::from_host(dims(p.d), p.f.data()),
+                                                       V::Volume3::from_host(dims(p.d), p.m.data()), sch, &trace);
+                EXPECT_TRUE(trace.size() == 6);
+                double e = 0;
+                for (size_t i = 0; i < trace.size() && i < 6; ++i) e = std::max(e, rel(trace[i].loss, tr[i]));
+                EXPECT_TRUE(e <= 1e-5);
+                double da = 0;
+                for (int i = 0; i < 9; ++i) da = std::max(da, std::fabs(a.matrix.m[i] - A[i]));
+                for (int i = 0; i < 3; ++i) da = std::max(da, std::fabs(a.translation[i] - t[i]));
+                EXPECT_TRUE(da <= 1e-5);
+            });
+    }
+    run("driver: register_volumes (affine + deformable, MSE deformable through loss_and_grad)", [] {
+        Pair p = make_pair(22, 20, 18, 4243, false);
+        V::RegistrationConfig cfg;
+        cfg.affine.steps = {V::ScaleStep{2, 2}};
+        cfg.affine.lr = 0.01;
+        cfg.affine.loss.kind = V::LossKind::mi;
+        cfg.deformable.steps = {V::ScaleStep{2, 2}, V::ScaleStep{1, 2}};
+        cfg.deformable.loss.kind = V::LossKind::mse;
+        auto f = V::Volume3::from_host(dims(p.d), p.f.data()), m = V::Volume3::from_host(dims(p.d), p.m.data());
+        const auto r = V::register_volumes(f, m, cfg);
+        EXPECT_TRUE(r.trace.size() == 6 && r.trace[2].scale_index == 1 && r.trace[5].scale_index == 2);
+        EXPECT_TRUE(r.warp.dims == f.dims);
+        EXPECT_TRUE(r.jacobian_positive_fraction > 0.5 && r.jacobian_positive_fraction <= 1.0);
+        bool finite = true;
+        for (const auto& e : r.trace) finite = finite && std::isfinite(e.loss);
+        EXPECT_TRUE(finite);
+    });
     run("driver: schedule rejects (registration.hpp:60-72)", [] {
         V::ScaleSchedule sch;
         EXPECT_THROW(sch.validate(), std::invalid_argument);
