@@ -9,6 +9,7 @@
 // 64-bit fixed-point histogram. Integer sums are order independent, so the histogram
 // (and with it the loss and ghat) is deterministic run to run.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "ffdp_common.cuh"
@@ -382,6 +383,21 @@ static SlabIdx make_slab_idx(const ffdp_dims& d, const ffdp_slab& s) {
 
 bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                           const ffdp_parzen& k);
+// Below this many interior voxels the fused MI step uses the scalar kernels: their 2^-36
+// fixed-point residual counters keep the sparse histograms of tiny lattices exact to
+// ~1e-11, where the quad path's 2^-23 grid is visible in the gradient (bins fed only by
+// tail products); the quad path pays off only on large lattices anyway.
+// FFDP_MI_QUAD_MIN overrides the threshold (tests exercise both paths on one lattice).
+inline int64_t quad_min_voxels() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("FFDP_MI_QUAD_MIN");
+        return e ? std::atoll(e) : (int64_t)(1 << 16);
+    }();
+    return v;
+}
+inline bool mi_use_quad(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m, const ffdp_parzen& k) {
+    return d.nx * d.ny * (s.z_end - s.z_begin) >= quad_min_voxels() && mi_quad_path_applies(d, s, m, k);
+}
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
                  int32_t* miss, cudaStream_t st, float* rec = nullptr, double* table = nullptr,
@@ -462,7 +478,7 @@ int ffdp_step_mi_hist(const float* f, const float* u, ffdp_dims d, ffdp_slab s, 
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!f || !u || !raw || !m.data) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    if (mi_quad_path_applies(d, s, m, *kernel))
+    if (mi_use_quad(d, s, m, *kernel))
         return mi_quad_hist(f, u, d, s, m, *args, *kernel, raw, (unsigned long long*)workspace, miss, st);
     const int B = kernel->bins;
     const int nh = B * B + 2 * B;
@@ -492,7 +508,7 @@ int ffdp_step_mi(const float* f, const float* u, ffdp_dims d, ffdp_slab s, ffdp_
     if (!raw || !table) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null raw/table");
     const int B = kernel->bins;
     cudaMemsetAsync(raw, 0, sizeof(double) * (B * B + 2 * B), (cudaStream_t)stream);
-    const bool use_rec = rec && kernel->kind == FFDP_PARZEN_BSPLINE3 && mi_quad_path_applies(d, s, m, *kernel);
+    const bool use_rec = rec && kernel->kind == FFDP_PARZEN_BSPLINE3 && mi_use_quad(d, s, m, *kernel);
     if (use_rec && workspace) {
         // one rank, caller workspace: pass 1 with the finalize fused into its last CTA
         if (int rc = ffdp_step_mi_hist_final(f, u, d, s, m, args, kernel, raw, -1.0, table, workspace, rec, miss,
@@ -564,7 +580,7 @@ int ffdp_step_mi_grad(const float* f, const float* u, ffdp_dims d, ffdp_slab s, 
     if (!args || !valid_args(*args, &why)) return set_error(FFDP_INVALID_ARGUMENT, "%s", why ? why : "null args");
     if (!f || !u || !table || !g_u || !m.data) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: null pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    if (mi_quad_path_applies(d, s, m, *kernel))
+    if (mi_use_quad(d, s, m, *kernel))
         return mi_quad_grad(f, u, d, s, m, *args, *kernel, table, g_u, miss, st);
     const int B = kernel->bins;
     const ffdp_dims out{d.nx, d.ny, s.nz_global};

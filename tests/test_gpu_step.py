@@ -149,3 +149,28 @@ def test_step_operator_composed_losses(V, orc, mode):
     res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, p)
     assert res.loss == pytest.approx(ref_loss, rel=1e-5)
     assert maxrel(host(res.g_u), ref_gu) <= 1e-4
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 33), (8, 9, 65), (1, 6, 7), (2, 40, 31)])
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_step_ragged_and_thin_lattices(V, orc, shape, loss):
+    """Lattices thinner than the LNCC window, single planes (lattice_coord n = 1,
+    geometry.hpp:101-104) and x extents off the 32-wide warp units, on random
+    intensities and a random sub-voxel warp, against the oracle step."""
+    from gpu_util import dev, host, maxrel
+    r = orc.rng(500 + sum(shape))
+    f = orc.random_volume(r, shape, 0.0, 1.0)
+    m = np.clip(0.7 * f + 0.3 * orc.random_volume(r, shape, 0.0, 1.0), 0.0, 1.0)
+    u = orc.random_volume(r, shape + (3,), -0.01, 0.01)
+    A = np.eye(3) + orc.random_volume(r, (3, 3), -0.02, 0.02)
+    t = orc.random_volume(r, (3,), -0.02, 0.02)
+    f, m, u = (a.astype(np.float32).astype(np.float64) for a in (f, m, u))
+    if loss == "lncc":
+        ref = orc.step_lncc(f, m, u, A, t)
+        p = V.LossParams(kind="lncc")
+    else:
+        ref = orc.step_mi(f, m, u, orc.parzen("bspline3", 32), A, t)
+        p = V.LossParams(kind="mi", bins=32, mi_bspline_kernel=True)
+    res = V.warp_loss_step(dev(f), dev(m), dev(u), A, t, p)
+    assert res.loss == pytest.approx(ref["loss"], rel=1e-5, abs=1e-7)
+    assert maxrel(host(res.g_u), ref["g_u"]) <= 1e-4
