@@ -479,3 +479,225 @@ def sharded_deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine, 
     if tuple(warp.shape[:3]) != tuple(fixed.shape):
         warp = R.resample_warp(warp, fixed.shape)
     return warp
+
+
+# ------------------------------------------------------------------ standalone sharded operators
+# The reference's collective operator API (distops.hpp:54-396) one call at a time: every
+# rank calls in the same order. They compose the operator kernels with the exchanges; the
+# fused ShardedStep is the fast path for the deformable step itself.
+@dataclass
+class DistLoss:
+    """DistLoss (distops.hpp:251-257)."""
+    loss: float
+    grad_moved: torch.Tensor
+    mi_payload_elements: int = 0
+
+
+@dataclass
+class RingSampleGrads:
+    """RingSampleGrads (distops.hpp:170-176): gradients for the rank's own shards."""
+    image: Optional[torch.Tensor] = None
+    warp: Optional[torch.Tensor] = None
+    affine: Optional[np.ndarray] = None
+    translation: Optional[np.ndarray] = None
+
+
+def _args_for(out_spec: ShardSpec, A, t):
+    from . import voxreg as V
+    nz = out_spec.global_shape[0]
+    lo = (-1.0, -1.0, axis_coord(out_spec.lo, nz))
+    hi = (1.0, 1.0, axis_coord(out_spec.hi - 1, nz))
+    return V.SamplerArgs(A=np.eye(3) if A is None else A, t=np.zeros(3) if t is None else t,
+                         bounds=V.DomainBounds(lo, hi))
+
+
+def _moving_window(m_shard: torch.Tensor, u_shard: torch.Tensor, args, m_global_dims, out_spec: ShardSpec):
+    """The moving planes the rank's samples touch (ffdp_sampler_z_extent over its u slab,
+    exact), gathered from their owners: (planes, zero-bordered copy, z0, z1, m_spec)."""
+    from . import voxreg as V
+    from ._lib import lib
+    m_spec = make_shard_spec(m_global_dims, out_spec.world, out_spec.rank)
+    ext = torch.empty(2, dtype=torch.int64, device=u_shard.device)
+    lib.ffdp_sampler_z_extent(V._ptr(u_shard), V._dims(u_shard.shape), V._dims(m_global_dims),
+                              C.byref(args.to_c()), V._ptr(ext), V._stream())
+    lo, hi = ext.tolist()
+    z0, z1 = (lo, hi + 1) if lo <= hi else (0, 0)
+    planes = fetch_planes(m_shard, m_spec, z0, z1)
+    z0, z1 = max(0, z0), max(0, z0) + planes.shape[0]
+    pad = torch.zeros((planes.shape[0] + 4, planes.shape[1] + 4, planes.shape[2] + 4), dtype=torch.float32,
+                      device=m_shard.device)
+    pad[2:-2, 2:-2, 2:-2].copy_(planes)
+    return planes, pad, z0, z1, m_spec
+
+
+def ring_sample(m_shard: torch.Tensor, u_shard: torch.Tensor, A, t, m_global_dims, out_spec: ShardSpec) -> torch.Tensor:
+    """ring_sample (distops.hpp:144-168): the moved image on the rank's output slab. The
+    reference rotates every moving shard around the ring and sums zero-padded partial
+    interpolations; their sum is the global interpolation, computed here from the moving
+    planes the slab's samples actually touch (fetched once, exact)."""
+    from . import voxreg as V
+    from ._lib import Dims, ImageWindow, lib
+    u_shard = V._warp(u_shard, "ring_sample")
+    m_shard = V._vol(m_shard, "ring_sample")
+    args = _args_for(out_spec, A, t)
+    args.validate()
+    _, pad, z0, z1, _ = _moving_window(m_shard, u_shard, args, m_global_dims, out_spec)
+    nz, ny, nx = m_global_dims
+    win = ImageWindow(pad.data_ptr(), Dims(nx, ny, nz), z0, z1, 2)
+    out = torch.empty(tuple(u_shard.shape[:3]), dtype=torch.float32, device=u_shard.device)
+    lib.ffdp_sampler_fwd(win, V._ptr(u_shard), V._dims(u_shard.shape), C.byref(args.to_c()), V._ptr(out), 0, None,
+                         None, V._stream())
+    return out
+
+
+def ring_sample_backward(upstream: torch.Tensor, m_shard: torch.Tensor, u_shard: torch.Tensor, A, t, m_global_dims,
+                         out_spec: ShardSpec, want) -> RingSampleGrads:
+    """ring_sample_backward (distops.hpp:179-248): gradients w.r.t. the rank's u slab, its
+    moving shard (image contributions routed back to the owning ranks, 230-239) and the
+    affine / translation (allreduced, 241-246)."""
+    from . import voxreg as V
+    from ._lib import Dims, ImageWindow, lib
+    u_shard = V._warp(u_shard, "ring_sample_backward")
+    m_shard = V._vol(m_shard, "ring_sample_backward")
+    upstream = V._vol(upstream, "ring_sample_backward")
+    args = _args_for(out_spec, A, t)
+    args.validate()
+    planes, pad, z0, z1, m_spec = _moving_window(m_shard, u_shard, args, m_global_dims, out_spec)
+    nz, ny, nx = m_global_dims
+    win = ImageWindow(pad.data_ptr(), Dims(nx, ny, nz), z0, z1, 2)
+    g = RingSampleGrads()
+    dev = u_shard.device
+    g_img = torch.zeros((nz, ny, nx), dtype=torch.float32, device=dev) if want.image else None
+    g_win = torch.zeros((z1 - z0, ny, nx), dtype=torch.float32, device=dev) if want.image else None
+    if want.warp:
+        g.warp = torch.empty(tuple(u_shard.shape), dtype=torch.float32, device=dev)
+    gat = torch.zeros(12, dtype=torch.float64, device=dev) if (want.affine or want.translation) else None
+    if want.image and z1 > z0:
+        # the image gradient lands on the window's planes: sample through the unpadded
+        # window so g_img shares its dense layout
+        wimg = ImageWindow(planes.data_ptr(), Dims(nx, ny, nz), z0, z1, 0)
+        lib.ffdp_sampler_bwd(V._ptr(upstream), wimg, V._ptr(u_shard), V._dims(u_shard.shape), C.byref(args.to_c()),
+                             V.WANT_IMAGE, V._ptr(g_win), None, None, None, V._stream())
+        g_img[z0:z1] += g_win
+    if want.warp or gat is not None:
+        mask = (V.WANT_WARP if want.warp else 0) | (V.WANT_AFFINE if want.affine else 0) | \
+               (V.WANT_TRANSLATION if want.translation else 0)
+        lib.ffdp_sampler_bwd(V._ptr(upstream), win, V._ptr(u_shard), V._dims(u_shard.shape), C.byref(args.to_c()),
+                             mask, None, V._ptr(g.warp), V._ptr(gat), None, V._stream())
+    if want.image:
+        all_reduce(g_img)  # every rank's window contributions, summed at the owners' planes
+        g.image = g_img[m_spec.lo:m_spec.hi].contiguous()
+    if gat is not None:
+        all_reduce(gat)
+        h = gat.cpu().numpy()
+        if want.affine:
+            g.affine = h[:9].reshape(3, 3).copy()
+        if want.translation:
+            g.translation = h[9:].copy()
+    return g
+
+
+def gp_convolve(slab: torch.Tensor, taps, spec: ShardSpec, mode: str = "zero_pad", sync: bool = True) -> torch.Tensor:
+    """gp_convolve (distops.hpp:84-101): the separable convolution of a z-sharded volume or
+    warp with the neighbours' halo planes (sync), or of the shard treated as a standalone
+    volume along z (sync = False, the ablation)."""
+    from . import voxreg as V
+    from ._lib import Slab
+    taps = np.ascontiguousarray(taps, dtype=np.float64)
+    if taps.size % 2 == 0:
+        raise InvalidArgument("gp_convolve: kernel must be odd")
+    slab = slab.to(torch.float32).contiguous()
+    r = taps.size // 2
+    if not sync or spec.world == 1 or r == 0:
+        return V.gp_convolve(slab, taps, mode)
+    h, lo, hi = halo_exchange(slab, spec, r)
+    return V.gp_convolve(h, taps, mode, slab=Slab(spec.lo - lo, slab.shape[0] + lo + hi, spec.lo, spec.hi,
+                                                  spec.global_shape[0]))
+
+
+def dist_mse(f_shard: torch.Tensor, moved_shard: torch.Tensor, n_total: int) -> DistLoss:
+    """dist_mse (distops.hpp:260-282): allreduced sum of squares over N_total, grad 2 d / N."""
+    from . import voxreg as V
+    from ._lib import lib
+    f, m = V._vol(f_shard, "dist_mse"), V._vol(moved_shard, "dist_mse")
+    if tuple(f.shape) != tuple(m.shape):
+        raise InvalidArgument("dist_mse: shard lattices differ")
+    s = torch.zeros(1, dtype=torch.float64, device=f.device)
+    g = torch.empty_like(m)
+    lib.ffdp_mse(V._ptr(f), V._ptr(m), f.numel(), n_total, V._ptr(g), V._ptr(s), V._stream())
+    s = allreduce_sum(s)
+    return DistLoss(float(s.item()) / n_total, g)
+
+
+def dist_mi(f_shard: torch.Tensor, moved_shard: torch.Tensor, bins: int, kernel, approx_forward: bool,
+            n_total: int) -> DistLoss:
+    """dist_mi (distops.hpp:355-396): local raw histograms, allreduced (B*B + 2B payload,
+    365-373), finalize, loss = -MI, mi_backward_impl on the local shard with upstream -1."""
+    from . import voxreg as V
+    from ._lib import lib
+    f, m = V._vol(f_shard, "dist_mi"), V._vol(moved_shard, "dist_mi")
+    if tuple(f.shape) != tuple(m.shape):
+        raise InvalidArgument("dist_mi: shard lattices differ")
+    b = bins
+    raw = torch.zeros(b * b + 2 * b, dtype=torch.float64, device=f.device)
+    lib.ffdp_mi_hist(V._ptr(f), V._ptr(m), f.numel(), C.byref(kernel.c), int(approx_forward), V._ptr(raw), None,
+                     None, V._stream())
+    raw = allreduce_sum(raw)
+    table = torch.empty(2 * b * b + 2 * b + 4, dtype=torch.float64, device=f.device)
+    lib.ffdp_mi_finalize(V._ptr(raw), b, -1.0, V._ptr(table), V._stream())
+    g = torch.empty_like(m)
+    lib.ffdp_mi_bwd(V._ptr(f), V._ptr(m), f.numel(), C.byref(kernel.c), V._ptr(table), None, V._ptr(g), V._stream())
+    return DistLoss(-float(table[2 * b * b + 2 * b + 1].item()), g, b * b + 2 * b)
+
+
+def dist_lncc(spec: ShardSpec, f_shard: torch.Tensor, moved_shard: torch.Tensor, window: int = 7, eps: float = 1e-5,
+              ants_approx: bool = True, gp_sync: bool = True, n_total: Optional[int] = None) -> DistLoss:
+    """dist_lncc (distops.hpp:285-352): the five window moments over the slab with the
+    neighbours' halo planes (r = window // 2; 2r for the exact backward, whose gamma family
+    is box-filtered again), sum_n allreduced, loss = 1 - sum_n / N_total, dL/dn_i = -1/N."""
+    from . import voxreg as V
+    from ._lib import Slab, lib
+    f, m = V._vol(f_shard, "dist_lncc"), V._vol(moved_shard, "dist_lncc")
+    if tuple(f.shape) != tuple(m.shape):
+        raise InvalidArgument("dist_lncc: shard lattices differ")
+    if window < 1 or window % 2 == 0:
+        raise InvalidArgument("lncc: window must be odd and >= 1")
+    n_total = n_total or spec.global_shape[0] * f.shape[1] * f.shape[2]
+    r = window // 2
+    sync = gp_sync and spec.world > 1
+    nz_g = spec.global_shape[0] if sync else f.shape[0]
+    g_lo = spec.lo if sync else 0
+    pad = (r if ants_approx else 2 * r) if sync else 0
+    fh, lo, hi = halo_exchange(f, spec, pad) if sync else (f, 0, 0)
+    mh, _, _ = halo_exchange(m, spec, pad) if sync else (m, 0, 0)
+    dims = V._dims(fh.shape)
+    nint = f.numel()
+    plane = f.shape[1] * f.shape[2]
+    s = torch.zeros(1, dtype=torch.float64, device=f.device)
+    state = torch.empty((5,) + tuple(f.shape), dtype=torch.float64, device=f.device)
+    interior = Slab(g_lo - lo, fh.shape[0], g_lo, g_lo + f.shape[0], nz_g)
+    lib.ffdp_lncc_fwd(V._ptr(fh), V._ptr(mh), dims, interior, window, eps, V._ptr(state), None, V._ptr(s),
+                      V._stream())
+    s = allreduce_sum(s)
+    loss = 1.0 - float(s.item()) / n_total
+    g = torch.empty_like(m)
+    gi = -1.0 / n_total
+    if ants_approx:
+        lib.ffdp_lncc_gamma(V._ptr(state), nint, eps, gi, V._stream())
+        lib.ffdp_lncc_combine(V._ptr(state), V._dims(f.shape), V._full_slab(f.shape[0]), window, 1,
+                              V._ptr(f), V._ptr(m), None, V._ptr(g), V._stream())
+        return DistLoss(loss, g)
+    # exact: the gamma family on the slab +- r planes (inside the lattice; the 2r halo holds
+    # their windows), box-filtered again (lncc.hpp:376-406). One exchange of 2r planes where
+    # the reference exchanges r planes twice (neighbours must be >= 2r planes thick).
+    e0 = max(0, g_lo - r)
+    e1 = min(nz_g, g_lo + f.shape[0] + r)
+    ext = Slab(g_lo - lo, fh.shape[0], e0, e1, nz_g)
+    next_ = (e1 - e0) * plane
+    st_ext = torch.empty((5, e1 - e0) + tuple(f.shape[1:]), dtype=torch.float64, device=f.device)
+    lib.ffdp_lncc_fwd(V._ptr(fh), V._ptr(mh), dims, ext, window, eps, V._ptr(st_ext), None, None, V._stream())
+    lib.ffdp_lncc_gamma(V._ptr(st_ext), next_, eps, gi, V._stream())
+    gslab = Slab(e0, e1 - e0, g_lo, g_lo + f.shape[0], nz_g)
+    lib.ffdp_lncc_combine(V._ptr(st_ext), V._dims((e1 - e0,) + tuple(f.shape[1:])), gslab, window, 0, V._ptr(f),
+                          V._ptr(m), None, V._ptr(g), V._stream())
+    return DistLoss(loss, g)

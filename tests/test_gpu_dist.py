@@ -152,3 +152,89 @@ def test_sharded_deformable_stage_matches_oracle(orc, loss):
     assert np.max(np.abs(tr - tr_ref) / np.abs(tr_ref)) <= 1e-5
     assert l2rel(w, w_ref) <= 1e-3
     assert np.max(np.abs(w - w_ref)) <= 0.25 * V.deformable_lr_norm(si.f.shape, 0.5)
+
+
+OPS_SHAPE = (19, 22, 37)
+
+
+def _ops_inputs():
+    rng = np.random.default_rng(31)
+    f = rng.uniform(0, 1, OPS_SHAPE).astype(np.float32)
+    m = np.clip(0.7 * f + 0.3 * rng.uniform(0, 1, OPS_SHAPE), 0, 1).astype(np.float32)
+    u = rng.uniform(-0.03, 0.03, OPS_SHAPE + (3,)).astype(np.float32)
+    A = np.eye(3) + rng.uniform(-0.03, 0.03, (3, 3))
+    t = rng.uniform(-0.03, 0.03, 3)
+    up = rng.uniform(-1, 1, OPS_SHAPE).astype(np.float32)
+    return f, m, u, A, t, up
+
+
+def w_ops(rank, world):
+    """The standalone sharded operators (distops.hpp:54-396) on real ranks."""
+    import torch
+
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200 import voxreg as V
+    f, m, u, A, t, up = _ops_inputs()
+    spec = D.make_shard_spec(OPS_SHAPE, world, rank)
+    sl = slice(spec.lo, spec.hi)
+    dev = torch.device("cuda", 0)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a[sl])).to(dev)
+    fs, ms, us, ups = T(f), T(m), T(u), T(up)
+    out = {}
+    moved = D.ring_sample(ms, us, A, t, OPS_SHAPE, spec)
+    out["moved"] = moved.cpu().numpy()
+    g = D.ring_sample_backward(ups, ms, us, A, t, OPS_SHAPE, spec,
+                               V.SamplerGradWant(image=True, warp=True, affine=True, translation=True))
+    out["g_img"], out["g_u"], out["gA"], out["gt"] = g.image.cpu().numpy(), g.warp.cpu().numpy(), g.affine, g.translation
+    n = int(np.prod(OPS_SHAPE))
+    for name, r in (("mse", D.dist_mse(fs, moved, n)),
+                    ("mi", D.dist_mi(fs, moved, 32, V.ParzenKernel.bspline3(32), False, n)),
+                    ("lncc_ants", D.dist_lncc(spec, fs, moved, 7, 1e-5, True, True, n)),
+                    ("lncc_exact", D.dist_lncc(spec, fs, moved, 7, 1e-5, False, True, n))):
+        out[name] = (r.loss, r.grad_moved.cpu().numpy())
+    out["gp"] = D.gp_convolve(us, V.gaussian_taps(1.0), spec, "renormalize").cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_standalone_sharded_operators_match_single_gpu(world):
+    """ring_sample / ring_sample_backward / dist_mse / dist_mi / dist_lncc (ANTs and exact)
+    / gp_convolve over `world` ranks against the same operators on the whole volume on one
+    GPU (the reference's invariance property, test_distops.cpp:139-423)."""
+    need_gpu()
+    import torch
+
+    from gpu_util import maxrel
+    from paper_2509_25044_b200 import voxreg as V
+    f, m, u, A, t, up = _ops_inputs()
+    dev = torch.device("cuda", 0)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    args = V.SamplerArgs(A=A, t=t)
+    moved = V.fused_sample(T(m), T(u), args)
+    g = V.fused_sample_backward(T(up), T(m), T(u), args,
+                                V.SamplerGradWant(image=True, warp=True, affine=True, translation=True))
+    out = spawn(w_ops, world)
+    cat = lambda k: np.concatenate([out[r][k] for r in range(world)], axis=0)
+    assert maxrel(cat("moved"), moved.cpu().numpy()) <= 1e-6
+    assert maxrel(cat("g_u"), g.warp.cpu().numpy()) <= 1e-6
+    assert maxrel(cat("g_img"), g.image.cpu().numpy()) <= 1e-5
+    assert np.max(np.abs(out[0]["gA"] - g.affine)) <= 1e-6 * max(1.0, np.max(np.abs(g.affine)))
+    assert np.max(np.abs(out[0]["gt"] - g.translation)) <= 1e-6 * max(1.0, np.max(np.abs(g.translation)))
+    n = int(np.prod(f.shape))
+    fm, mm = T(f), moved
+    # single-GPU references of the losses on the whole moved volume
+    sm = ((mm.double() - fm.double()) ** 2).sum().item() / n
+    refs = {"mse": (sm, (2.0 * (mm - fm) / n).cpu().numpy())}
+    k = V.ParzenKernel.bspline3(32)
+    res = V.mi_forward_exact(fm, mm, 32, k)
+    refs["mi"] = (-res.mi, V.mi_backward(-1.0, fm, mm, res.hist, k)[1].cpu().numpy())
+    for ants in (True, False):
+        lr, st = V.lncc_forward_fused(fm, mm, 7, 1e-5)
+        refs["lncc_ants" if ants else "lncc_exact"] = (lr.loss, V.lncc_backward_fused(1.0, st, fm, mm, ants)[1].cpu()
+                                                       .numpy())
+    for name, (lv, gv) in refs.items():
+        losses = [out[r][name][0] for r in range(world)]
+        assert all(v == losses[0] for v in losses), name
+        assert losses[0] == pytest.approx(lv, rel=1e-6), name
+        assert maxrel(np.concatenate([out[r][name][1] for r in range(world)], axis=0), gv) <= 1e-5, name
+    assert np.array_equal(cat("gp"), V.gp_convolve(T(u), V.gaussian_taps(1.0), "renormalize").cpu().numpy())
