@@ -214,10 +214,15 @@ class Stepper:
                          else self._p(self.ws.lncc_workspace(self.dims, self.slab)))
         else:
             self.kernel = voxreg.ParzenKernel.bspline3(bins)
+            # the pass-1 records (16 B/voxel) when they fit next to the step's buffers; else
+            # pass 2 samples the warp again (ffdp_step_mi without records)
+            free, _ = torch.cuda.mem_get_info()
+            self.use_rec = free > 16 * self.n + (4 << 30)
         self.kernel_ms = {}
         # lncc: sample, moments, partial-sum reduction (fused: 1); mi: pass 1 (finalize fused
         # into its last CTA) and pass 2 (memsets of the histogram are not kernels of ours)
-        self.launches_per_step = (1 if self._lws is None else 3) if loss == "lncc" else 2
+        self.launches_per_step = ((1 if self._lws is None else 3) if loss == "lncc" else
+                                  2 if self.use_rec else 4)
 
     def _p(self, t):
         return self.C.c_void_p(t.data_ptr())
@@ -247,7 +252,19 @@ class Stepper:
             lib.ffdp_step_lncc_passes(*a, self._lws, 2, s)
             ev[2].record()
             return [("k_lncc_sample", ev[0], ev[1]), ("k_lncc_moments", ev[1], ev[2])]
-        rec = self.ws.records(self.dims, self.slab)
+        rec = self.ws.records(self.dims, self.slab) if self.use_rec else None
+        if rec is None and record:
+            self.ws.raw.zero_()
+            ev[0].record()
+            lib.ffdp_step_mi_hist(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
+                                  C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.scratch), None, s)
+            lib.ffdp_mi_finalize(self._p(self.ws.raw), self.bins, -1.0, self._p(self.ws.table), s)
+            ev[1].record()
+            lib.ffdp_step_mi_grad(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win,
+                                  C.byref(self.args), C.byref(self.kernel.c), self._p(self.ws.table),
+                                  self._p(self.g_u), None, s)
+            ev[2].record()
+            return [("k_mi_hist_bs+finalize", ev[0], ev[1]), ("k_step_mi_grad", ev[1], ev[2])]
         if not record:
             lib.ffdp_step_mi(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
                              C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.table), self._p(self.g_u),
@@ -562,6 +579,10 @@ def run_registration(shape, schedule_spec):
 
 def run_e2e(args, st, f, m, u, A, t, loss, world):
     import torch
+    if 4 * (f.numel() + m.numel() + u.numel()) > (8 << 30):
+        # pinned host copies of the inputs would exceed the host budget of a shared box
+        return {"value": None, "unit": "Gvoxel/s", "skipped": "inputs exceed the 8 GiB pinned-host budget",
+                "h2d_bytes_per_step": 4 * (f.numel() + m.numel() + u.numel()), "d2h_bytes_per_step": 8}
     steps = max(3, min(args.steps, 20))
     hf, hm, hu = (x.cpu().pin_memory() for x in (f, m, u))
     torch.cuda.synchronize()
