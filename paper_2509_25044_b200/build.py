@@ -63,7 +63,8 @@ def build_cpp_tests(force: bool = False, verbose: bool = False) -> str:
     """The C++ parity suite of the host mirror (include/ffdp/voxreg.hpp), linked against
     libffdp.so and the oracle (test infrastructure) with $ORIGIN-relative rpaths."""
     cuda = os.path.dirname(os.path.dirname(nvcc()))
-    deps = [CPP_TEST_SRC, os.path.join(ROOT, "include", "ffdp", "voxreg.hpp"), os.path.join(ROOT, "include", "ffdp.h"),
+    deps = [CPP_TEST_SRC, os.path.join(ROOT, "include", "ffdp", "voxreg.hpp"),
+            os.path.join(ROOT, "include", "ffdp", "nifti.hpp"), os.path.join(ROOT, "include", "ffdp.h"),
             LIB, os.path.join(ROOT, "oracle", "libffdp_oracle.so")]
     if force or _stale(CPP_TEST_BIN, deps):
         cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"),

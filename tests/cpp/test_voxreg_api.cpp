@@ -8,11 +8,15 @@
 // Built by paper_2509_25044_b200/build.py (tests/cpp/test_voxreg_api), run by
 // tests/test_cpp_api.py on a GPU. Exit code 0 = all checks passed.
 #include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iterator>
 #include <cstdlib>
 #include <functional>
 #include <string>
 #include <vector>
 
+#include "ffdp/nifti.hpp"
 #include "ffdp/voxreg.hpp"
 
 // ---------------------------------------------------------------- oracle (C, fp64)
@@ -536,6 +540,60 @@ static void driver_tests() {
     });
 }
 
+// ---------------------------------------------------------------- NIfTI / warp IO
+static std::string gold_dir() {
+    const char* e = std::getenv("FFDP_GOLDEN_NIFTI");
+    return e ? e : "tests/golden/nifti";
+}
+
+static std::vector<unsigned char> slurp(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    return std::vector<unsigned char>((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+}
+
+static void io_tests() {
+    run("io: reference-written NIfTI read back; write_nifti byte-identical (nifti.hpp:99-239)", [] {
+        const std::string d = gold_dir();
+        const auto a = V::read_nifti(d + "/vol_f32.nii");
+        const auto be = V::read_nifti(d + "/vol_be.nii");
+        EXPECT_TRUE(!a.header.big_endian && be.header.big_endian);
+        EXPECT_TRUE(a.dims == be.dims && a.data == be.data);
+        EXPECT_TRUE(a.dims == (V::Dims3{7, 5, 3}) && std::fabs(a.spacing[2] - 2.5) < 1e-6);
+        const auto lab = V::read_nifti(d + "/labels.nii"), sc = V::read_nifti(d + "/scaled_i16.nii");
+        bool scaled = lab.data.size() == sc.data.size();
+        for (size_t i = 0; scaled && i < lab.data.size(); ++i) scaled = sc.data[i] == 0.5 * lab.data[i] - 3.0;
+        EXPECT_TRUE(scaled);
+        // device round trip: write the fp32 volume back, byte for byte the reference's file
+        auto v = a.to_device();
+        V::write_nifti(v, "/tmp/ffdp_io_test.nii");
+        EXPECT_TRUE(slurp("/tmp/ffdp_io_test.nii") == slurp(d + "/vol_f32.nii"));
+        std::vector<unsigned char> bad = slurp(d + "/vol_f32.nii");
+        bad[344] = 'x';
+        EXPECT_THROW(V::read_nifti_bytes(bad), V::FormatError);
+        EXPECT_THROW(V::read_nifti("/nonexistent/x.nii"), V::IoError);
+    });
+    run("io: raw + JSON warp (nifti.hpp:268-303) round trip", [] {
+        const std::string d = gold_dir();
+        auto w = V::read_warp(d + "/warp");
+        EXPECT_TRUE(w.dims == (V::Dims3{5, 4, 3}));
+        V::Vec3 sp{{0.7, 1.1, 2.5}}, og{{-10.0, 4.5, 0.25}};
+        V::write_warp(w, "/tmp/ffdp_io_warp", sp, og);
+        // the device field is fp32: the written payload is the reference's fp64 values
+        // rounded to float, and nothing else
+        const auto mine = slurp("/tmp/ffdp_io_warp.raw"), ref = slurp(d + "/warp.raw");
+        bool same = mine.size() == ref.size();
+        for (size_t i = 0; same && i + 8 <= ref.size(); i += 8) {
+            double a, b;
+            std::memcpy(&a, mine.data() + i, 8);
+            std::memcpy(&b, ref.data() + i, 8);
+            same = a == double(float(b));
+        }
+        EXPECT_TRUE(same);
+        auto w2 = V::read_warp("/tmp/ffdp_io_warp");
+        EXPECT_TRUE(w2.to_host() == w.to_host());
+    });
+}
+
 int main() {
     if (ffdp_device_check() != FFDP_OK) {
         std::printf("no usable sm_100 device: %s\n", ffdp_last_error());
@@ -546,6 +604,7 @@ int main() {
     mi_tests();
     step_tests();
     driver_tests();
+    io_tests();
     std::printf("%d checks, %d failed\n", g_checks, g_failed);
     return g_failed ? 1 : 0;
 }

@@ -56,6 +56,63 @@ def margin_fixture(orc, seed, img_shape, out_shape, perturb):
     return img, u, A, t, S
 
 
+def nifti_fixtures(orc):
+    """Files in tests/golden/nifti/ written by the reference's write_nifti / write_warp, two
+    hand-made variants (big-endian, int16 with scl_slope), and the reference's parse of
+    each (read_nifti / read_warp)."""
+    import ctypes as C
+    import struct
+    so = os.path.join(ROOT, "oracle", "_ref", "libvoxreg_io.so")
+    if not os.path.exists(so):
+        raise SystemExit("make -C oracle ref-io first")
+    L = C.CDLL(so)
+    dp, i64p = C.POINTER(C.c_double), C.POINTER(C.c_int64)
+    P = lambda a: a.ctypes.data_as(dp)
+    d3 = lambda shape: (C.c_int64 * 3)(shape[2], shape[1], shape[0])
+    nd = os.path.join(OUT, "nifti")
+    os.makedirs(nd, exist_ok=True)
+    g = {}
+    v = orc.random_volume(orc.rng(951), (3, 5, 7), -2.0, 3.0)
+    sp, og = np.array([0.7, 1.1, 2.5]), np.array([-10.0, 4.5, 0.25])
+    for f64 in (0, 1):
+        fn = os.path.join(nd, f"vol_f{64 if f64 else 32}.nii")
+        assert L.refio_write_nifti(P(v), d3(v.shape), P(sp), P(og), f64, fn.encode()) == 0
+    lab = (orc.random_volume(orc.rng(952), (4, 3, 6), 0, 300)).astype(np.uint16)
+    assert L.refio_write_labels(lab.ctypes.data_as(C.POINTER(C.c_uint16)), d3(lab.shape), P(sp),
+                                os.path.join(nd, "labels.nii").encode()) == 0
+    # big-endian copy of the fp32 file: every header field and voxel byte-swapped
+    b = bytearray(open(os.path.join(nd, "vol_f32.nii"), "rb").read())
+    be = bytearray(b)
+    struct.pack_into(">i", be, 0, 348)
+    struct.pack_into(">8h", be, 40, *struct.unpack_from("<8h", b, 40))
+    struct.pack_into(">2h", be, 70, *struct.unpack_from("<2h", b, 70))
+    struct.pack_into(">8f", be, 76, *struct.unpack_from("<8f", b, 76))
+    struct.pack_into(">3f", be, 108, *struct.unpack_from("<3f", b, 108))
+    struct.pack_into(">3f", be, 268, *struct.unpack_from("<3f", b, 268))
+    n = v.size
+    be[352:] = np.frombuffer(bytes(b[352:352 + 4 * n]), dtype="<f4").astype(">f4").tobytes()
+    open(os.path.join(nd, "vol_be.nii"), "wb").write(bytes(be))
+    # int16 payload with scl_slope / scl_inter (a scanner-style file)
+    sc = bytearray(open(os.path.join(nd, "labels.nii"), "rb").read())
+    struct.pack_into("<2f", sc, 112, 0.5, -3.0)
+    open(os.path.join(nd, "scaled_i16.nii"), "wb").write(bytes(sc))
+    for name in ("vol_f32", "vol_f64", "labels", "vol_be", "scaled_i16"):
+        fn = os.path.join(nd, name + ".nii").encode()
+        dims, spo, ogo = (C.c_int64 * 3)(), np.zeros(3), np.zeros(3)
+        assert L.refio_read_nifti(fn, dims, P(spo), P(ogo), None) == 0
+        out = np.zeros((dims[2], dims[1], dims[0]))
+        assert L.refio_read_nifti(fn, dims, P(spo), P(ogo), P(out)) == 0
+        g.update({f"nii_{name}": out, f"nii_{name}_spacing": spo, f"nii_{name}_origin": ogo})
+    g.update({"nii_src": v, "nii_src_spacing": sp, "nii_src_origin": og, "nii_labels_src": lab.astype(np.int64)})
+    w = orc.random_volume(orc.rng(953), (3, 4, 5, 3), -0.1, 0.1)
+    assert L.refio_write_warp(P(w), d3(w.shape[:3]), P(sp), P(og), os.path.join(nd, "warp").encode()) == 0
+    dims = (C.c_int64 * 3)()
+    wo = np.zeros_like(w)
+    assert L.refio_read_warp(os.path.join(nd, "warp").encode(), dims, P(wo)) == 0
+    g.update({"warp_src": w, "warp_read": wo})
+    return g
+
+
 def main():
     orc, ref = Oracle(), Reference()
     g = {}
@@ -176,6 +233,9 @@ def main():
             g.update({f"def_{loss}_{kind}_H{world}_warp": w, f"def_{loss}_{kind}_H{world}_trace": tr})
     jw = orc.random_volume(orc.rng(901), (8, 9, 10, 3), -0.4, 0.4)
     g.update({"jac_w": jw, "jac_frac": np.array(ref.jacobian_positive(jw))})
+
+    # --- NIfTI-1 / raw + JSON IO (nifti.hpp), written and parsed by the reference itself
+    g.update(nifti_fixtures(orc))
 
     path = os.path.join(OUT, "voxreg_golden.npz")
     np.savez_compressed(path, **g)

@@ -19,7 +19,8 @@ def test_cpp_mirror_compiles_against_the_abi():
 @pytest.mark.gpu
 def test_cpp_mirror_parity_suite():
     b = build.build_cpp_tests()
-    r = subprocess.run([b], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, FFDP_GOLDEN_NIFTI=os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "nifti"))
+    r = subprocess.run([b], capture_output=True, text=True, timeout=600, env=env)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
