@@ -1,0 +1,130 @@
+"""Size-independent properties at BASELINE.json's full sizes, where the CPU oracle cannot
+run: the MI step at 256^3 (configs[1]) and the LNCC step and warp update at 720x640x720
+(configs[2]) on the bench's synthetic pair. Determinism (fixed-order / integer
+reductions: bit-identical repeats), shard invariance (two emulated z slabs with halos and
+the allreduced payload vs the whole volume), and the records / re-sampling MI passes
+agreeing bit for bit."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from gpu_util import host, maxrel, need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def V():
+    need_gpu()
+    from paper_2509_25044_b200 import voxreg
+    return voxreg
+
+
+def _inputs(shape, loss):
+    import bench
+    return bench.synth_inputs(shape, loss, 1234, "cuda")
+
+
+def _window(V, m, z0, z1):
+    """A zero-bordered moving window of planes [z0, z1) (ffdp_pad_window)."""
+    import torch
+    from paper_2509_25044_b200._lib import Dims, ImageWindow, lib
+    nz, ny, nx = m.shape
+    mp = torch.empty((z1 - z0 + 4, ny + 4, nx + 4), device="cuda")
+    lib.ffdp_pad_window(V._ptr(m), Dims(nx, ny, nz), z0, z1, V._ptr(mp), V._stream())
+    return mp, ImageWindow(mp.data_ptr(), Dims(nx, ny, nz), z0, z1, 2)
+
+
+def test_mi256_deterministic_sharded_and_record_free(V):
+    import torch
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200._lib import Slab, lib
+    f, m, u, A, t = _inputs((256, 256, 256), "mi")
+    p = V.LossParams(kind="mi", bins=32, mi_bspline_kernel=True)
+    a = V.warp_loss_step(f, m, u, A, t, p)
+    g_a = a.g_u.clone()
+    b = V.warp_loss_step(f, m, u, A, t, p)
+    assert a.loss == b.loss and torch.equal(g_a, b.g_u)  # integer histogram: bit-reproducible
+    # two z slabs: per-slab histograms, summed (the allreduce), finalize, per-slab pass 2
+    nz, bins = f.shape[0], 32
+    args = V.SamplerArgs(A=A, t=t).to_c()
+    k = V.ParzenKernel.bspline3(bins)
+    raw = torch.zeros(bins * bins + 2 * bins, dtype=torch.float64, device="cuda")
+    mp, win = _window(V, m, 0, nz)
+    ctx = []
+    for lo, hi in D.shard_ranges(nz, 2):
+        fb, ub = f[lo:hi].contiguous(), u[lo:hi].contiguous()
+        slab = Slab(lo, hi - lo, lo, hi, nz)
+        part = torch.zeros_like(raw)
+        lib.ffdp_step_mi_hist(V._ptr(fb), V._ptr(ub), V._dims(fb.shape), slab, win, C.byref(args), C.byref(k.c),
+                              V._ptr(part), None, None, V._stream())
+        raw += part
+        ctx.append((fb, ub, slab))
+    table = torch.empty(2 * bins * bins + 2 * bins + 4, dtype=torch.float64, device="cuda")
+    lib.ffdp_mi_finalize(V._ptr(raw), bins, -1.0, V._ptr(table), V._stream())
+    parts = []
+    for fb, ub, slab in ctx:
+        g = torch.empty(tuple(ub.shape), device="cuda")
+        lib.ffdp_step_mi_grad(V._ptr(fb), V._ptr(ub), V._dims(fb.shape), slab, win, C.byref(args), C.byref(k.c),
+                              V._ptr(table), V._ptr(g), None, V._stream())
+        parts.append(g)
+    loss = -float(table[2 * bins * bins + 2 * bins + 1].item())
+    assert loss == pytest.approx(a.loss, rel=1e-12)
+    assert maxrel(host(torch.cat(parts, 0)), host(g_a)) <= 1e-6
+    # the record-free step (pass 2 samples the warp again) equals the records path
+    ws = V.StepWorkspace(f.device, bins)
+    g2 = torch.empty_like(u)
+    mi = V.MovingImage(m)
+    lib.ffdp_step_mi(V._ptr(f), V._ptr(u), V._dims(f.shape), V._full_slab(nz), mi.window(), C.byref(args),
+                     C.byref(k.c), V._ptr(ws.raw), V._ptr(ws.table), V._ptr(g2), V._ptr(ws.scratch), None, None,
+                     V._stream())
+    assert -float(ws.table[2 * bins * bins + 2 * bins + 1].item()) == a.loss
+    assert torch.equal(g2, g_a)
+
+
+def test_lncc720_deterministic_and_sharded(V):
+    import torch
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200._lib import Slab, lib
+    f, m, u, A, t = _inputs((720, 640, 720), "lncc")
+    shifts = (V.intensity_shift(f), V.intensity_shift(m))
+    p = V.LossParams(kind="lncc")
+    a = V.warp_loss_step(f, m, u, A, t, p, shifts=shifts)
+    g_a = a.g_u.clone()
+    b = V.warp_loss_step(f, m, u, A, t, p, shifts=shifts)
+    assert a.loss == b.loss and torch.equal(g_a, b.g_u)  # fixed-order reductions
+    del b
+    nz = f.shape[0]
+    args = V.SamplerArgs(A=A, t=t).to_c()
+    mp, win = _window(V, m, 0, nz)
+    total, parts = 0.0, []
+    for lo, hi in D.shard_ranges(nz, 2):
+        b0, b1 = max(0, lo - 3), min(nz, hi + 3)
+        fb, ub = f[b0:b1].contiguous(), u[b0:b1].contiguous()
+        slab = Slab(b0, b1 - b0, lo, hi, nz)
+        g = torch.empty((hi - lo,) + tuple(u.shape[1:]), device="cuda")
+        sn = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ws = torch.empty(int(lib.ffdp_step_lncc_workspace_bytes(V._dims(fb.shape), slab)) // 4, device="cuda")
+        lib.ffdp_step_lncc(V._ptr(fb), V._ptr(ub), V._dims(fb.shape), slab, win, C.byref(args), 7, 1e-5,
+                           -1.0 / f.numel(), shifts[0], shifts[1], V._ptr(g), V._ptr(sn), None, V._ptr(ws),
+                           V._stream())
+        total += float(sn.item())
+        parts.append(host(g))
+        del fb, ub, ws
+    loss = 1.0 - total / f.numel()
+    assert loss == pytest.approx(a.loss, rel=1e-7)
+    assert maxrel(np.concatenate(parts, 0), host(g_a)) <= 2e-5
+
+
+def test_warp_update_720_sharded_bit_identical(V):
+    import torch
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200._lib import Slab
+    g = torch.empty((720, 640, 720, 3), device="cuda").uniform_(-1e-6, 1e-6)
+    taps = V.gaussian_taps(1.0)
+    full = V.gp_convolve(g, taps, "renormalize")
+    for lo, hi in D.shard_ranges(720, 3):
+        b0, b1 = max(0, lo - 3), min(720, hi + 3)
+        part = V.gp_convolve(g[b0:b1].contiguous(), taps, "renormalize", slab=Slab(b0, b1 - b0, lo, hi, 720))
+        assert torch.equal(part, full[lo:hi])
