@@ -41,15 +41,15 @@ struct SParams {
     int32_t nx, ny, nxb, nyq;
     FastDiv div_nxb, div_nyq;
     int64_t plane, buf_z0, p0, z_begin, z_end, nunits;
+    int64_t gd_skip;  // (z_begin - buf_z0) * plane: the halo planes G does not hold
     float sm;
 };
 
 // The unit of a warp: 32 consecutive x voxels (lane = x offset) of 4 consecutive rows of
 // one plane; consecutive lanes gather neighbouring source positions (coalesced).
 struct SUnit {
-    int32_t x, y0;
+    int32_t x, y0, nrow;  // nrow: rows of the unit inside the lattice (0 for lanes past nx)
     int64_t p, bi;
-    bool vx;
 };
 
 __device__ __forceinline__ SUnit sunit(const SParams& P, int64_t unit, int lane) {
@@ -59,19 +59,22 @@ __device__ __forceinline__ SUnit sunit(const SParams& P, int64_t unit, int lane)
     const uint32_t zz = fdiv(r1, P.div_nyq);
     w.y0 = (int32_t)(r1 - zz * P.nyq) * 4;
     w.p = P.p0 + zz;
-    w.vx = w.x < P.nx;
-    w.bi = (w.p - P.buf_z0) * P.plane + (int64_t)w.y0 * P.nx + (w.vx ? w.x : 0);
+    const bool vx = w.x < P.nx;
+    w.nrow = vx ? min(4, P.ny - w.y0) : 0;
+    w.bi = (w.p - P.buf_z0) * P.plane + (int64_t)w.y0 * P.nx + (vx ? w.x : 0);
     return w;
 }
 
+// row k of the unit is 3 * nx floats of u after row k - 1: one 64-bit base per unit
 __device__ __forceinline__ void sload(const SParams& P, const SUnit& w, float (&uu)[12]) {
+    const float* q = P.u + 3 * w.bi;
+    const int32_t rs = 3 * P.nx;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const bool ok = w.vx && w.y0 + k < P.ny;
-        const int64_t i = w.bi + (int64_t)k * P.nx;
-        uu[3 * k] = ok ? __ldg(P.u + 3 * i) : 0.0f;
-        uu[3 * k + 1] = ok ? __ldg(P.u + 3 * i + 1) : 0.0f;
-        uu[3 * k + 2] = ok ? __ldg(P.u + 3 * i + 2) : 0.0f;
+        const bool ok = k < w.nrow;
+        uu[3 * k] = ok ? __ldg(q + k * rs) : 0.0f;
+        uu[3 * k + 1] = ok ? __ldg(q + k * rs + 1) : 0.0f;
+        uu[3 * k + 2] = ok ? __ldg(q + k * rs + 2) : 0.0f;
     }
 }
 
@@ -81,7 +84,7 @@ __device__ __forceinline__ void sload(const SParams& P, const SUnit& w, float (&
 #ifndef FFDP_L2_SPREF
 #define FFDP_L2_SPREF 1
 #endif
-template <bool FULLWIN>
+template <bool FULLWIN, bool OFF32>
 __global__ void __launch_bounds__(256, FFDP_L2_SMINB) k_lncc_sample(const SParams P) {
     int miss = 0;
     const int lane = threadIdx.x & 31;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(256, FFDP_L2_SMINB) k_lncc_sample(const SParam
         }
         Corners cr[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN>(P.g, c[k], miss);
+        for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN, OFF32>(P.g, c[k], miss);
         const SUnit cw = w;
         if (FFDP_L2_SPREF) {
             // the next unit's displacements are in flight while this unit's corners land
@@ -112,15 +115,17 @@ __global__ void __launch_bounds__(256, FFDP_L2_SMINB) k_lncc_sample(const SParam
             }
         }
         const bool interior = cw.p >= P.z_begin && cw.p < P.z_end;
+        float* mwp = P.mw + cw.bi;
+        float* gdp = P.gd + 3 * (cw.bi - P.gd_skip);
+        const int32_t rs = 3 * P.nx;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             float d[3];
             const float v = interp_grad(cr[k], c[k], d);
-            if (cw.vx && cw.y0 + k < P.ny) {
-                const int64_t i = cw.bi + (int64_t)k * P.nx;
-                P.mw[i] = v - P.sm;
+            if (k < cw.nrow) {
+                mwp[k * P.nx] = v - P.sm;
                 if (interior) {
-                    float* o = P.gd + 3 * (i - (P.z_begin - P.buf_z0) * P.plane);
+                    float* o = gdp + k * rs;
                     o[0] = P.g.dscale[0] * d[0];
                     o[1] = P.g.dscale[1] * d[1];
                     o[2] = P.g.dscale[2] * d[2];
@@ -450,16 +455,24 @@ int lncc2_step(const float* f, const float* u, const ffdp_dims& d, const ffdp_sl
     S.z_begin = s.z_begin;
     S.z_end = s.z_end;
     S.nunits = (int64_t)S.nxb * S.nyq * (s_hi - s_lo);
+    S.gd_skip = (s.z_begin - s.buf_z0) * plane;
     S.sm = shift_m;
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
 #ifndef FFDP_L2_SCTAS
 #define FFDP_L2_SCTAS 3  // one wave (3 CTAs per SM): measured 2.64 -> 2.51 ms vs 16
 #endif
     const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((S.nunits + 7) / 8, (int64_t)FFDP_L2_SCTAS * num_sms()));
-    if ((passes & 1) && full)
-        k_lncc_sample<true><<<g1, 256, 0, st>>>(S);
-    else if (passes & 1)
-        k_lncc_sample<false><<<g1, 256, 0, st>>>(S);
+    if (passes & 1) {
+        const bool o32 = window_off32(S.g);
+        if (full && o32)
+            k_lncc_sample<true, true><<<g1, 256, 0, st>>>(S);
+        else if (full)
+            k_lncc_sample<true, false><<<g1, 256, 0, st>>>(S);
+        else if (o32)
+            k_lncc_sample<false, true><<<g1, 256, 0, st>>>(S);
+        else
+            k_lncc_sample<false, false><<<g1, 256, 0, st>>>(S);
+    }
     if (!(passes & 2)) return check_launch("step_lncc (warp sampling pass)");
 
     MParams M;
