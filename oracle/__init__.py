@@ -413,6 +413,9 @@ class Reference:
         L.ref_affine_stage.argtypes = [_dp, _dp, _i64p, C.c_int, _dp, C.POINTER(C.c_int), C.c_double, C.c_int,
                                        C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
         L.ref_jacobian_positive.argtypes = [_dp, _i64p, _dp]
+        _u16p = C.POINTER(C.c_uint16)
+        L.ref_label_metrics.argtypes = [_u16p, _u16p, _i64p, _dp, _dp]
+        L.ref_warp_labels_nn.argtypes = [_u16p, _i64p, _dp, _i64p, _dp, _dp, _u16p]
         L.ref_warp_update.argtypes = [_dp, _dp, _dp, _dp, _i64p, C.c_double, C.c_double, C.c_double, C.c_int64,
                                       C.c_int]
         L.ref_step.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _i64p, _dp, _dp, C.c_int, C.c_double, C.c_int,
@@ -544,6 +547,27 @@ class Reference:
         out = C.c_double()
         self._check(self.lib.ref_jacobian_positive(_p(u), _arr_dims(u.shape[:3]), C.byref(out)))
         return out.value
+
+    def label_metrics(self, a, b, spacing=(1.0, 1.0, 1.0)):
+        """(dice mean, inv_dice, hd90_cumulative) of two uint16 label maps (nz, ny, nx)."""
+        a, b = (np.ascontiguousarray(x, dtype=np.uint16) for x in (a, b))
+        sp = np.asarray(spacing, dtype=np.float64)
+        out = np.zeros(3)
+        u16 = C.POINTER(C.c_uint16)
+        self._check(self.lib.ref_label_metrics(a.ctypes.data_as(u16), b.ctypes.data_as(u16), _arr_dims(a.shape),
+                                               _p(sp), _p(out)))
+        return tuple(float(x) for x in out)
+
+    def warp_labels_nn(self, labels, u, A=None, t=None):
+        lab = np.ascontiguousarray(labels, dtype=np.uint16)
+        u = _f64(u)
+        A = _f64(np.eye(3) if A is None else A).reshape(9)
+        t = _f64(np.zeros(3) if t is None else t).reshape(3)
+        out = np.zeros(u.shape[:3], dtype=np.uint16)
+        u16 = C.POINTER(C.c_uint16)
+        self._check(self.lib.ref_warp_labels_nn(lab.ctypes.data_as(u16), _arr_dims(lab.shape), _p(u),
+                                                _arr_dims(u.shape[:3]), _p(A), _p(t), out.ctypes.data_as(u16)))
+        return out
 
     def warp_update(self, g_u, u, m1, m2, lr, step, sigma_grad=1.0, sigma_warp=0.5, world=1):
         """registration.hpp:313-317 over `world` ranks (gp_convolve halos): (u, m1, m2)."""

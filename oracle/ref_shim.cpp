@@ -398,4 +398,31 @@ int ref_step(int loss_kind, int fp32, const double* f, const double* m, const do
     });
 }
 
+// Label evaluation (metrics.hpp:44-201, sampler.hpp:331-365): out3 = dice mean,
+// inv_dice (fixed-volume weights), hd90_cumulative with `spacing` (x, y, z).
+int ref_label_metrics(const uint16_t* a, const uint16_t* b, const int64_t* dims, const double* spacing,
+                      double* out3) {
+    return guarded([&] {
+        auto la = LabelVolume::zeros(D(dims)), lb = LabelVolume::zeros(D(dims));
+        std::memcpy(la.data.data(), a, la.data.size() * sizeof(uint16_t));
+        std::memcpy(lb.data.data(), b, lb.data.size() * sizeof(uint16_t));
+        out3[0] = dice(la, lb).mean;
+        out3[1] = inv_dice(la, lb);
+        out3[2] = hd90_cumulative(la, lb, Vec3{spacing[0], spacing[1], spacing[2]});
+    });
+}
+
+int ref_warp_labels_nn(const uint16_t* labels, const int64_t* ldims, const double* u, const int64_t* udims,
+                       const double* A, const double* t, uint16_t* out) {
+    return guarded([&] {
+        auto l = LabelVolume::zeros(D(ldims));
+        std::memcpy(l.data.data(), labels, l.data.size() * sizeof(uint16_t));
+        SamplerArgs args;
+        for (int i = 0; i < 9; ++i) args.A.m[static_cast<std::size_t>(i)] = A[i];
+        args.t = Vec3{t[0], t[1], t[2]};
+        const auto w = warp_labels_nn(l, warp<double>(u, D(udims)), args);
+        std::memcpy(out, w.data.data(), w.data.size() * sizeof(uint16_t));
+    });
+}
+
 } // extern "C"

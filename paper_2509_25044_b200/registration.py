@@ -159,11 +159,20 @@ def deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine=None, sch
     opts = opts or DeformableOptions()
     if opts.shards < 1:
         raise InvalidArgument("deformable_stage: shards must be >= 1")
-    if opts.shards > 1:
-        raise InvalidArgument("deformable_stage: shards > 1 runs one process per GPU (dist.sharded_deformable_stage)")
     fixed, moving = V._vol(fixed, "deformable_stage"), V._vol(moving, "deformable_stage")
     if tuple(fixed.shape) != tuple(moving.shape):
         raise InvalidArgument("deformable_stage: F and M must share a lattice (registration.hpp:268-270)")
+    if opts.shards > 1:
+        # one process per GPU: the shards are the torch.distributed ranks
+        from . import dist as D
+        _, world = D._world()
+        if world != opts.shards:
+            raise InvalidArgument(f"deformable_stage: shards = {opts.shards} needs {opts.shards} torch.distributed "
+                                  f"ranks (this job has {world})")
+        if not opts.gp_sync:
+            raise InvalidArgument("deformable_stage: the halo-free ablation (gp_sync = false) is not supported by "
+                                  "the sharded step")
+        return D.sharded_deformable_stage(fixed, moving, affine, schedule, trace, scale_index_base)
     A, t = (np.eye(3), np.zeros(3)) if affine is None else (np.asarray(affine[0]), np.asarray(affine[1]))
     warp = None
     for s, step in enumerate(schedule.steps):

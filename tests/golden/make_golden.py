@@ -56,6 +56,17 @@ def margin_fixture(orc, seed, img_shape, out_shape, perturb):
     return img, u, A, t, S
 
 
+def label_maps(c1, c2, shape=(14, 16, 18)):
+    """Two ellipsoids and a slab of labels 1-3 on a (nz, ny, nx) lattice."""
+    nz, ny, nx = shape
+    z, y, x = np.mgrid[:nz, :ny, :nx]
+    a = np.zeros(shape, np.uint16)
+    a[((x - c1[0]) ** 2 / 16 + (y - c1[1]) ** 2 / 9 + (z - c1[2]) ** 2 / 9) < 1] = 1
+    a[((x - c2[0]) ** 2 / 6 + (y - c2[1]) ** 2 / 4 + (z - c2[2]) ** 2 / 5) < 1] = 2
+    a[(x < 3) & (y > 10)] = 3
+    return a
+
+
 def nifti_fixtures(orc):
     """Files in tests/golden/nifti/ written by the reference's write_nifti / write_warp, two
     hand-made variants (big-endian, int16 with scl_slope), and the reference's parse of
@@ -233,6 +244,17 @@ def main():
             g.update({f"def_{loss}_{kind}_H{world}_warp": w, f"def_{loss}_{kind}_H{world}_trace": tr})
     jw = orc.random_volume(orc.rng(901), (8, 9, 10, 3), -0.4, 0.4)
     g.update({"jac_w": jw, "jac_frac": np.array(ref.jacobian_positive(jw))})
+
+    # --- label evaluation (metrics.hpp:44-201) and nearest-neighbour label warping
+    #     (sampler.hpp:331-365) on two overlapping ellipsoid maps
+    la, lb = label_maps((7, 7, 6), (12, 5, 4)), label_maps((9, 8, 7), (11, 6, 5))
+    lu = orc.random_volume(orc.rng(903), (14, 16, 18, 3), -0.2, 0.2)
+    lA = np.eye(3) + orc.random_volume(orc.rng(904), (3, 3, 1), -0.03, 0.03).reshape(3, 3)
+    lt = orc.random_volume(orc.rng(905), (3, 1, 1), -0.03, 0.03).reshape(3)
+    lw = ref.warp_labels_nn(lb, lu, lA, lt)
+    g.update({"lab_a": la, "lab_b": lb, "lab_u": lu, "lab_A": lA, "lab_t": lt, "lab_warped": lw,
+              "lab_metrics": np.array(ref.label_metrics(la, lb)),
+              "lab_metrics_sp": np.array(ref.label_metrics(la, lw, (0.7, 1.3, 2.1)))})
 
     # --- NIfTI-1 / raw + JSON IO (nifti.hpp), written and parsed by the reference itself
     g.update(nifti_fixtures(orc))
