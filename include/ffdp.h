@@ -386,6 +386,74 @@ FFDP_API int ffdp_minmax(const float* in, int64_t n, float* out, void* stream);
 FFDP_API int ffdp_sampler_z_extent(const float* u, ffdp_dims out_dims, ffdp_dims m_dims, const ffdp_sampler_args* args,
                           int64_t* out, void* stream);
 
+/* ----------------------------------------------------------- sharded context */
+/*
+ * One process drives `world` ranks (WorkerGroup(H), fabric.hpp:266-300): rank r is a z
+ * slab on devices[r] (devices may repeat; NULL = rank r on device r mod count) with its
+ * own stream; exchanges are peer copies (NVLink / NVSwitch between B200s). Collectives
+ * take arrays of `world` per-rank device pointers (rank r's on devices[r]) and run all
+ * ranks in lock step; they return when every rank's results are complete. Slabs follow
+ * shard_ranges (fabric.hpp:44-70) of the global z extent. Reductions are rank-ordered
+ * (fabric.hpp:246-263): deterministic for a given world size.
+ */
+typedef struct ffdp_comm_s* ffdp_comm;
+FFDP_API int ffdp_comm_create(int world, const int* devices, ffdp_comm* out);
+FFDP_API int ffdp_comm_destroy(ffdp_comm comm);
+FFDP_API int ffdp_comm_world(ffdp_comm comm);
+FFDP_API int ffdp_comm_device(ffdp_comm comm, int rank);
+/* shard_ranges (fabric.hpp:44-57): planes [lo, hi) of `rank` among `world` for n planes */
+FFDP_API int ffdp_shard_range(int64_t n, int world, int rank, int64_t* lo, int64_t* hi);
+/* halo_exchange (fabric.hpp:315-370): out[r] = [lo_r planes of rank r-1 | slab r | hi_r
+ * planes of rank r+1], lo_r = pad except on rank 0, hi_r = pad except on the last rank;
+ * `channels` floats per voxel. FFDP_INVALID_ARGUMENT when pad exceeds a neighbour's
+ * thickness (fabric.hpp:321-326). */
+FFDP_API int ffdp_halo_exchange(ffdp_comm comm, const float* const* slabs, ffdp_dims global, int channels, int pad,
+                                float* const* out, int64_t* lo_out, int64_t* hi_out);
+/* gp_convolve (distops.hpp:54-101): the separable convolution of a z-sharded volume /
+ * warp (ffdp_gp_convolve semantics per rank) with the neighbours' halo planes (sync), or
+ * of each shard as a standalone volume along z (sync = 0, the ablation). */
+FFDP_API int ffdp_dist_gp_convolve(ffdp_comm comm, const float* const* slabs, ffdp_dims global, int channels,
+                                   const double* taps, int ntaps, int mode, int sync, float* const* out);
+/* ring_sample (distops.hpp:144-168): the moved image on each rank's output slab of
+ * `out_global`, from the z-sharded moving image of `m_global` (u_shards interleaved xyz on
+ * the output slabs; A row-major 9, t 3, NULL = identity). Each rank gathers exactly the
+ * moving planes its samples touch (ffdp_sampler_z_extent) from their owners. */
+FFDP_API int ffdp_ring_sample(ffdp_comm comm, const float* const* m_shards, ffdp_dims m_global,
+                              const float* const* u_shards, ffdp_dims out_global, const double* A, const double* t,
+                              float* const* out);
+/* ring_sample_backward (distops.hpp:179-248): `want` as ffdp_sampler_bwd; g_img[r] is
+ * rank r's moving shard (every rank's contributions routed to the owners, added in rank
+ * order), g_u[r] its warp slab, gAt (host, 12 doubles: dA row-major, dt) summed over ranks. */
+FFDP_API int ffdp_ring_sample_bwd(ffdp_comm comm, const float* const* upstream, const float* const* m_shards,
+                                  ffdp_dims m_global, const float* const* u_shards, ffdp_dims out_global,
+                                  const double* A, const double* t, int want, float* const* g_img, float* const* g_u,
+                                  double* gAt);
+/* dist_mse (distops.hpp:260-282): *loss = sum over ranks of (F - M)^2 / n_total; grad = 2 (M - F) / n_total. */
+FFDP_API int ffdp_dist_mse(ffdp_comm comm, const float* const* f, const float* const* moved, ffdp_dims global,
+                           int64_t n_total, double* loss, float* const* grad);
+/* dist_mi (distops.hpp:355-396): local raw histograms, rank-ordered sum (the B*B + 2B
+ * payload, reported in *payload_elements), finalize, *loss = -MI, grad = dL/dmoved per rank. */
+FFDP_API int ffdp_dist_mi(ffdp_comm comm, const float* const* f, const float* const* moved, ffdp_dims global,
+                          const ffdp_parzen* kernel, int approx_forward, int64_t n_total, double* loss,
+                          float* const* grad, int64_t* payload_elements);
+/* dist_lncc (distops.hpp:285-352): window moments with r-plane halos (2r for the exact
+ * backward; none with gp_sync = 0, the ablation), sum of n allreduced, *loss = 1 - sum / N,
+ * grad = dL/dmoved (upstream 1, gi = -1/N). n_total <= 0: the global voxel count. */
+FFDP_API int ffdp_dist_lncc(ffdp_comm comm, const float* const* f, const float* const* moved, ffdp_dims global,
+                            int window, double eps, int ants_approx, int gp_sync, int64_t n_total, double* loss,
+                            float* const* grad);
+
+/* The fused deformable step over the ranks (ring_sample -> dist_lncc (ANTs) / dist_mi ->
+ * ring_sample_backward(warp), registration.hpp:277-312): per rank F and u with the
+ * window radius of halo planes (LNCC), the exact moving window of its samples, the
+ * single-GPU step kernels on the slab (ffdp_step_lncc / ffdp_step_mi_hist[_rec] +
+ * ffdp_step_mi_grad[_rec]), rank-ordered sums of sum_n / the joint histogram.
+ * loss_kind 0 = LNCC (window, eps; moment shifts = the global mid-ranges of F and M),
+ * 1 = MI (kernel); *loss as the single-GPU step; g_u[r] = dL/du on rank r's slab. */
+FFDP_API int ffdp_dist_step(ffdp_comm comm, int loss_kind, const float* const* f, const float* const* m,
+                            const float* const* u, ffdp_dims global, const double* A, const double* t, int window,
+                            double eps, const ffdp_parzen* kernel, double* loss, float* const* g_u);
+
 #ifdef __cplusplus
 }
 #endif

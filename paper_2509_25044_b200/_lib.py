@@ -67,6 +67,7 @@ class ParzenC(C.Structure):
 
 
 _vp, _dp = C.c_void_p, C.POINTER(C.c_double)
+_vpp = C.POINTER(C.c_void_p)
 _SIGS = {
     "ffdp_last_error": (C.c_char_p, []),
     "ffdp_abi_version": (C.c_int, []),
@@ -116,6 +117,24 @@ _SIGS = {
     "ffdp_minmax": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
     "ffdp_pad_window": (C.c_int, [_vp, Dims, C.c_int64, C.c_int64, _vp, _vp]),
     "ffdp_sampler_z_extent": (C.c_int, [_vp, Dims, Dims, C.POINTER(SamplerArgsC), _vp, _vp]),
+    # the sharded context: per-rank arguments are arrays of device pointers
+    "ffdp_comm_create": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+    "ffdp_comm_destroy": (C.c_int, [_vp]),
+    "ffdp_comm_world": (C.c_int, [_vp]),
+    "ffdp_comm_device": (C.c_int, [_vp, C.c_int]),
+    "ffdp_shard_range": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ffdp_halo_exchange": (C.c_int, [_vp, _vpp, Dims, C.c_int, C.c_int, _vpp, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int64)]),
+    "ffdp_dist_gp_convolve": (C.c_int, [_vp, _vpp, Dims, C.c_int, _dp, C.c_int, C.c_int, C.c_int, _vpp]),
+    "ffdp_ring_sample": (C.c_int, [_vp, _vpp, Dims, _vpp, Dims, _dp, _dp, _vpp]),
+    "ffdp_ring_sample_bwd": (C.c_int, [_vp, _vpp, _vpp, Dims, _vpp, Dims, _dp, _dp, C.c_int, _vpp, _vpp, _dp]),
+    "ffdp_dist_mse": (C.c_int, [_vp, _vpp, _vpp, Dims, C.c_int64, _dp, _vpp]),
+    "ffdp_dist_mi": (C.c_int, [_vp, _vpp, _vpp, Dims, C.POINTER(ParzenC), C.c_int, C.c_int64, _dp, _vpp,
+                               C.POINTER(C.c_int64)]),
+    "ffdp_dist_lncc": (C.c_int, [_vp, _vpp, _vpp, Dims, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int64, _dp,
+                                 _vpp]),
+    "ffdp_dist_step": (C.c_int, [_vp, C.c_int, _vpp, _vpp, _vpp, Dims, _dp, _dp, C.c_int, C.c_double,
+                                 C.POINTER(ParzenC), _dp, _vpp]),
 }
 
 
@@ -146,7 +165,8 @@ class _Lib:
         lib = self.load()
         fn = getattr(lib, name)
         if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check", "ffdp_step_mi_workspace_bytes",
-                    "ffdp_step_mi_record_bytes", "ffdp_step_lncc_workspace_bytes"):
+                    "ffdp_step_mi_record_bytes", "ffdp_step_lncc_workspace_bytes", "ffdp_comm_world",
+                    "ffdp_comm_device"):
             return fn
 
         def call(*args):

@@ -109,6 +109,13 @@ int num_sms() {
     return cached;
 }
 
+bool first_on_device(std::atomic<unsigned long long>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    return !(mask.fetch_or(bit) & bit);
+}
+
 void* scratch_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;
     if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) return nullptr;

@@ -8,6 +8,7 @@
 // trilinear weights and the gather run in fp32.
 #pragma once
 
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -530,6 +531,8 @@ int num_sms();
 // Stream-ordered scratch (cudaMallocAsync); freed with scratch_free on the same stream.
 void* scratch_alloc(size_t bytes, cudaStream_t s);
 void scratch_free(void* p, cudaStream_t s);
+// true the first time it is called for the current device (per-device kernel attributes)
+bool first_on_device(std::atomic<unsigned long long>& mask);
 
 }  // namespace ffdp
 

@@ -391,11 +391,10 @@ static int step_lncc_impl(const float* f, const float* u, ffdp_dims d, ffdp_slab
     P.zchunk = (int32_t)((nzs + chunks - 1) / chunks);
     chunks = (nzs + P.zchunk - 1) / P.zchunk;
     if (ty > 65535 || chunks > 65535) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: grid too large");
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_mask{0};
+    if (first_on_device(attr_mask)) {
         cudaFuncSetAttribute(k_step_lncc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
         cudaFuncSetAttribute(k_step_lncc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-        attr_set = true;
     }
     const dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)chunks);
     if (m.z_begin == 0 && m.z_end == m.dims.nz)

@@ -710,11 +710,10 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     }
     P.miss = miss;
     P.rec = reinterpret_cast<float4*>(rec);
-    static bool attr_set = false;  // opt in to > 48 KB dynamic shared memory, once
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_mask{0};  // opt in to > 48 KB dynamic shared memory
+    if (first_on_device(attr_mask)) {
         for (auto fn : {k_step_mi_hist<false, true, false>, k_step_mi_hist<false, false, false>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
-        attr_set = true;
     }
     const int64_t chunks = (P.nunits + HNT / 32 - 1) / (HNT / 32);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)num_sms()));
@@ -734,8 +733,8 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
             k_mi_hist_bs<false, true, 0, true>,    k_mi_hist_bs<true, true, 0, true>,
             k_mi_hist_bs<false, false, 32, true>,  k_mi_hist_bs<true, false, 32, true>,
             k_mi_hist_bs<false, true, 32, true>,   k_mi_hist_bs<true, true, 32, true>};
-        static bool bs_attr = false;
-        if (!bs_attr) {
+        static std::atomic<unsigned long long> bs_attr{0};
+        if (first_on_device(bs_attr)) {
             // the smallest shared-memory carve-out that holds the histogram: the rest is L1,
             // which the gather needs (percent of the 228 KB maximum, rounded up)
             const int pct = (int)std::min<size_t>(100, (smem + 2048) * 100 / (228 * 1024) + 1);
@@ -743,7 +742,6 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
                 cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             }
-            bs_attr = true;
         }
         table_[sel]<<<grid, HNT, smem, st>>>(P);
     } else {
@@ -792,11 +790,10 @@ int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ff
     const float* fi = f + (s.z_begin - s.buf_z0) * d.nx * d.ny;  // interior planes
     const int64_t n = d.nx * d.ny * (s.z_end - s.z_begin);
     const size_t smem = sizeof(float) * grad_tab_floats(B);
-    static bool attr_set = false;  // B up to 64: the 4 table copies may exceed 48 KB
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_mask{0};  // B up to 64: the 4 table copies may exceed 48 KB
+    if (first_on_device(attr_mask)) {
         for (auto fn : {k_step_mi_grad_rec<true>, k_step_mi_grad_rec<false>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * grad_tab_floats(64)));
-        attr_set = true;
     }
     const bool vec = (((uintptr_t)fi | (uintptr_t)rec | (uintptr_t)g_u) & 15) == 0;
     const int64_t work = vec ? n / 4 : n;
