@@ -976,5 +976,262 @@ inline RegistrationResult register_volumes(const Volume3& fixed, const Volume3& 
     return res;
 }
 
+// ------------------------------------------------------------------ sharded context
+// WorkerGroup(H) (fabric.hpp:266-300) as one process over H devices (ffdp_comm, DESIGN.md
+// "Sharded context"): rank r's shards live on device(r) (devices may repeat); every
+// collective runs all ranks in lock step. Shards follow shard_ranges (fabric.hpp:44-70).
+class DeviceScope {
+  public:
+    explicit DeviceScope(int d) {
+        cudaGetDevice(&prev_);
+        check_cuda(cudaSetDevice(d), "cudaSetDevice");
+    }
+    ~DeviceScope() { cudaSetDevice(prev_); }
+
+  private:
+    int prev_ = 0;
+};
+
+class WorkerGroup {
+  public:
+    explicit WorkerGroup(int world, const std::vector<int>& devices = {}) {
+        if (!devices.empty() && static_cast<int>(devices.size()) != world)
+            throw std::invalid_argument("WorkerGroup: one device per rank");
+        check(ffdp_comm_create(world, devices.empty() ? nullptr : devices.data(), &h_));
+    }
+    ~WorkerGroup() {
+        if (h_) ffdp_comm_destroy(h_);
+    }
+    WorkerGroup(const WorkerGroup&) = delete;
+    WorkerGroup& operator=(const WorkerGroup&) = delete;
+
+    int world() const { return ffdp_comm_world(h_); }
+    int device(int rank) const { return ffdp_comm_device(h_, rank); }
+    ffdp_comm handle() const { return h_; }
+    std::pair<std::int64_t, std::int64_t> shard_range(std::int64_t nz, int rank) const {
+        std::int64_t lo = 0, hi = 0;
+        check(ffdp_shard_range(nz, world(), rank, &lo, &hi));
+        return {lo, hi};
+    }
+    // rank r's z slab of v / w, allocated on device(r)
+    std::vector<Volume3> scatter(const Volume3& v) const {
+        std::vector<Volume3> out;
+        for (int r = 0; r < world(); ++r) {
+            const auto [lo, hi] = shard_range(v.dims.nz, r);
+            DeviceScope ds(device(r));
+            Volume3 s = Volume3::uninitialized(Dims3{v.dims.nx, v.dims.ny, hi - lo});
+            check_cuda(cudaMemcpy(s.data.data(), v.data.data() + lo * v.dims.nx * v.dims.ny,
+                                  sizeof(float) * s.dims.voxels(), cudaMemcpyDefault), "scatter");
+            out.push_back(std::move(s));
+        }
+        return out;
+    }
+    std::vector<WarpField> scatter(const WarpField& w) const {
+        std::vector<WarpField> out;
+        for (int r = 0; r < world(); ++r) {
+            const auto [lo, hi] = shard_range(w.dims.nz, r);
+            DeviceScope ds(device(r));
+            WarpField s = WarpField::uninitialized(Dims3{w.dims.nx, w.dims.ny, hi - lo});
+            check_cuda(cudaMemcpy(s.data.data(), w.data.data() + 3 * lo * w.dims.nx * w.dims.ny,
+                                  sizeof(float) * 3 * s.dims.voxels(), cudaMemcpyDefault), "scatter");
+            out.push_back(std::move(s));
+        }
+        return out;
+    }
+    // gather_volume / gather_warp (fabric.hpp:102-132): the global field on the current device
+    template <class Field>
+    Field gather(const std::vector<Field>& shards, Dims3 global) const {
+        Field out = Field::uninitialized(global);
+        const std::size_t per = out.data.size() / static_cast<std::size_t>(global.voxels());
+        for (int r = 0; r < world(); ++r) {
+            const auto lo = shard_range(global.nz, r).first;
+            check_cuda(cudaMemcpy(out.data.data() + per * lo * global.nx * global.ny, shards[r].data.data(),
+                                  sizeof(float) * shards[r].data.size(), cudaMemcpyDefault), "gather");
+        }
+        return out;
+    }
+    template <class Field>
+    std::vector<Field> empty_like(Dims3 global) const {
+        std::vector<Field> out;
+        for (int r = 0; r < world(); ++r) {
+            const auto [lo, hi] = shard_range(global.nz, r);
+            DeviceScope ds(device(r));
+            out.push_back(Field::uninitialized(Dims3{global.nx, global.ny, hi - lo}));
+        }
+        return out;
+    }
+
+  private:
+    ffdp_comm h_ = nullptr;
+};
+
+namespace detail {
+template <class Field>
+std::vector<const float*> cptrs(const std::vector<Field>& v) {
+    std::vector<const float*> p;
+    for (const auto& x : v) p.push_back(x.data.data());
+    return p;
+}
+template <class Field>
+std::vector<float*> mptrs(std::vector<Field>& v) {
+    std::vector<float*> p;
+    for (auto& x : v) p.push_back(x.data.data());
+    return p;
+}
+inline void check_world(const WorkerGroup& g, std::size_t n, const char* what) {
+    if (static_cast<int>(n) != g.world()) throw std::invalid_argument(std::string(what) + ": one shard per rank");
+}
+}  // namespace detail
+
+struct DistLoss {
+    double loss = 0;
+    std::vector<Volume3> grad_moved;
+    std::int64_t mi_payload_elements = 0;
+};
+
+struct RingSampleGrads {
+    std::optional<std::vector<Volume3>> image;
+    std::optional<std::vector<WarpField>> warp;
+    std::optional<Mat3> affine;
+    std::optional<Vec3> translation;
+};
+
+// halo_exchange (fabric.hpp:315-370): per rank [pad planes of r-1 | slab | pad planes of r+1]
+template <class Field>
+std::vector<Field> halo_exchange(const WorkerGroup& g, const std::vector<Field>& slabs, Dims3 global, int pad) {
+    detail::check_world(g, slabs.size(), "halo_exchange");
+    const int ch = static_cast<int>(slabs[0].data.size() / static_cast<std::size_t>(slabs[0].dims.voxels()));
+    std::vector<Field> out;
+    for (int r = 0; r < g.world(); ++r) {
+        const auto [lo, hi] = g.shard_range(global.nz, r);
+        const std::int64_t a = r > 0 ? pad : 0, b = r < g.world() - 1 ? pad : 0;
+        DeviceScope ds(g.device(r));
+        out.push_back(Field::uninitialized(Dims3{global.nx, global.ny, std::max<std::int64_t>(1, hi - lo + a + b)}));
+    }
+    auto in = detail::cptrs(slabs);
+    auto o = detail::mptrs(out);
+    check(ffdp_halo_exchange(g.handle(), in.data(), global.c(), ch, pad, o.data(), nullptr, nullptr));
+    return out;
+}
+
+// gp_convolve (distops.hpp:54-101) over the ranks' slabs
+template <class Field>
+std::vector<Field> gp_convolve(const WorkerGroup& g, const std::vector<Field>& slabs, Dims3 global,
+                               const std::vector<double>& taps, EdgeMode mode = EdgeMode::zero_pad, bool sync = true) {
+    detail::check_world(g, slabs.size(), "gp_convolve");
+    const int ch = static_cast<int>(slabs[0].data.size() / static_cast<std::size_t>(slabs[0].dims.voxels()));
+    auto out = g.template empty_like<Field>(global);
+    auto in = detail::cptrs(slabs);
+    auto o = detail::mptrs(out);
+    check(ffdp_dist_gp_convolve(g.handle(), in.data(), global.c(), ch, taps.data(), static_cast<int>(taps.size()),
+                                mode == EdgeMode::renormalize ? 1 : 0, sync ? 1 : 0, o.data()));
+    return out;
+}
+
+// ring_sample (distops.hpp:144-168): the moved image on every rank's output slab
+inline std::vector<Volume3> ring_sample(const WorkerGroup& g, const std::vector<Volume3>& m_shards, Dims3 m_global,
+                                        const std::vector<WarpField>& u_shards, Dims3 out_global, const Mat3& A,
+                                        const Vec3& t) {
+    detail::check_world(g, m_shards.size(), "ring_sample");
+    detail::check_world(g, u_shards.size(), "ring_sample");
+    auto out = g.empty_like<Volume3>(out_global);
+    auto m = detail::cptrs(m_shards);
+    auto u = detail::cptrs(u_shards);
+    auto o = detail::mptrs(out);
+    check(ffdp_ring_sample(g.handle(), m.data(), m_global.c(), u.data(), out_global.c(), A.m, t.v, o.data()));
+    return out;
+}
+
+// ring_sample_backward (distops.hpp:179-248)
+inline RingSampleGrads ring_sample_backward(const WorkerGroup& g, const std::vector<Volume3>& upstream,
+                                            const std::vector<Volume3>& m_shards, Dims3 m_global,
+                                            const std::vector<WarpField>& u_shards, Dims3 out_global, const Mat3& A,
+                                            const Vec3& t, const SamplerGradWant& want) {
+    detail::check_world(g, upstream.size(), "ring_sample_backward");
+    RingSampleGrads r;
+    std::vector<float*> gi, gu;
+    if (want.image) {
+        r.image = g.empty_like<Volume3>(m_global);
+        gi = detail::mptrs(*r.image);
+    }
+    if (want.warp) {
+        r.warp = g.empty_like<WarpField>(out_global);
+        gu = detail::mptrs(*r.warp);
+    }
+    double gat[12] = {0};
+    auto up = detail::cptrs(upstream);
+    auto m = detail::cptrs(m_shards);
+    auto u = detail::cptrs(u_shards);
+    check(ffdp_ring_sample_bwd(g.handle(), up.data(), m.data(), m_global.c(), u.data(), out_global.c(), A.m, t.v,
+                               want.mask(), want.image ? gi.data() : nullptr, want.warp ? gu.data() : nullptr, gat));
+    if (want.affine) {
+        Mat3 a;
+        std::memcpy(a.m, gat, sizeof(a.m));
+        r.affine = a;
+    }
+    if (want.translation) r.translation = Vec3{{gat[9], gat[10], gat[11]}};
+    return r;
+}
+
+inline DistLoss dist_mse(const WorkerGroup& g, const std::vector<Volume3>& f, const std::vector<Volume3>& moved,
+                         Dims3 global, std::int64_t n_total = 0) {
+    detail::check_world(g, f.size(), "dist_mse");
+    DistLoss d;
+    d.grad_moved = g.empty_like<Volume3>(global);
+    auto a = detail::cptrs(f), b = detail::cptrs(moved);
+    auto o = detail::mptrs(d.grad_moved);
+    check(ffdp_dist_mse(g.handle(), a.data(), b.data(), global.c(), n_total > 0 ? n_total : global.voxels(), &d.loss,
+                        o.data()));
+    return d;
+}
+
+inline DistLoss dist_mi(const WorkerGroup& g, const std::vector<Volume3>& f, const std::vector<Volume3>& moved,
+                        Dims3 global, const ParzenKernel& k, bool approx_forward = false, std::int64_t n_total = 0) {
+    detail::check_world(g, f.size(), "dist_mi");
+    DistLoss d;
+    d.grad_moved = g.empty_like<Volume3>(global);
+    auto a = detail::cptrs(f), b = detail::cptrs(moved);
+    auto o = detail::mptrs(d.grad_moved);
+    const ffdp_parzen kc = k.c();
+    check(ffdp_dist_mi(g.handle(), a.data(), b.data(), global.c(), &kc, approx_forward ? 1 : 0,
+                       n_total > 0 ? n_total : global.voxels(), &d.loss, o.data(), &d.mi_payload_elements));
+    return d;
+}
+
+inline DistLoss dist_lncc(const WorkerGroup& g, const std::vector<Volume3>& f, const std::vector<Volume3>& moved,
+                          Dims3 global, int window = 7, double eps = 1e-5, bool ants_approx = true, bool gp_sync = true,
+                          std::int64_t n_total = 0) {
+    detail::check_world(g, f.size(), "dist_lncc");
+    DistLoss d;
+    d.grad_moved = g.empty_like<Volume3>(global);
+    auto a = detail::cptrs(f), b = detail::cptrs(moved);
+    auto o = detail::mptrs(d.grad_moved);
+    check(ffdp_dist_lncc(g.handle(), a.data(), b.data(), global.c(), window, eps, ants_approx ? 1 : 0, gp_sync ? 1 : 0,
+                         n_total, &d.loss, o.data()));
+    return d;
+}
+
+// The fused deformable step over the ranks (ffdp_dist_step): (loss, g_u slabs)
+inline std::pair<double, std::vector<WarpField>> dist_step(const WorkerGroup& g, const std::vector<Volume3>& f,
+                                                           const std::vector<Volume3>& m,
+                                                           const std::vector<WarpField>& u, Dims3 global,
+                                                           const SamplerArgs& args, const LossParams& p) {
+    detail::check_world(g, f.size(), "dist_step");
+    if (p.kind == LossKind::mse || (p.kind == LossKind::lncc && !p.ants_approx) ||
+        (p.kind == LossKind::mi && p.mi_approx_forward))
+        throw std::invalid_argument("dist_step: the fused step runs LNCC (ANTs) and exact MI");
+    auto out = g.empty_like<WarpField>(global);
+    auto a = detail::cptrs(f), b = detail::cptrs(m), c = detail::cptrs(u);
+    auto o = detail::mptrs(out);
+    ffdp_parzen kc{};
+    if (p.kind == LossKind::mi)
+        kc = (p.mi_bspline_kernel ? ParzenKernel::bspline3(p.bins) : ParzenKernel::gaussian(p.bins)).c();
+    double loss = 0;
+    check(ffdp_dist_step(g.handle(), p.kind == LossKind::lncc ? 0 : 1, a.data(), b.data(), c.data(), global.c(),
+                         args.A.m, args.t.v, p.window, p.epsilon, p.kind == LossKind::mi ? &kc : nullptr, &loss,
+                         o.data()));
+    return {loss, std::move(out)};
+}
+
 }  // namespace voxreg
 }  // namespace ffdp

@@ -594,6 +594,58 @@ static void io_tests() {
     });
 }
 
+// ---------------------------------------------------------------- sharded context (test_distops.cpp)
+static double maxrel_f(const std::vector<float>& a, const std::vector<float>& b) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        num = std::max(num, (double)std::fabs(a[i] - b[i]));
+        den = std::max(den, (double)std::fabs(b[i]));
+    }
+    return den > 0 ? num / den : num;
+}
+
+static void comm_tests() {
+    run("WorkerGroup collectives = single GPU (2 and 3 ranks on one device)", [] {
+        const Pair p = make_pair(22, 19, 17, 611, false);
+        const V::Dims3 d = dims(p.d);
+        auto f = V::Volume3::from_host(d, p.f.data()), m = V::Volume3::from_host(d, p.m.data());
+        auto u = V::WarpField::from_host(d, p.u.data());
+        const V::SamplerArgs a = args_of(p);
+        const auto moved = V::fused_sample(m, &u, a);
+        for (int world : {2, 3}) {
+            V::WorkerGroup g(world, std::vector<int>(world, 0));
+            EXPECT_TRUE(g.world() == world && g.device(world - 1) == 0);
+            auto fs = g.scatter(f), ms = g.scatter(m);
+            auto us = g.scatter(u);
+            auto mv = V::ring_sample(g, ms, d, us, d, a.A, a.t);
+            EXPECT_TRUE(maxrel_f(g.gather(mv, d).to_host(), moved.to_host()) <= 1e-6);
+            // halo'd Sobolev smoothing equals the whole-volume convolution bit for bit
+            const auto taps = V::gaussian_taps(1.0);
+            const auto gs = V::gp_convolve(g, us, d, taps, V::EdgeMode::renormalize);
+            EXPECT_TRUE(g.gather(gs, d).to_host() == V::gp_convolve(u, taps, V::EdgeMode::renormalize).to_host());
+            // distributed LNCC on the moved slabs vs the fused operator on the whole volume
+            auto ref = V::lncc_forward_fused(f, moved, 7, 1e-5);
+            const auto rg = V::lncc_backward_fused(1.0, ref.second, f, moved, true).second;
+            const auto dl = V::dist_lncc(g, fs, mv, d);
+            EXPECT_TRUE(rel(dl.loss, ref.first.loss) <= 1e-6);
+            EXPECT_TRUE(maxrel_f(g.gather(dl.grad_moved, d).to_host(), rg.to_host()) <= 1e-5);
+            // the fused sharded step vs the single-GPU fused step
+            V::LossParams lp;
+            V::DeformableStep st(f, m, lp);
+            auto g1 = V::WarpField::uninitialized(d);
+            const auto r1 = st.step(u, a, g1);
+            const auto ds = V::dist_step(g, fs, ms, us, d, a, lp);
+            EXPECT_TRUE(rel(ds.first, r1.loss) <= 1e-5);
+            EXPECT_TRUE(maxrel_f(g.gather(ds.second, d).to_host(), g1.to_host()) <= 1e-4);
+        }
+        EXPECT_THROW(V::WorkerGroup(2, std::vector<int>{0}), std::invalid_argument);
+        EXPECT_THROW(V::WorkerGroup(2, std::vector<int>{0, 99}), std::invalid_argument);
+        V::WorkerGroup g3(3, std::vector<int>(3, 0));
+        auto thin = g3.scatter(V::Volume3::zeros(V::Dims3{5, 4, 7}));  // thicknesses 3, 2, 2
+        EXPECT_THROW(V::halo_exchange(g3, thin, V::Dims3{5, 4, 7}, 3), std::invalid_argument);
+    });
+}
+
 int main() {
     if (ffdp_device_check() != FFDP_OK) {
         std::printf("no usable sm_100 device: %s\n", ffdp_last_error());
@@ -605,6 +657,7 @@ int main() {
     step_tests();
     driver_tests();
     io_tests();
+    comm_tests();
     std::printf("%d checks, %d failed\n", g_checks, g_failed);
     return g_failed ? 1 : 0;
 }
