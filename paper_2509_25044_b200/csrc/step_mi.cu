@@ -345,10 +345,11 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
     uint32_t* mine = s32 + (lane % HCOPY) * CS + HPAD * LD + HPAD;
     const int64_t stride = (int64_t)gridDim.x * (HNT / 32);
     const int64_t zrec = (P.z_begin - P.buf_z0) * P.plane;  // records cover the interior planes
-    // The unit's F and u rows. (Loading them one unit ahead -- in registers after the
-    // interpolation, or staged in shared memory by cp.async -- measured slower: 0.206 and
-    // 0.200 vs 0.177 ms at 256^3; the first spills at 64 registers, the second takes L1
-    // from the gather.)
+    // The unit's F and u rows. (Loading them one unit ahead -- in registers across the
+    // gathers, in registers issued after this unit's interpolations so they fly during the
+    // histogram updates, or staged in shared memory by cp.async -- measured slower: 0.206,
+    // 0.187 and 0.200 vs 0.177 ms at 256^3; the first spills at 64 registers, the third
+    // takes L1 from the gather.)
     struct Ld {
         Unit w;
         float ff[4], uu[12];
