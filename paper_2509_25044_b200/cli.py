@@ -387,7 +387,6 @@ def run_info(path: str) -> int:
 def main(argv: Optional[List[str]] = None) -> int:
     """main (main.cpp:372-496), with its exit-code mapping."""
     from . import nifti
-    from ._lib import InvalidArgument
     args = list(sys.argv[1:] if argv is None else argv)
     if args and args[0] == "synth":
         print("config error: the 'synth' subcommand (fixture generation) is not part of this build",
@@ -409,6 +408,18 @@ def main(argv: Optional[List[str]] = None) -> int:
     if ns.command is None:
         print("A subcommand is required", file=sys.stderr)
         return 1
+    own = []
+    try:
+        return _dispatch(ns, own)
+    finally:
+        if own:  # the process group this call created (torchrun)
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def _dispatch(ns, own: list) -> int:
+    from . import nifti
+    from ._lib import InvalidArgument
     try:
         if ns.command == "register":
             world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -419,6 +430,7 @@ def main(argv: Optional[List[str]] = None) -> int:
                     if torch.cuda.is_available():  # several ranks may share one GPU (gloo staging)
                         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
                     dist.init_process_group(os.environ.get("FFDP_DIST_BACKEND", "nccl"))
+                    own.append(True)
             return run_register(ns)
         if ns.command == "metrics":
             return run_metrics(ns.a, ns.b, ns.spacing, ns.out)
