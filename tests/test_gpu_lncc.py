@@ -56,3 +56,62 @@ def test_convolve_axis_matches_oracle(V, orc):
             out = host(V.convolve_axis(dev(v), axis, taps, renormalize=(mode == "renormalize")))
             ref = orc.convolve_axis(v, axis, taps, mode)
             assert maxrel(out, ref) < 1e-6
+
+
+def _interior(a, r):
+    return a[r:-r, r:-r, r:-r]
+
+
+def test_lncc_affine_intensity_invariance(V, orc):
+    """test_lncc.cpp:38-53: M = 1.7 F + 0.4 correlates perfectly in full windows (eps 0)."""
+    f = r32(orc.random_volume(orc.rng(223), (12, 12, 12)))
+    m = r32(1.7 * f.astype(np.float64) + 0.4)
+    res, _ = V.lncc_forward_fused(dev(f), dev(m), 5, 0.0, want_map=True)
+    assert np.allclose(_interior(host(res.ncc_map), 2), 1.0, atol=1e-5)
+
+
+def test_lncc_near_stationary_at_self_similarity(V, orc):
+    """test_lncc.cpp:159-173: with F == M the exact gradient is O(eps) and far below a
+    generic pair's."""
+    f = r32(orc.random_volume(orc.rng(241), (12, 12, 12)))
+    other = r32(orc.random_volume(orc.rng(242), (12, 12, 12)))
+    _, st = V.lncc_forward_fused(dev(f), dev(f), 5, 1e-5)
+    gf, gm = V.lncc_backward_fused(1.0, st, dev(f), dev(f), False)
+    bound = 2e-5 * np.linalg.norm(f.astype(np.float64))
+    assert np.linalg.norm(host(gf)) <= bound and np.linalg.norm(host(gm)) <= bound
+    _, st2 = V.lncc_forward_fused(dev(f), dev(other), 5, 1e-5)
+    gf2, _ = V.lncc_backward_fused(1.0, st2, dev(f), dev(other), False)
+    assert np.linalg.norm(host(gf)) <= 0.01 * np.linalg.norm(host(gf2))
+
+
+def test_lncc_swap_symmetry(V, orc):
+    """test_lncc.cpp:175-185: swapping F and M swaps the gradients (bit-exact in the
+    reference; here the 5 channels are formed in the same order either way)."""
+    f = r32(orc.random_volume(orc.rng(251), (9, 9, 9)))
+    m = r32(orc.random_volume(orc.rng(252), (9, 9, 9)))
+    _, s1 = V.lncc_forward_fused(dev(f), dev(m), 5, 1e-5)
+    gf1, gm1 = V.lncc_backward_fused(1.0, s1, dev(f), dev(m), False)
+    _, s2 = V.lncc_forward_fused(dev(m), dev(f), 5, 1e-5)
+    gm2, gf2 = V.lncc_backward_fused(1.0, s2, dev(m), dev(f), False)
+    assert maxrel(host(gf1), host(gf2).astype(np.float64)) <= 1e-6
+    assert maxrel(host(gm1), host(gm2).astype(np.float64)) <= 1e-6
+
+
+def test_lncc_ants_equals_exact_for_window_1(V, orc):
+    """test_lncc.cpp:187-199: with a 1-voxel window the gamma box filter is the identity."""
+    f = r32(orc.random_volume(orc.rng(257), (7, 7, 7)))
+    m = r32(orc.random_volume(orc.rng(258), (7, 7, 7)))
+    _, s1 = V.lncc_forward_fused(dev(f), dev(m), 1, 1e-5)
+    ge = V.lncc_backward_fused(1.0, s1, dev(f), dev(m), False)
+    _, s2 = V.lncc_forward_fused(dev(f), dev(m), 1, 1e-5)
+    ga = V.lncc_backward_fused(1.0, s2, dev(f), dev(m), True)
+    for a, b in zip(ge, ga):
+        assert maxrel(host(a), host(b).astype(np.float64)) <= 1e-6
+
+
+def test_lncc_loss_non_decreasing_in_eps(V, orc):
+    """test_lncc.cpp:201-211."""
+    f = r32(orc.random_volume(orc.rng(263), (10, 10, 10)))
+    m = r32(orc.random_volume(orc.rng(264), (10, 10, 10)))
+    losses = [V.lncc_forward_fused(dev(f), dev(m), 5, eps)[0].loss for eps in (0.0, 1e-6, 1e-4, 1e-2, 1.0)]
+    assert all(b >= a for a, b in zip(losses, losses[1:]))

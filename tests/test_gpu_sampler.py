@@ -108,3 +108,15 @@ def test_zero_upstream_zero_gradients(V, orc):
                                 V.SamplerGradWant(True, True, True, True))
     assert not host(g.image).any() and not host(g.warp).any()
     assert not g.affine.any() and not g.translation.any()
+
+
+def test_sampler_linearity(V, orc):
+    """test_sampler.cpp:138-151: the sample is linear in the image."""
+    a = orc.random_volume(orc.rng(141), (6, 7, 8))
+    b = orc.random_volume(orc.rng(142), (6, 7, 8))
+    u = r32(orc.random_volume(orc.rng(143), (6, 7, 8, 3), -0.05, 0.05))
+    args = V.SamplerArgs()
+    sa = host(V.fused_sample(dev(r32(a)), dev(u), args)).astype(np.float64)
+    sb = host(V.fused_sample(dev(r32(b)), dev(u), args)).astype(np.float64)
+    sab = host(V.fused_sample(dev(r32(2.0 * a - 0.5 * b)), dev(u), args)).astype(np.float64)
+    assert np.max(np.abs(sab - (2.0 * sa - 0.5 * sb))) <= 1e-5
