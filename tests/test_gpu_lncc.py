@@ -115,3 +115,11 @@ def test_lncc_loss_non_decreasing_in_eps(V, orc):
     m = r32(orc.random_volume(orc.rng(264), (10, 10, 10)))
     losses = [V.lncc_forward_fused(dev(f), dev(m), 5, eps)[0].loss for eps in (0.0, 1e-6, 1e-4, 1e-2, 1.0)]
     assert all(b >= a for a, b in zip(losses, losses[1:]))
+
+
+def test_lncc_state_is_five_lattices(V, orc):
+    """test_lncc.cpp:81-98: the fused forward keeps exactly the 5 channel lattices."""
+    f = r32(orc.random_volume(orc.rng(81), (9, 10, 11)))
+    m = r32(orc.random_volume(orc.rng(82), (9, 10, 11)))
+    _, st = V.lncc_forward_fused(dev(f), dev(m), 5, 1e-5)
+    assert tuple(st.channels.shape) == (5, 9, 10, 11)

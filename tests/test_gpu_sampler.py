@@ -120,3 +120,16 @@ def test_sampler_linearity(V, orc):
     sb = host(V.fused_sample(dev(r32(b)), dev(u), args)).astype(np.float64)
     sab = host(V.fused_sample(dev(r32(2.0 * a - 0.5 * b)), dev(u), args)).astype(np.float64)
     assert np.max(np.abs(sab - (2.0 * sa - 0.5 * sb))) <= 1e-5
+
+
+def test_sampler_allocates_only_its_output(V, orc):
+    """test_sampler.cpp:89-107: fused_sample allocates exactly one output lattice."""
+    import torch
+    img = dev(r32(orc.random_volume(orc.rng(89), (20, 21, 22))))
+    u = dev(r32(orc.random_volume(orc.rng(90), (20, 21, 22, 3), -0.05, 0.05)))
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    out = V.fused_sample(img, u, V.SamplerArgs())
+    torch.cuda.synchronize()
+    grown = torch.cuda.memory_allocated() - before
+    assert out.numel() * 4 <= grown <= out.numel() * 4 + 511  # one block (allocator rounds to 512 B)
