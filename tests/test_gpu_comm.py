@@ -135,3 +135,28 @@ def test_comm_fused_step_matches_single_gpu(V, orc, loss, world):
     assert maxrel(cat(g), ref.g_u.cpu().numpy()) <= 1e-4
     if world == 1 and loss == "lncc":
         assert lv == ref.loss and np.array_equal(cat(g), ref.g_u.cpu().numpy())
+
+
+def test_comm_step_fd_across_ranks(V, orc):
+    """test_distops.cpp:314-367: the gradient through the collective (2 ranks, MI B-spline
+    step) matches a directional finite difference of the reduced loss (5%: fp32)."""
+    import torch
+    from oracle import step_inputs
+    from paper_2509_25044_b200.comm import Comm
+    si = step_inputs(orc, (40, 44, 48), seed=4242, loss="mi")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+    f, m, u = T(si.f), T(si.m), T(si.u)
+    p = V.LossParams(kind="mi", mi_bspline_kernel=True)
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    v = V.gp_convolve(torch.randn(u.shape, device="cuda", generator=gen).contiguous(), V.gaussian_taps(2.0),
+                      "renormalize")
+    with Comm(2, [0, 0]) as c:
+        fs, ms = c.scatter(f), c.scatter(m)
+        loss = lambda uu: c.step(fs, ms, c.scatter(uu.contiguous()), tuple(f.shape), si.A, si.t, p)
+        _, g = loss(u)
+        g = torch.cat([x.double() for x in g], 0)
+        for vox in (0.01, 0.03):
+            d = v / v.abs().max() * (vox * 2.0 / 39)
+            fd = (loss(u + d)[0] - loss(u - d)[0]) / 2.0
+            an = float((g * d.double()).sum())
+            assert abs(fd - an) <= 5e-2 * abs(an), (vox, fd, an)
