@@ -633,6 +633,26 @@ def cpu_reference(loss, sample_shape, steps, threads):
             "s_per_step": round(dt, 4)}
 
 
+def cpu_variants(loss, sample_shape, threads):
+    """SURVEY.md 8(d)'s other CPU timings of the reference step on the same sample: one
+    worker (H = 1) in double, and all host threads in T=float. One step each."""
+    from oracle import Oracle, Reference, step_inputs
+    try:
+        ref = Reference()
+    except FileNotFoundError:
+        return []
+    si = step_inputs(Oracle(), sample_shape, seed=4242, loss=loss)
+    n = int(si.f.size)
+    out = []
+    for world, fp32 in ((1, False), (threads, True)):
+        t0 = time.perf_counter()
+        ref.step(loss, si.f, si.m, si.u, si.A, si.t, world=world, fp32=fp32)
+        dt = time.perf_counter() - t0
+        out.append({"threads": world, "T": "float" if fp32 else "double", "value": round(n / dt / 1e9, 6),
+                    "unit": "Gvoxel/s", "s_per_step": round(dt, 4)})
+    return out
+
+
 def cpu_sample_for(loss):
     return (96, 96, 96) if loss == "mi" else (128, 128, 128)
 
@@ -691,6 +711,7 @@ def main():
         if not args.no_cpu and world == 1:
             try:
                 out["cpu_baseline"] = cpu_reference(loss, cpu_sample_for(loss), 2, os.cpu_count() or 1)
+                out["cpu_baseline"]["variants"] = cpu_variants(loss, cpu_sample_for(loss), os.cpu_count() or 1)
             except Exception as e:  # the baseline is reported, never required
                 out["cpu_baseline"] = {"value": None, "unit": "Gvoxel/s", "cores": 0, "kind": "port",
                                        "sample": f"unavailable: {e}"}
