@@ -415,6 +415,7 @@ class Reference:
         L.ref_jacobian_positive.argtypes = [_dp, _i64p, _dp]
         _u16p = C.POINTER(C.c_uint16)
         L.ref_label_metrics.argtypes = [_u16p, _u16p, _i64p, _dp, _dp]
+        L.ref_synth_labels.argtypes = [C.c_uint64, _i64p, C.c_int, C.c_double, _u16p, _u16p, _dp]
         L.ref_warp_labels_nn.argtypes = [_u16p, _i64p, _dp, _i64p, _dp, _dp, _u16p]
         L.ref_warp_update.argtypes = [_dp, _dp, _dp, _dp, _i64p, C.c_double, C.c_double, C.c_double, C.c_int64,
                                       C.c_int]
@@ -547,6 +548,15 @@ class Reference:
         out = C.c_double()
         self._check(self.lib.ref_jacobian_positive(_p(u), _arr_dims(u.shape[:3]), C.byref(out)))
         return out.value
+
+    def synth_labels(self, seed, shape, k=5, max_disp=0.12):
+        """(labels_fixed, labels_moving, pre_blur_fixed) of synth_pair."""
+        lf, lm = np.zeros(shape, np.uint16), np.zeros(shape, np.uint16)
+        pre = np.zeros(shape)
+        u16 = C.POINTER(C.c_uint16)
+        self._check(self.lib.ref_synth_labels(seed, _arr_dims(shape), k, max_disp, lf.ctypes.data_as(u16),
+                                              lm.ctypes.data_as(u16), _p(pre)))
+        return lf, lm, pre
 
     def label_metrics(self, a, b, spacing=(1.0, 1.0, 1.0)):
         """(dice mean, inv_dice, hd90_cumulative) of two uint16 label maps (nz, ny, nx)."""

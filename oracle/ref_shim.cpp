@@ -236,6 +236,17 @@ int ref_synth_pair(uint64_t seed, const int64_t* dims, int k, double max_disp, d
     });
 }
 
+// The label maps and the pre-blur image of synth_pair (synth.hpp:116-135).
+int ref_synth_labels(uint64_t seed, const int64_t* dims, int k, double max_disp, uint16_t* labels_fixed,
+                     uint16_t* labels_moving, double* pre_blur) {
+    return guarded([&] {
+        auto p = synth_pair(seed, D(dims), k, max_disp);
+        std::memcpy(labels_fixed, p.labels_fixed.data.data(), p.labels_fixed.data.size() * sizeof(uint16_t));
+        std::memcpy(labels_moving, p.labels_moving.data.data(), p.labels_moving.data.size() * sizeof(uint16_t));
+        put(p.pre_blur_fixed.data, pre_blur);
+    });
+}
+
 // gp_convolve (distops.hpp:84-101) of a whole volume sharded over H ranks, gathered.
 int ref_gp_convolve(const double* v, const int64_t* dims, int channels, const double* taps, int ntaps,
                     int renormalize, int sync, int world, double* out) {

@@ -3,6 +3,7 @@ subcommand, flags, `--config` file rules, output files and exit codes.
 
     python -m paper_2509_25044_b200.cli register --fixed F.nii --moving M.nii --out run [...]
     python -m paper_2509_25044_b200.cli metrics --a A.nii --b B.nii [--spacing x,y,z] [--out m.json]
+    python -m paper_2509_25044_b200.cli synth --out pair [--seed S] [--dims N|Nx,Ny,Nz] [--labels K]
     python -m paper_2509_25044_b200.cli info --in F.nii
 
 Exit codes (main.cpp:3-4): 0 success, 1 configuration error, 2 I/O or format error,
@@ -19,8 +20,8 @@ whatever `--float32` says (the flag is recorded in the summary); `--lncc-backend
 names the reference's materialised-graph ablation, whose values equal the fused
 backend's (test_lncc.cpp:70-79), and runs the fused path (single worker only, as in
 registration.hpp:238-239). `peak_alloc_bytes` is the device allocator's peak.
-`metrics` and the label block of the summary use metrics.py (host numpy, as the
-reference's are host code); `synth` (fixture generation, main.cpp:326-356) is not provided.
+`metrics` and the label block of the summary use metrics.py and `synth` uses synth.py
+(host numpy, as the reference's are host code; both bit-identical to the reference).
 """
 from __future__ import annotations
 
@@ -191,6 +192,13 @@ def _build_parser() -> argparse.ArgumentParser:
     met.add_argument("--b", dest="b", required=True, help="second label map (.nii)")
     met.add_argument("--spacing", dest="spacing", default="", help="override spacing x,y,z (mm)")
     met.add_argument("--out", dest="out", default="", help="also write the JSON here")
+    syn = sub.add_parser("synth", help="generate a labeled synthetic pair")
+    syn.add_argument("--seed", dest="seed", type=_int, default=2024, help="generator seed")
+    syn.add_argument("--dims", dest="dims", default="48", help="volume size, N or Nx,Ny,Nz (>= 16)")
+    syn.add_argument("--labels", dest="labels", type=_int, default=5, help="number of ellipsoidal labels (1..16)")
+    syn.add_argument("--max-disp", dest="max_disp", type=float, default=0.15,
+                     help="ground-truth warp cap, normalized units")
+    syn.add_argument("--out", dest="out", required=True, help="output prefix")
     inf = sub.add_parser("info", help="print a NIfTI header summary")
     inf.add_argument("--in", dest="in_path", required=True, help="input volume (.nii)")
     return app
@@ -369,6 +377,28 @@ def run_metrics(a_path: str, b_path: str, spacing_csv: str, out_path: str) -> in
     return 0
 
 
+def run_synth(seed: int, dims_csv: str, labels: int, max_disp: float, prefix: str) -> int:
+    """run_synth (main.cpp:326-356): synth_pair written as NIfTI volumes, label maps and the
+    true warp (synth.py reproduces the reference's generator bit for bit)."""
+    from . import nifti, synth
+    d = parse_list(dims_csv)
+    if len(d) == 1:
+        nx = ny = nz = int(d[0])
+    elif len(d) == 3:
+        nx, ny, nz = (int(v) for v in d)
+    else:
+        raise ConfigError("dims must be N or Nx,Ny,Nz")
+    p = synth.synth_pair(seed, (nz, ny, nx), labels, max_disp)
+    nifti.write_nifti(p.fixed, prefix + "_fixed.nii")
+    nifti.write_nifti(p.moving, prefix + "_moving.nii")
+    nifti.write_labels(p.labels_fixed, prefix + "_fixed_labels.nii")
+    nifti.write_labels(p.labels_moving, prefix + "_moving_labels.nii")
+    nifti.write_warp(p.true_warp, prefix + "_true_warp")
+    sys.stdout.write(f"wrote {prefix}_{{fixed,moving,fixed_labels,moving_labels}}.nii and "
+                     f"{prefix}_true_warp.{{raw,json}}\n")
+    return 0
+
+
 def run_info(path: str) -> int:
     """run_info (main.cpp:358-370)."""
     from .nifti import read_nifti
@@ -388,10 +418,6 @@ def main(argv: Optional[List[str]] = None) -> int:
     """main (main.cpp:372-496), with its exit-code mapping."""
     from . import nifti
     args = list(sys.argv[1:] if argv is None else argv)
-    if args and args[0] == "synth":
-        print("config error: the 'synth' subcommand (fixture generation) is not part of this build",
-              file=sys.stderr)
-        return 1
     try:
         args = expand_register_config(args)
     except (ConfigError, nifti.IoError, ValueError) as e:
@@ -434,6 +460,8 @@ def _dispatch(ns, own: list) -> int:
             return run_register(ns)
         if ns.command == "metrics":
             return run_metrics(ns.a, ns.b, ns.spacing, ns.out)
+        if ns.command == "synth":
+            return run_synth(ns.seed, ns.dims, ns.labels, ns.max_disp, ns.out)
         return run_info(ns.in_path)
     except ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)

@@ -186,6 +186,8 @@ def main():
     # --- synth pair + the full step at H = 1 and H = 2 / 3 (ring + halo + allreduce)
     f, m, w = ref.synth_pair(4242, (16, 17, 18), 5, 0.12)
     g.update({"synth_f": f, "synth_m": m, "synth_w": w})
+    lf, lm, pre = ref.synth_labels(4242, (16, 17, 18), 5, 0.12)
+    g.update({"synth_lf": lf, "synth_lm": lm, "synth_pre": pre})
     for loss in ("lncc", "mi"):
         si = step_inputs(orc, (18, 17, 16), seed=4242, loss=loss)
         g.update({f"step_{loss}_f": si.f, f"step_{loss}_m": si.m, f"step_{loss}_u": si.u, f"step_{loss}_A": si.A,

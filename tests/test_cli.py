@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2509_25044_b200 import cli, metrics as MT, nifti, registration as R
+from paper_2509_25044_b200 import cli, metrics as MT, nifti, registration as R, synth
 
 
 def run(capsys, *argv):
@@ -80,7 +80,9 @@ def test_config_missing_file_exit_1(tmp_path, capsys):
 @pytest.mark.parametrize("argv", [[], ["register", "--fixed", "a"], ["register", "--fixed", "a", "--moving", "b",
                                                                       "--out", "o", "--loss", "ncc"],
                                   ["register", "--fixed", "a", "--moving", "b", "--out", "o", "--window", "7.5"],
-                                  ["frobnicate"], ["synth", "--out", "x"]])
+                                  ["frobnicate"], ["synth", "--dims", "1,2", "--out", "x"],
+                                  ["synth", "--dims", "8", "--out", "x"], ["synth", "--labels", "0", "--out", "x"],
+                                  ["synth", "--max-disp", "0.2", "--out", "x"], ["synth", "--seed", "1"]])
 def test_parse_errors_exit_1(capsys, argv):
     assert run(capsys, *argv)[0] == 1
 
@@ -202,3 +204,24 @@ def test_register_config_errors(pair, capsys, monkeypatch):
     assert run(capsys, *base, "--scales", "x", "--iters", "1")[0] == 1        # stod
     assert run(capsys, *base, "--shards", "0")[0] == 1
     assert run(capsys, *base, "--shards", "2", "--lncc-backend", "naive")[0] == 1
+
+
+# ---------------------------------------------------------------- synth (synth.hpp, main.cpp:326-356)
+def test_synth_pair_matches_reference(golden):
+    p = synth.synth_pair(4242, (16, 17, 18), 5, 0.12)
+    for mine, key in ((p.fixed, "synth_f"), (p.moving, "synth_m"), (p.true_warp, "synth_w"),
+                      (p.labels_fixed, "synth_lf"), (p.labels_moving, "synth_lm"), (p.pre_blur_fixed, "synth_pre")):
+        assert np.array_equal(mine, golden[key]), key
+
+
+def test_synth_subcommand(golden, tmp_path, capsys):
+    pre = str(tmp_path / "pair")
+    code, out, _ = run(capsys, "synth", "--seed", "4242", "--dims", "18,17,16", "--labels", "5", "--max-disp", "0.12",
+                       "--out", pre)
+    assert code == 0 and out.startswith("wrote ")
+    f, m = nifti.read_nifti(pre + "_fixed.nii"), nifti.read_nifti(pre + "_moving.nii")
+    assert f.header.datatype == 64 and np.array_equal(f.volume, golden["synth_f"])
+    assert np.array_equal(m.volume, golden["synth_m"])
+    assert np.array_equal(nifti.nifti_to_labels(nifti.read_nifti(pre + "_fixed_labels.nii")), golden["synth_lf"])
+    assert np.array_equal(nifti.nifti_to_labels(nifti.read_nifti(pre + "_moving_labels.nii")), golden["synth_lm"])
+    assert np.array_equal(nifti.read_warp(pre + "_true_warp"), golden["synth_w"])
