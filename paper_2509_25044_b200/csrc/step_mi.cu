@@ -349,7 +349,8 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
     // gathers, in registers issued after this unit's interpolations so they fly during the
     // histogram updates, or staged in shared memory by cp.async -- measured slower: 0.206,
     // 0.187 and 0.200 vs 0.177 ms at 256^3; the first spills at 64 registers, the third
-    // takes L1 from the gather.)
+    // takes L1 from the gather. With 768 or 896 threads the registers allow the second:
+    // 0.178 / 0.180 ms, no better than 1024 threads without it.)
     struct Ld {
         Unit w;
         float ff[4], uu[12];
