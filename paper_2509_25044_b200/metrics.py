@@ -9,7 +9,7 @@ Label maps are uint16 arrays (nz, ny, nx), x fastest (volume.hpp:41-43); spacing
 """
 from __future__ import annotations
 
-from typing import Dict, Optional, Sequence, Tuple
+from typing import Dict, Sequence, Tuple
 
 import numpy as np
 
