@@ -268,7 +268,7 @@ class Stepper:
         if not record:
             lib.ffdp_step_mi(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
                              C.byref(self.kernel.c), self._p(self.ws.raw), self._p(self.ws.table), self._p(self.g_u),
-                             self._p(self.ws.scratch), self._p(rec), None, s)
+                             self._p(self.ws.scratch), self._p(rec) if rec is not None else None, None, s)
             return None
         self.ws.raw.zero_()
         ev[0].record()
