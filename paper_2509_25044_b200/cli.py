@@ -13,9 +13,10 @@ Exit codes (main.cpp:3-4): 0 success, 1 configuration error, 2 I/O or format err
 stage, then the multi-scale deformable stage on the GPU), warps the ORIGINAL moving
 image with the result and writes `<out>_warp.{raw,json}`, `<out>_moved.nii` (fp64),
 `<out>_trace.csv` and `<out>_summary.json` (also printed), as main.cpp:219-300 does.
-`--shards H` runs the z-slab sharded deformable stage and needs H torch.distributed ranks
-(`python -m torch.distributed.run --nproc-per-node H -m paper_2509_25044_b200.cli
-register ... --shards H`); rank 0 writes the outputs. The GPU path computes in fp32
+`--shards H` runs the z-slab sharded deformable stage: in this process over the node's
+GPUs (ffdp_comm, the reference's one-process model), or one rank per process under
+`python -m torch.distributed.run --nproc-per-node H -m paper_2509_25044_b200.cli
+register ... --shards H` (rank 0 writes the outputs). The GPU path computes in fp32
 whatever `--float32` says (the flag is recorded in the summary); `--lncc-backend naive`
 names the reference's materialised-graph ablation, whose values equal the fused
 backend's (test_lncc.cpp:70-79), and runs the fused path (single worker only, as in

@@ -195,3 +195,68 @@ class Comm:
                            None if t3 is None else t3.ctypes.data_as(C.POINTER(C.c_double)), p.window, p.epsilon,
                            None if k is None else C.byref(k.c), C.byref(loss), _ptrs(g))
         return loss.value, g
+
+    def warp_update(self, u, g_u, states, lr_norm: float, global_shape, sigma_grad: float = 1.0,
+                    sigma_warp: float = 0.5):
+        """The warp update of one iteration on the ranks' slabs (registration.hpp:313-317):
+        g_u halo exchange, ffdp_sobolev_adam per rank (u, m1, m2 in place), then the
+        halo'd warp smoothing (ffdp_dist_gp_convolve). Bit-identical to one GPU."""
+        from . import voxreg as V
+        from ._lib import Slab
+        for x, n in ((u, "u"), (g_u, "g_u")):
+            self._check(x, f"warp_update ({n})")
+        tg, tw = V.gaussian_taps(sigma_grad), V.gaussian_taps(sigma_warp)
+        g_h, lo, hi = self.halo_exchange(g_u, global_shape, len(tg) // 2)
+        nz = int(global_shape[0])
+        for r in range(self.world):
+            a, b = self.shard_range(nz, r)
+            st = states[r]
+            st.step += 1
+            with torch.cuda.device(self.devices[r]):
+                lib.ffdp_sobolev_adam(V._ptr(g_h[r]), V._ptr(u[r]), V._ptr(st.m1), V._ptr(st.m2),
+                                      V._dims(g_h[r].shape), Slab(a - lo[r], g_h[r].shape[0], a, b, nz),
+                                      V._taps_ptr(tg), len(tg), lr_norm, st.beta1, st.beta2, st.eps, st.step,
+                                      V._stream())
+        return self.gp_convolve(u, tw, global_shape, "renormalize")
+
+    def gather(self, slabs, device=None) -> torch.Tensor:
+        """gather_volume / gather_warp (fabric.hpp:102-132) onto one device."""
+        dev = device if device is not None else slabs[0].device
+        return torch.cat([s.to(dev) for s in slabs], 0)
+
+
+def comm_deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine, schedule, devices: Sequence[int],
+                          trace=None, scale_index_base: int = 0) -> torch.Tensor:
+    """deformable_stage (registration.hpp:230-331) with shards = len(devices), all ranks in
+    this process (the reference's own WorkerGroup model): per scale the resampled F, M and
+    warp are scattered to the ranks, each iteration runs ffdp_dist_step and the sharded
+    warp update, and the slabs are gathered at the end of the scale."""
+    from . import registration as R
+    from . import voxreg as V
+    schedule.validate()
+    A, t = (np.eye(3), np.zeros(3)) if affine is None else (np.asarray(affine[0]), np.asarray(affine[1]))
+    world = len(devices)
+    warp = None
+    with Comm(world, list(devices)) as c:
+        for s, step in enumerate(schedule.steps):
+            factor = 1.0 / step.downsample
+            f_s = fixed if factor == 1.0 else R.resample_scale(fixed, factor)
+            m_s = moving if factor == 1.0 else R.resample_scale(moving, factor)
+            shape = tuple(f_s.shape)
+            if shape[0] < world:
+                raise InvalidArgument(f"deformable_stage: {shape[0]} planes for {world} shards")
+            warp = R.resample_warp(warp, shape) if warp is not None else torch.zeros(shape + (3,), device=fixed.device)
+            fs, ms, us = c.scatter(f_s), c.scatter(m_s), c.scatter(warp)
+            states = [V.AdamState.zeros(x) for x in us]
+            lr_norm = V.deformable_lr_norm(shape, schedule.lr)
+            for it in range(step.iterations):
+                loss, g = c.step(fs, ms, us, shape, A, t, schedule.loss)
+                if not np.isfinite(loss):
+                    raise R.NumericalError("deformable stage diverged (non-finite loss)", trace or [])
+                if trace is not None:
+                    trace.append(R.TraceEntry(scale_index_base + s, it, loss))
+                us = c.warp_update(us, g, states, lr_norm, shape, schedule.sigma_grad, schedule.sigma_warp)
+            warp = c.gather(us, fixed.device)
+    if tuple(warp.shape[:3]) != tuple(fixed.shape):
+        warp = R.resample_warp(warp, fixed.shape)
+    return warp

@@ -108,8 +108,9 @@ class NumericalError(RuntimeError):
 
 @dataclass
 class DeformableOptions:
-    """DeformableOptions (registration.hpp:221-224); shards > 1 runs through
-    dist.ShardedStep / dist.sharded_warp_update under torch.distributed."""
+    """DeformableOptions (registration.hpp:221-224); shards > 1 runs one rank per
+    torch.distributed process when launched that way (dist.sharded_deformable_stage),
+    else all ranks in this process over the node's GPUs (comm.comm_deformable_stage)."""
     shards: int = 1
     gp_sync: bool = True
 
@@ -163,16 +164,22 @@ def deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine=None, sch
     if tuple(fixed.shape) != tuple(moving.shape):
         raise InvalidArgument("deformable_stage: F and M must share a lattice (registration.hpp:268-270)")
     if opts.shards > 1:
-        # one process per GPU: the shards are the torch.distributed ranks
-        from . import dist as D
-        _, world = D._world()
-        if world != opts.shards:
-            raise InvalidArgument(f"deformable_stage: shards = {opts.shards} needs {opts.shards} torch.distributed "
-                                  f"ranks (this job has {world})")
         if not opts.gp_sync:
             raise InvalidArgument("deformable_stage: the halo-free ablation (gp_sync = false) is not supported by "
                                   "the sharded step")
-        return D.sharded_deformable_stage(fixed, moving, affine, schedule, trace, scale_index_base)
+        from . import dist as D
+        _, world = D._world()
+        if world > 1:
+            # one process per GPU: the shards are the torch.distributed ranks
+            if world != opts.shards:
+                raise InvalidArgument(f"deformable_stage: shards = {opts.shards} with {world} torch.distributed "
+                                      "ranks")
+            return D.sharded_deformable_stage(fixed, moving, affine, schedule, trace, scale_index_base)
+        # one process over the node's GPUs (ffdp_comm; ranks share devices round-robin)
+        from .comm import comm_deformable_stage
+        n = max(1, torch.cuda.device_count())
+        return comm_deformable_stage(fixed, moving, affine, schedule, [r % n for r in range(opts.shards)], trace,
+                                     scale_index_base)
     A, t = (np.eye(3), np.zeros(3)) if affine is None else (np.asarray(affine[0]), np.asarray(affine[1]))
     warp = None
     for s, step in enumerate(schedule.steps):

@@ -1,7 +1,8 @@
 """`voxreg register` end to end on the GPU (cli.py over registration.register_volumes):
 the files it writes equal the library call's results, the label block is filled, and
-`--shards 2` under torch.distributed.run (gloo staging, two ranks on one GPU) reproduces
-the single-process warp to the sharded-stage tolerances."""
+`--shards 2` -- under torch.distributed.run (gloo staging, two ranks on one GPU) and in
+one process over ffdp_comm -- reproduces the one-shard warp to the sharded-stage
+tolerances."""
 import json
 import os
 import subprocess
@@ -92,8 +93,20 @@ def test_register_sharded_torchrun(files):
     s1, s2 = (json.load(open(str(d / f"{h}_summary.json"))) for h in ("h1", "h2"))
     assert s2["config"]["shards"] == 2 and s1["iterations"] == s2["iterations"] == 6
     assert abs(s2["final_loss"] - s1["final_loss"]) <= 1e-5 * abs(s1["final_loss"])
-    # a shard count that does not match the ranks is a configuration error
-    bad = subprocess.run([sys.executable, "-m", "paper_2509_25044_b200.cli"] + base
-                         + ["--out", str(d / "h3"), "--shards", "2"], cwd=ROOT, capture_output=True, text=True,
-                         timeout=600)
-    assert bad.returncode == 1 and "config error" in bad.stderr
+    # --shards 2 in ONE process (the reference's model): both ranks over ffdp_comm, here
+    # sharing the GPU
+    one2 = subprocess.run([sys.executable, "-m", "paper_2509_25044_b200.cli"] + base
+                          + ["--out", str(d / "h3"), "--shards", "2"], cwd=ROOT, capture_output=True, text=True,
+                          timeout=600)
+    assert one2.returncode == 0, one2.stderr[-2000:]
+    w3 = nifti.read_warp(str(d / "h3_warp"))
+    assert l2rel(w3, w1) <= 1e-3
+    assert np.max(np.abs(w3 - w1)) <= 0.25 * V.deformable_lr_norm(w1.shape[:3], 0.5)
+    s3 = json.load(open(str(d / "h3_summary.json")))
+    assert abs(s3["final_loss"] - s1["final_loss"]) <= 1e-5 * abs(s1["final_loss"])
+    # a shard count that does not match the torch.distributed ranks is a configuration error
+    bad = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr=127.0.0.1", "--master-port=29534", "-m", "paper_2509_25044_b200.cli"]
+                         + base + ["--out", str(d / "h4"), "--shards", "3"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert bad.returncode != 0 and "config error" in bad.stderr
