@@ -33,29 +33,35 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
-// a device allocation on one device, freed on scope exit
+// A device allocation of one rank, stream-ordered on the rank's stream (cudaMallocAsync
+// from the device's pool, which the context keeps cached: repeated collectives reuse
+// memory instead of paying cudaMalloc / cudaFree), freed on scope exit. Every collective
+// synchronises its ranks before returning, so the frees never overtake a reader.
 struct Buf {
     void* p = nullptr;
     int dev = 0;
+    cudaStream_t st = nullptr;
     Buf() = default;
     Buf(const Buf&) = delete;
     Buf& operator=(const Buf&) = delete;
-    Buf(Buf&& o) noexcept : p(o.p), dev(o.dev) { o.p = nullptr; }
+    Buf(Buf&& o) noexcept : p(o.p), dev(o.dev), st(o.st) { o.p = nullptr; }
     ~Buf() {
         if (p) {
             cudaSetDevice(dev);
-            cudaFree(p);
+            cudaFreeAsync(p, st);
         }
     }
-    int alloc(int d, size_t bytes, bool zero) {
-        dev = d;
-        cudaSetDevice(d);
-        if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+    int alloc(const ffdp_comm_s* c, int rank, size_t bytes, bool zero) {
+        dev = c->dev[rank];
+        st = c->st[rank];
+        cudaSetDevice(dev);
+        const size_t n = std::max<size_t>(bytes, 16);
+        if (cudaMallocAsync(&p, n, st) != cudaSuccess) {
             p = nullptr;
+            cudaGetLastError();
             return set_error(FFDP_CUDA, "comm: device allocation of %zu bytes failed", bytes);
         }
-        if (zero && cudaMemset(p, 0, std::max<size_t>(bytes, 16)) != cudaSuccess)
-            return set_error(FFDP_CUDA, "comm: memset failed");
+        if (zero && cudaMemsetAsync(p, 0, n, st) != cudaSuccess) return set_error(FFDP_CUDA, "comm: memset failed");
         return FFDP_OK;
     }
     template <typename T>
@@ -133,7 +139,7 @@ int allreduce_f64(const ffdp_comm_s* c, double* const* bufs, int64_t n) {
     const int w = c->world;
     if (w == 1 || n == 0) return FFDP_OK;
     Buf rows;
-    COMM_TRY(rows.alloc(c->dev[0], sizeof(double) * n * w, false));
+    COMM_TRY(rows.alloc(c, 0, sizeof(double) * n * w, false));
     for (int r = 0; r < w; ++r) COMM_TRY(copy(c, 0, rows.as<double>() + r * n, r, bufs[r], sizeof(double) * n));
     cudaSetDevice(c->dev[0]);
     k_sum_rows<<<grid_for(n), 256, 0, c->st[0]>>>(rows.as<double>(), w, n, bufs[0]);
@@ -174,7 +180,7 @@ int halo(const ffdp_comm_s* c, const float* const* slabs, ffdp_dims g, int ch, i
         lo[(size_t)r] = r > 0 ? pad : 0;
         hi[(size_t)r] = r < w - 1 ? pad : 0;
         const int64_t th = sh[(size_t)r].th();
-        COMM_TRY(out[(size_t)r].alloc(c->dev[r], sizeof(float) * plane * (th + lo[(size_t)r] + hi[(size_t)r]), false));
+        COMM_TRY(out[(size_t)r].alloc(c, r, sizeof(float) * plane * (th + lo[(size_t)r] + hi[(size_t)r]), false));
         float* o = out[(size_t)r].as<float>();
         COMM_TRY(copy(c, r, o + lo[(size_t)r] * plane, r, slabs[r], sizeof(float) * plane * th));
         if (lo[(size_t)r])  // the left neighbour's last planes
@@ -214,7 +220,7 @@ int moving_windows(const ffdp_comm_s* c, const float* const* m_shards, ffdp_dims
     const int64_t plane = mg.nx * mg.ny;
     std::vector<Buf> ext((size_t)w);
     for (int r = 0; r < w; ++r) {
-        COMM_TRY(ext[(size_t)r].alloc(c->dev[r], 2 * sizeof(int64_t), false));
+        COMM_TRY(ext[(size_t)r].alloc(c, r, 2 * sizeof(int64_t), false));
         const ffdp_dims od{og.nx, og.ny, osh[(size_t)r].th()};
         COMM_TRY(ffdp_sampler_z_extent(u_shards[r], od, mg, &args[(size_t)r], ext[(size_t)r].as<int64_t>(), c->st[r]));
     }
@@ -230,8 +236,8 @@ int moving_windows(const ffdp_comm_s* c, const float* const* m_shards, ffdp_dims
         W.z1 = e[0] <= e[1] ? std::min<int64_t>(mg.nz, e[1] + 1) : 0;
         W.z1 = std::max(W.z1, W.z0);
         const int64_t nzw = W.z1 - W.z0;
-        COMM_TRY(W.planes.alloc(c->dev[r], sizeof(float) * plane * nzw, false));
-        COMM_TRY(W.padded.alloc(c->dev[r], sizeof(float) * (mg.nx + 4) * (mg.ny + 4) * (nzw + 4), nzw == 0));
+        COMM_TRY(W.planes.alloc(c, r, sizeof(float) * plane * nzw, false));
+        COMM_TRY(W.padded.alloc(c, r, sizeof(float) * (mg.nx + 4) * (mg.ny + 4) * (nzw + 4), nzw == 0));
         for (int s = 0; s < w; ++s) {  // the owners' planes inside the window
             const int64_t a = std::max(W.z0, msh[(size_t)s].lo), b = std::min(W.z1, msh[(size_t)s].hi);
             if (a < b)
@@ -279,6 +285,12 @@ int ffdp_comm_create(int world, const int* devices, ffdp_comm* out) {
             return set_error(FFDP_CUDA, "comm_create: stream creation failed");
         }
         c->st.push_back(s);
+        // keep freed stream-ordered memory cached in the device's default pool
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->dev[r]) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
         for (int q = 0; q < r; ++q)  // NVLink peer access between distinct devices
             if (c->dev[q] != c->dev[r]) {
                 int ok = 0;
@@ -435,7 +447,7 @@ int ffdp_ring_sample_bwd(ffdp_comm c, const float* const* upstream, const float*
         const ffdp_dims od{out_global.nx, out_global.ny, osh[(size_t)r].th()};
         if (wi) {
             // image gradients land on the window's planes (dense, pad = 0 window)
-            COMM_TRY(gwin[(size_t)r].alloc(c->dev[r], sizeof(float) * plane * (W.z1 - W.z0), true));
+            COMM_TRY(gwin[(size_t)r].alloc(c, r, sizeof(float) * plane * (W.z1 - W.z0), true));
             if (W.z1 > W.z0) {
                 const ffdp_image_window iw{W.planes.as<float>(), m_global, W.z0, W.z1, 0};
                 COMM_TRY(ffdp_sampler_bwd(upstream[r], iw, u_shards[r], od, &args[(size_t)r], FFDP_WANT_IMAGE,
@@ -443,7 +455,7 @@ int ffdp_ring_sample_bwd(ffdp_comm c, const float* const* upstream, const float*
             }
         }
         if (ww || wat) {
-            if (wat) COMM_TRY(gat[(size_t)r].alloc(c->dev[r], 12 * sizeof(double), true));
+            if (wat) COMM_TRY(gat[(size_t)r].alloc(c, r, 12 * sizeof(double), true));
             const ffdp_image_window iw{W.padded.as<float>(), m_global, W.z0, W.z1, 2};
             const int mask = want & (FFDP_WANT_WARP | FFDP_WANT_AFFINE | FFDP_WANT_TRANSLATION);
             COMM_TRY(ffdp_sampler_bwd(upstream[r], iw, u_shards[r], od, &args[(size_t)r], mask, nullptr,
@@ -459,7 +471,7 @@ int ffdp_ring_sample_bwd(ffdp_comm c, const float* const* upstream, const float*
             cudaSetDevice(c->dev[s]);
             FFDP_CHECK_CUDA(cudaMemsetAsync(g_img[s], 0, sizeof(float) * plane * msh[(size_t)s].th(), c->st[s]));
             Buf tmp;
-            COMM_TRY(tmp.alloc(c->dev[s], sizeof(float) * plane * msh[(size_t)s].th(), false));
+            COMM_TRY(tmp.alloc(c, s, sizeof(float) * plane * msh[(size_t)s].th(), false));
             for (int r = 0; r < w; ++r) {
                 const Window& W = win[(size_t)r];
                 const int64_t a = std::max(W.z0, msh[(size_t)s].lo), b = std::min(W.z1, msh[(size_t)s].hi);
@@ -501,7 +513,7 @@ int ffdp_dist_mse(ffdp_comm c, const float* const* f, const float* const* moved,
     std::vector<Buf> s((size_t)w);
     std::vector<double*> bufs;
     for (int r = 0; r < w; ++r) {
-        COMM_TRY(s[(size_t)r].alloc(c->dev[r], sizeof(double), true));
+        COMM_TRY(s[(size_t)r].alloc(c, r, sizeof(double), true));
         COMM_TRY(ffdp_mse(f[r], moved[r], global.nx * global.ny * sh[(size_t)r].th(), n_total, grad[r],
                           s[(size_t)r].as<double>(), c->st[r]));
         bufs.push_back(s[(size_t)r].as<double>());
@@ -533,7 +545,7 @@ int ffdp_dist_mi(ffdp_comm c, const float* const* f, const float* const* moved, 
     std::vector<Buf> raw((size_t)w), tab((size_t)w);
     std::vector<double*> bufs;
     for (int r = 0; r < w; ++r) {
-        COMM_TRY(raw[(size_t)r].alloc(c->dev[r], sizeof(double) * nraw, true));
+        COMM_TRY(raw[(size_t)r].alloc(c, r, sizeof(double) * nraw, true));
         COMM_TRY(ffdp_mi_hist(f[r], moved[r], global.nx * global.ny * sh[(size_t)r].th(), kernel, approx_forward,
                               raw[(size_t)r].as<double>(), nullptr, nullptr, c->st[r]));
         bufs.push_back(raw[(size_t)r].as<double>());
@@ -541,7 +553,7 @@ int ffdp_dist_mi(ffdp_comm c, const float* const* f, const float* const* moved, 
     COMM_TRY(sync_all(c));
     COMM_TRY(allreduce_f64(c, bufs.data(), nraw));  // the B*B + 2B payload (distops.hpp:365-373)
     for (int r = 0; r < w; ++r) {
-        COMM_TRY(tab[(size_t)r].alloc(c->dev[r], sizeof(double) * ntab, false));
+        COMM_TRY(tab[(size_t)r].alloc(c, r, sizeof(double) * ntab, false));
         COMM_TRY(ffdp_mi_finalize(bufs[(size_t)r], B, -1.0, tab[(size_t)r].as<double>(), c->st[r]));
         COMM_TRY(ffdp_mi_bwd(f[r], moved[r], global.nx * global.ny * sh[(size_t)r].th(), kernel,
                              tab[(size_t)r].as<double>(), nullptr, grad[r], c->st[r]));
@@ -587,8 +599,8 @@ int ffdp_dist_lncc(ffdp_comm c, const float* const* f, const float* const* moved
         const int64_t nz_g = sync ? global.nz : th, g_lo = sync ? sh[(size_t)r].lo : 0;
         const int64_t nb = th + lo[(size_t)r] + hi[(size_t)r];
         const ffdp_dims bd{global.nx, global.ny, nb};
-        COMM_TRY(sn[(size_t)r].alloc(c->dev[r], sizeof(double), true));
-        COMM_TRY(state[(size_t)r].alloc(c->dev[r], sizeof(double) * 5 * plane * th, false));
+        COMM_TRY(sn[(size_t)r].alloc(c, r, sizeof(double), true));
+        COMM_TRY(state[(size_t)r].alloc(c, r, sizeof(double) * 5 * plane * th, false));
         COMM_TRY(ffdp_lncc_fwd(fh[(size_t)r].as<float>(), mh[(size_t)r].as<float>(), bd,
                                ffdp_slab{g_lo - lo[(size_t)r], nb, g_lo, g_lo + th, nz_g}, window, eps,
                                state[(size_t)r].as<double>(), nullptr, sn[(size_t)r].as<double>(), c->st[r]));
@@ -616,7 +628,7 @@ int ffdp_dist_lncc(ffdp_comm c, const float* const* f, const float* const* moved
         const int64_t nb = th + lo[(size_t)r] + hi[(size_t)r];
         const int64_t e0 = std::max<int64_t>(0, g_lo - rad), e1 = std::min<int64_t>(nz_g, g_lo + th + rad);
         Buf st_ext;
-        COMM_TRY(st_ext.alloc(c->dev[r], sizeof(double) * 5 * plane * (e1 - e0), false));
+        COMM_TRY(st_ext.alloc(c, r, sizeof(double) * 5 * plane * (e1 - e0), false));
         COMM_TRY(ffdp_lncc_fwd(fh[(size_t)r].as<float>(), mh[(size_t)r].as<float>(), ffdp_dims{global.nx, global.ny, nb},
                                ffdp_slab{g_lo - lo[(size_t)r], nb, e0, e1, nz_g}, window, eps, st_ext.as<double>(),
                                nullptr, nullptr, c->st[r]));
@@ -672,7 +684,7 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
     {
         std::vector<Buf> ext((size_t)w);
         for (int r = 0; r < w; ++r) {
-            COMM_TRY(ext[(size_t)r].alloc(c->dev[r], 2 * sizeof(int64_t), false));
+            COMM_TRY(ext[(size_t)r].alloc(c, r, 2 * sizeof(int64_t), false));
             const ffdp_dims bd{global.nx, global.ny, sh[(size_t)r].th() + lo[(size_t)r] + hi[(size_t)r]};
             COMM_TRY(ffdp_sampler_z_extent(uptr[(size_t)r], bd, global, &wargs[(size_t)r], ext[(size_t)r].as<int64_t>(),
                                            c->st[r]));
@@ -686,8 +698,8 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
             W.z0 = e[0] <= e[1] ? std::max<int64_t>(0, e[0]) : 0;
             W.z1 = std::max(W.z0, e[0] <= e[1] ? std::min<int64_t>(global.nz, e[1] + 1) : 0);
             const int64_t nzw = W.z1 - W.z0;
-            COMM_TRY(W.planes.alloc(c->dev[r], sizeof(float) * plane * nzw, false));
-            COMM_TRY(W.padded.alloc(c->dev[r], sizeof(float) * (global.nx + 4) * (global.ny + 4) * (nzw + 4), nzw == 0));
+            COMM_TRY(W.planes.alloc(c, r, sizeof(float) * plane * nzw, false));
+            COMM_TRY(W.padded.alloc(c, r, sizeof(float) * (global.nx + 4) * (global.ny + 4) * (nzw + 4), nzw == 0));
             for (int s2 = 0; s2 < w; ++s2) {
                 const int64_t a = std::max(W.z0, sh[(size_t)s2].lo), b = std::min(W.z1, sh[(size_t)s2].hi);
                 if (a < b)
@@ -705,7 +717,7 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
     if (lncc) {
         std::vector<Buf> mm((size_t)w);
         for (int r = 0; r < w; ++r) {
-            COMM_TRY(mm[(size_t)r].alloc(c->dev[r], 4 * sizeof(float), false));
+            COMM_TRY(mm[(size_t)r].alloc(c, r, 4 * sizeof(float), false));
             COMM_TRY(ffdp_minmax(f[r], plane * sh[(size_t)r].th(), mm[(size_t)r].as<float>(), c->st[r]));
             COMM_TRY(ffdp_minmax(m[r], plane * sh[(size_t)r].th(), mm[(size_t)r].as<float>() + 2, c->st[r]));
         }
@@ -735,18 +747,18 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
         const ffdp_slab sl{s.lo - lo[(size_t)r], nb, s.lo, s.hi, global.nz};
         const Window& W = win[(size_t)r];
         const ffdp_image_window iw{W.padded.as<float>(), global, W.z0, W.z1, 2};
-        COMM_TRY(red[(size_t)r].alloc(c->dev[r], sizeof(double) * nraw, true));
-        COMM_TRY(miss[(size_t)r].alloc(c->dev[r], sizeof(int32_t), true));
+        COMM_TRY(red[(size_t)r].alloc(c, r, sizeof(double) * nraw, true));
+        COMM_TRY(miss[(size_t)r].alloc(c, r, sizeof(int32_t), true));
         bufs.push_back(red[(size_t)r].as<double>());
         if (lncc) {
-            COMM_TRY(ws[(size_t)r].alloc(c->dev[r], (size_t)ffdp_step_lncc_workspace_bytes(bd, sl), false));
+            COMM_TRY(ws[(size_t)r].alloc(c, r, (size_t)ffdp_step_lncc_workspace_bytes(bd, sl), false));
             COMM_TRY(ffdp_step_lncc(fh[(size_t)r].as<float>(), uh[(size_t)r].as<float>(), bd, sl, iw, &ga, window, eps,
                                     -1.0 / (double)n_total, sf, sm, g_u[r], red[(size_t)r].as<double>(),
                                     miss[(size_t)r].as<int32_t>(), ws[(size_t)r].p, c->st[r]));
         } else {
-            COMM_TRY(ws[(size_t)r].alloc(c->dev[r], (size_t)ffdp_step_mi_workspace_bytes(B), true));
+            COMM_TRY(ws[(size_t)r].alloc(c, r, (size_t)ffdp_step_mi_workspace_bytes(B), true));
             if (bs) {
-                COMM_TRY(rec[(size_t)r].alloc(c->dev[r], (size_t)ffdp_step_mi_record_bytes(bd, sl), false));
+                COMM_TRY(rec[(size_t)r].alloc(c, r, (size_t)ffdp_step_mi_record_bytes(bd, sl), false));
                 COMM_TRY(ffdp_step_mi_hist_rec(fh[(size_t)r].as<float>(), uh[(size_t)r].as<float>(), bd, sl, iw, &ga,
                                                kernel, red[(size_t)r].as<double>(), ws[(size_t)r].p,
                                                rec[(size_t)r].as<float>(), miss[(size_t)r].as<int32_t>(), c->st[r]));
@@ -779,7 +791,7 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
         const int64_t nb = s.th() + lo[(size_t)r] + hi[(size_t)r];
         const ffdp_dims bd{global.nx, global.ny, nb};
         const ffdp_slab sl{s.lo - lo[(size_t)r], nb, s.lo, s.hi, global.nz};
-        COMM_TRY(tab[(size_t)r].alloc(c->dev[r], sizeof(double) * ntab, false));
+        COMM_TRY(tab[(size_t)r].alloc(c, r, sizeof(double) * ntab, false));
         COMM_TRY(ffdp_mi_finalize(bufs[(size_t)r], B, -1.0, tab[(size_t)r].as<double>(), c->st[r]));
         if (bs) {
             COMM_TRY(ffdp_step_mi_grad_rec(fh[(size_t)r].as<float>(), bd, sl, kernel, tab[(size_t)r].as<double>(),
