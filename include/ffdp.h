@@ -227,6 +227,19 @@ FFDP_API int ffdp_lncc_gamma(double* state, int64_t voxels, double eps, double g
 FFDP_API int ffdp_lncc_combine(const double* gamma, ffdp_dims buf_dims, ffdp_slab slab, int window, int ants,
                       const float* f, const float* m, float* grad_f, float* grad_m, void* stream);
 
+/* lncc_backward_fused (lncc.hpp:226-280) of a whole volume in one call: the gamma family
+ * (gi = -upstream / N, lncc.hpp:361) then the combination; `state` (from ffdp_lncc_fwd
+ * over the whole volume) is consumed, as the reference rewrites LnccState in place. */
+FFDP_API int ffdp_lncc_bwd(double upstream, double* state, const float* f, const float* m, ffdp_dims dims,
+                           int window, double eps, int ants, float* grad_f, float* grad_m, void* stream);
+
+/* lncc_forward_fused + lncc_backward_fused of a whole volume in one call (the survey's
+ * ffdp_lncc_fwdbwd): *sum_n (device) += the sum of n_i (loss = 1 - sum_n / N), grad_m
+ * (and grad_f if non-NULL) = d(upstream * loss) / dM; state = 5 * N doubles of workspace. */
+FFDP_API int ffdp_lncc_fwdbwd(const float* f, const float* m, ffdp_dims dims, int window, double eps, int ants,
+                              double upstream, double* state, double* sum_n, float* grad_f, float* grad_m,
+                              void* stream);
+
 /* ---------------------------------------------------------------------------- MI */
 
 /* ParzenKernel::gaussian/bspline3/delta (mi.hpp:33-63) incl. the normalisation check

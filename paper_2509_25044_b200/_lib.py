@@ -79,6 +79,9 @@ _SIGS = {
                                      _vp]),
     "ffdp_lncc_fwd": (C.c_int, [_vp, _vp, Dims, Slab, C.c_int, C.c_double, _vp, _vp, _vp, _vp]),
     "ffdp_lncc_gamma": (C.c_int, [_vp, C.c_int64, C.c_double, C.c_double, _vp]),
+    "ffdp_lncc_bwd": (C.c_int, [C.c_double, _vp, _vp, _vp, Dims, C.c_int, C.c_double, C.c_int, _vp, _vp, _vp]),
+    "ffdp_lncc_fwdbwd": (C.c_int, [_vp, _vp, Dims, C.c_int, C.c_double, C.c_int, C.c_double, _vp, _vp, _vp, _vp,
+                                   _vp]),
     "ffdp_lncc_combine": (C.c_int, [_vp, Dims, Slab, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "ffdp_parzen_make": (C.c_int, [C.c_int, C.c_int, C.c_double, C.POINTER(ParzenC)]),
     "ffdp_mi_hist": (C.c_int, [_vp, _vp, C.c_int64, C.POINTER(ParzenC), C.c_int, _vp, _vp,

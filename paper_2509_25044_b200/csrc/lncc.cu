@@ -255,4 +255,25 @@ int ffdp_lncc_combine(const double* gamma, ffdp_dims d, ffdp_slab s, int window,
     return check_launch("lncc_combine");
 }
 
+
+int ffdp_lncc_bwd(double upstream, double* state, const float* f, const float* m, ffdp_dims d, int window, double eps,
+                  int ants, float* grad_f, float* grad_m, void* stream) {
+    // lncc_backward_fused (lncc.hpp:226-280): gi = -upstream / N (lncc.hpp:361)
+    if (!state || !f || !m || !grad_m) return set_error(FFDP_INVALID_ARGUMENT, "lncc_backward: null pointer");
+    const int64_t n = d.nx * d.ny * d.nz;
+    if (n < 1) return set_error(FFDP_INVALID_ARGUMENT, "lncc_backward: empty volume");
+    const ffdp_slab full{0, d.nz, 0, d.nz, d.nz};
+    if (int rc = check_slab(d, full, window)) return rc;
+    if (int rc = ffdp_lncc_gamma(state, n, eps, -upstream / (double)n, stream)) return rc;
+    return ffdp_lncc_combine(state, d, full, window, ants, f, m, grad_f, grad_m, stream);
+}
+
+int ffdp_lncc_fwdbwd(const float* f, const float* m, ffdp_dims d, int window, double eps, int ants, double upstream,
+                     double* state, double* sum_n, float* grad_f, float* grad_m, void* stream) {
+    if (!sum_n) return set_error(FFDP_INVALID_ARGUMENT, "lncc: null sum_n");
+    const ffdp_slab full{0, d.nz, 0, d.nz, d.nz};
+    if (int rc = ffdp_lncc_fwd(f, m, d, full, window, eps, state, nullptr, sum_n, stream)) return rc;
+    return ffdp_lncc_bwd(upstream, state, f, m, d, window, eps, ants, grad_f, grad_m, stream);
+}
+
 }  // extern "C"

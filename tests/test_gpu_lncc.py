@@ -123,3 +123,23 @@ def test_lncc_state_is_five_lattices(V, orc):
     m = r32(orc.random_volume(orc.rng(82), (9, 10, 11)))
     _, st = V.lncc_forward_fused(dev(f), dev(m), 5, 1e-5)
     assert tuple(st.channels.shape) == (5, 9, 10, 11)
+
+
+@pytest.mark.parametrize("ants", [True, False])
+def test_lncc_fwdbwd_one_call(V, orc, golden, ants):
+    """ffdp_lncc_fwdbwd / ffdp_lncc_bwd (the one-call forward + backward of the survey's
+    ABI list) equal lncc_forward_fused + lncc_backward_fused."""
+    import ctypes as C
+    import torch
+    from paper_2509_25044_b200._lib import lib
+    f, m, w = r32(golden["lncc1_f"]), r32(golden["lncc1_m"]), int(golden["lncc1_w"])
+    res, st = V.lncc_forward_fused(dev(f), dev(m), w, 1e-5)
+    g1, g2 = V.lncc_backward_fused(1.3, st, dev(f), dev(m), ants)
+    ft, mt = dev(f), dev(m)
+    state = torch.empty((5,) + ft.shape, dtype=torch.float64, device="cuda")
+    sn = torch.zeros(1, dtype=torch.float64, device="cuda")
+    gf, gm = torch.empty_like(ft), torch.empty_like(mt)
+    lib.ffdp_lncc_fwdbwd(V._ptr(ft), V._ptr(mt), V._dims(ft.shape), w, 1e-5, int(ants), 1.3, V._ptr(state),
+                         V._ptr(sn), V._ptr(gf), V._ptr(gm), V._stream())
+    assert 1.0 - float(sn.item()) / ft.numel() == res.loss
+    assert torch.equal(gf, g1) and torch.equal(gm, g2)
