@@ -117,8 +117,24 @@ bool first_on_device(std::atomic<unsigned long long>& mask) {
 }
 
 void* scratch_alloc(size_t bytes, cudaStream_t s) {
+    // Keep freed scratch cached in the device's default pool (release threshold raised
+    // once per device): with the default threshold of 0 every synchronisation hands the
+    // memory back and the next multi-GB scratch (resample_scale, the workspaces) pays a
+    // fresh mapping.
+    static std::atomic<unsigned long long> pool_mask{0};
+    if (first_on_device(pool_mask)) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
     return p;
 }
 
