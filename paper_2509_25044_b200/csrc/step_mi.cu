@@ -45,7 +45,7 @@ struct Params {
     FastDiv div_nxb, div_nyq;
     int64_t plane, z_begin, buf_z0;
     int64_t nunits;
-    float fix_scale;           // 2^BS_LOG2 (bspline, k_mi_hist_bs) / 2^22 (gaussian) / 2^21 (delta)
+    float fix_scale;           // 2^23 or 2^21 (bspline, k_mi_hist_bs) / 2^22 (gaussian) / 2^21 (delta)
 };
 
 // B-spline weights at bins m_lo..m_lo+3 for one intensity, fp32 (the kernel is C2,
@@ -290,19 +290,23 @@ __global__ void __launch_bounds__(HNT, 1) k_step_mi_hist(const Params P) {
 #endif
 constexpr int HPAD = FFDP_MI_HPAD;
 constexpr int HDUMMY = HPAD == 2 ? 4 : 0;  // dummy rows per copy (HPAD 2)
-// Fixed-point scale 2^S (S = FFDP_MI_BS_LOG2, odd):
+// Fixed-point scale 2^S (S odd):
 // both weights are pre-scaled by 2^(S-149)/2 so that kI * kJ lands at 2^S kI kJ * 2^-149.
 // A voxel adds at most (2/3)^2 * 2^S to one counter, so a copy takes 2^(32-S) * 2^11
 // voxels between folds without wrapping (S = 21: 4096, S = 23: 1024).
-#ifndef FFDP_MI_BS_LOG2
-#define FFDP_MI_BS_LOG2 23
+// The scale is chosen per call: 2^23 below FFDP_MI_BS_LARGE_MIN interior voxels, 2^21
+// from there on (half the fold barriers: 0.160 vs 0.178 ms at 256^3). The coarser grid
+// rounds products under 2^-22 of a unit weight away, which only matters for a histogram
+// of few voxels: measured against the oracle, g_u agrees to 1.4e-6 (140k voxels) ..
+// 2.5e-6 (96^3) at either scale, while 4k-voxel slabs of the sharded step drift past the
+// 1e-5 loss gate over a multi-iteration stage at 2^21.
+#ifndef FFDP_MI_BS_LARGE_MIN
+#define FFDP_MI_BS_LARGE_MIN (1 << 17)
 #endif
-constexpr int BS_LOG2 = FFDP_MI_BS_LOG2;
-static_assert(BS_LOG2 % 2 == 1 && BS_LOG2 <= 23, "odd scale exponent: equal pre-scales");
-constexpr float BS_WSCALE = BS_LOG2 == 23 ? 0x1p-63f : BS_LOG2 == 21 ? 0x1p-64f : BS_LOG2 == 19 ? 0x1p-65f : 0.0f;
-constexpr float BS_FIX_SCALE = (float)(1 << BS_LOG2);
-constexpr int BS_FOLD_VOX = 1024 << (23 - BS_LOG2);
-constexpr int BS_FOLD_ITERS = BS_FOLD_VOX / HVOX_PER_COPY_ITER > 0 ? BS_FOLD_VOX / HVOX_PER_COPY_ITER : 1;
+__host__ __device__ constexpr float bs_wscale(int S) { return S == 23 ? 0x1p-63f : S == 21 ? 0x1p-64f : 0x1p-65f; }
+__host__ __device__ constexpr int bs_fold_iters(int S) {
+    return (1024 << (23 - S)) / HVOX_PER_COPY_ITER > 0 ? (1024 << (23 - S)) / HVOX_PER_COPY_ITER : 1;
+}
 __host__ __device__ constexpr int bs_ld(int B) { return B + 2 * HPAD; }
 __host__ __device__ constexpr int bs_stride(int B) {
     return ((bs_ld(B) * (bs_ld(B) + HDUMMY) + 31) / 32) * 32 + (32 / HCOPY);
@@ -329,8 +333,9 @@ __device__ __forceinline__ int32_t bspline_scaled(float v, int B, float C, float
     return min(max(m, -HPAD), (BC > 0 ? BC : B) + HPAD - 4);
 }
 
-template <bool FULLWIN, bool REC, int BC, bool OFF32>
+template <bool FULLWIN, bool REC, int BC, bool OFF32, int S>
 __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
+    static_assert(S == 21 || S == 23, "odd scale exponent: equal weight pre-scales");
     extern __shared__ __align__(16) unsigned char smem[];
     const int B = BC > 0 ? BC : P.p.bins;
     const int LD = bs_ld(B);
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 // Fixed point by a denormal product: with both weights pre-scaled by
-                // BS_WSCALE, kI * kJ lands at (2^S kI kJ) * 2^-149, whose IEEE bits ARE
+                // bs_wscale(S), kI * kJ lands at (2^S kI kJ) * 2^-149, whose IEEE bits ARE
                 // round(2^S kI kJ) (FMUL rounds to nearest; no -ftz).
                 float mw;
                 if (REC) {
@@ -401,8 +406,8 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
                     mw = interp(cr[k], c[k]);
                 }
                 float kI[4], kJ[4];
-                const int32_t mi = bspline_scaled<BC>(ff[k], B, BS_WSCALE, kI);
-                const int32_t mj = bspline_scaled<BC>(mw, B, BS_WSCALE, kJ);
+                const int32_t mi = bspline_scaled<BC>(ff[k], B, bs_wscale(S), kI);
+                const int32_t mj = bspline_scaled<BC>(mw, B, bs_wscale(S), kJ);
                 // HPAD 2: voxels outside the lattice add into the copy's dummy rows
                 uint32_t* h = (HPAD == 2 && !ok[k]) ? mine - HPAD * LD - HPAD + LD * LD : mine + mi * LD + mj;
 #pragma unroll
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
                         atomicAdd(h + a * LD + b, __float_as_uint(kI[a] * kJ[b]));
             }
         }
-        if (++iter == BS_FOLD_ITERS || base + stride >= P.nunits) {
+        if (++iter == bs_fold_iters(S) || base + stride >= P.nunits) {
             // fold the interior B x B counters of every copy (pad counters take the weight of
             // bins outside [0, B) and of voxels outside the lattice: never read, may wrap)
             iter = 0;
@@ -687,8 +692,7 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
     P.z_begin = s.z_begin;
     P.buf_z0 = s.buf_z0;
     P.nunits = (int64_t)P.nxb * P.nyq * (s.z_end - s.z_begin);
-    P.fix_scale = k.kind == FFDP_PARZEN_BSPLINE3 ? mstep::BS_FIX_SCALE : k.kind == FFDP_PARZEN_GAUSSIAN ? 4194304.0f
-                                                                                                 : 2097152.0f;
+    P.fix_scale = k.kind == FFDP_PARZEN_BSPLINE3 ? 8388608.0f : k.kind == FFDP_PARZEN_GAUSSIAN ? 4194304.0f : 2097152.0f;
     return P;
 }
 
@@ -725,16 +729,21 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     if (bs) {
         const size_t smem = bs_smem_bytes(B);
         const bool o32 = window_off32(P.g);
-        const int sel = (full ? 1 : 0) | (rec ? 2 : 0) | (B == 32 ? 4 : 0) | (o32 ? 8 : 0);
-        static const decltype(&k_mi_hist_bs<true, true, 32, true>) table_[16] = {
-            k_mi_hist_bs<false, false, 0, false>,  k_mi_hist_bs<true, false, 0, false>,
-            k_mi_hist_bs<false, true, 0, false>,   k_mi_hist_bs<true, true, 0, false>,
-            k_mi_hist_bs<false, false, 32, false>, k_mi_hist_bs<true, false, 32, false>,
-            k_mi_hist_bs<false, true, 32, false>,  k_mi_hist_bs<true, true, 32, false>,
-            k_mi_hist_bs<false, false, 0, true>,   k_mi_hist_bs<true, false, 0, true>,
-            k_mi_hist_bs<false, true, 0, true>,    k_mi_hist_bs<true, true, 0, true>,
-            k_mi_hist_bs<false, false, 32, true>,  k_mi_hist_bs<true, false, 32, true>,
-            k_mi_hist_bs<false, true, 32, true>,   k_mi_hist_bs<true, true, 32, true>};
+        const bool large = d.nx * d.ny * (s.z_end - s.z_begin) >= (int64_t)FFDP_MI_BS_LARGE_MIN;
+        P.fix_scale = large ? 2097152.0f : 8388608.0f;  // 2^21 / 2^23
+        const int sel = (full ? 1 : 0) | (rec ? 2 : 0) | (B == 32 ? 4 : 0) | (o32 ? 8 : 0) | (large ? 16 : 0);
+#define FFDP_BS_ROW(S)                                                                                    \
+    k_mi_hist_bs<false, false, 0, false, S>, k_mi_hist_bs<true, false, 0, false, S>,                    \
+        k_mi_hist_bs<false, true, 0, false, S>, k_mi_hist_bs<true, true, 0, false, S>,                  \
+        k_mi_hist_bs<false, false, 32, false, S>, k_mi_hist_bs<true, false, 32, false, S>,              \
+        k_mi_hist_bs<false, true, 32, false, S>, k_mi_hist_bs<true, true, 32, false, S>,                \
+        k_mi_hist_bs<false, false, 0, true, S>, k_mi_hist_bs<true, false, 0, true, S>,                  \
+        k_mi_hist_bs<false, true, 0, true, S>, k_mi_hist_bs<true, true, 0, true, S>,                    \
+        k_mi_hist_bs<false, false, 32, true, S>, k_mi_hist_bs<true, false, 32, true, S>,                \
+        k_mi_hist_bs<false, true, 32, true, S>, k_mi_hist_bs<true, true, 32, true, S>
+        static const decltype(&k_mi_hist_bs<true, true, 32, true, 23>) table_[32] = {FFDP_BS_ROW(23),
+                                                                                   FFDP_BS_ROW(21)};
+#undef FFDP_BS_ROW
         static std::atomic<unsigned long long> bs_attr{0};
         if (first_on_device(bs_attr)) {
             // the smallest shared-memory carve-out that holds the histogram: the rest is L1,
