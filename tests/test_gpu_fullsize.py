@@ -128,3 +128,17 @@ def test_warp_update_720_sharded_bit_identical(V):
         b0, b1 = max(0, lo - 3), min(720, hi + 3)
         part = V.gp_convolve(g[b0:b1].contiguous(), taps, "renormalize", slab=Slab(b0, b1 - b0, lo, hi, 720))
         assert torch.equal(part, full[lo:hi])
+
+
+def test_mi256_matches_oracle(V, orc):
+    """The headline configuration itself (BASELINE configs[1]: 256^3, B-spline MI, 32
+    bins) against the fp64 C oracle on the survey's synthetic pair: loss and g_u at the
+    north-star gates (measured: loss 2.5e-8, g_u 2.7e-6). The oracle takes ~30 s here."""
+    import torch
+    from oracle import step_inputs
+    si = step_inputs(orc, (256, 256, 256), seed=4242, loss="mi")
+    ref = orc.step_mi(si.f, si.m, si.u, orc.parzen("bspline3", 32), si.A, si.t)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+    r = V.warp_loss_step(T(si.f), T(si.m), T(si.u), si.A, si.t, V.LossParams(kind="mi", mi_bspline_kernel=True))
+    assert abs(r.loss / ref["loss"] - 1) <= 1e-5
+    assert maxrel(host(r.g_u), ref["g_u"]) <= 1e-4
