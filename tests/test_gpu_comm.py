@@ -160,3 +160,28 @@ def test_comm_step_fd_across_ranks(V, orc):
             fd = (loss(u + d)[0] - loss(u - d)[0]) / 2.0
             an = float((g * d.double()).sum())
             assert abs(fd - an) <= 5e-2 * abs(an), (vox, fd, an)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_comm_ring_sample_distinct_lattices(V, world):
+    """ring_sample with a moving lattice different from the output lattice
+    (distops.hpp:144-168 allows it; test_distops.cpp:139-289 pattern)."""
+    import torch
+    from paper_2509_25044_b200.comm import Comm
+    rng = np.random.default_rng(61)
+    m = rng.uniform(0, 1, (21, 23, 25)).astype(np.float32)
+    u = rng.uniform(-0.04, 0.04, SHAPE + (3,)).astype(np.float32)
+    up = rng.uniform(-1, 1, SHAPE).astype(np.float32)
+    A = np.eye(3) + rng.uniform(-0.03, 0.03, (3, 3))
+    t = rng.uniform(-0.03, 0.03, 3)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    args = V.SamplerArgs(A=A, t=t)
+    ref = V.fused_sample(T(m), T(u), args).cpu().numpy()
+    g = V.fused_sample_backward(T(up), T(m), T(u), args, V.SamplerGradWant(image=True, warp=True))
+    with Comm(world, [0] * world) as c:
+        ms, us, ups = c.scatter(T(m)), c.scatter(T(u)), c.scatter(T(up))
+        out = c.ring_sample(ms, m.shape, us, SHAPE, A, t)
+        assert maxrel(cat(out), ref) <= 1e-6
+        gi, gu, _, _ = c.ring_sample_backward(ups, ms, m.shape, us, SHAPE, A, t, want=("image", "warp"))
+        assert maxrel(cat(gu), g.warp.cpu().numpy()) <= 1e-6
+        assert maxrel(cat(gi), g.image.cpu().numpy()) <= 1e-5
