@@ -2,15 +2,19 @@
 """Benchmark of the fused warp + loss forward+backward step (the FFDP hot path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload mi256|lncc720|lncc128|lncc1024|mi1760] [--no-secondary]
+                    [--workload auto|mi1760|lncc720|mi256|lncc128|lncc1024] [--jitter bench|survey]
+                    [--no-secondary] [--no-cpu]
 
 Metric (BASELINE.json): Gvoxel/s of the fused warp+loss fwd+bwd step, voxel = output
 (fixed-lattice) voxel; one step = read F, M, u -> Mw -> loss -> dL/dMw -> g_u
-(registration.hpp:277-312). Default workload = BASELINE configs[1]: a synthetic
-256^3 multimodal pair, warp + Mattes MI (32 bins, B-spline Parzen) on one B200.
-A secondary LNCC line (configs[2], 720x640x720, window 7, ANTs) is added as
-``secondary``. Inputs (F, M, u, g_u: 536 MB at 256^3) exceed the 126 MB L2, so no L2
-flush is needed between steps. Rank 0 prints ONE JSON line.
+(registration.hpp:277-312). The N = 1 headline (--workload auto) is the largest
+single-GPU configuration: BASELINE configs[4], a 1760x1760x1200 (3.7 G-voxel) multimodal
+pair, warp + Mattes MI (32 bins, B-spline Parzen), when it fits the GPU, else configs[2]
+(720x640x720 LNCC, window 7, ANTs). Secondary lines: configs[2] and configs[1] (256^3 MI),
+each with the bench's sub-voxel u jitter and with SURVEY 8(d)'s U(-0.01, 0.01)-normalized
+jitter, each with its roofline and CPU baseline; the warp update; the configs[2]
+multi-scale registration. Every input set exceeds the 126 MB L2, so no flush is needed
+between steps. Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -113,13 +117,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ synthetic inputs
-def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None):
+def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, jitter="bench"):
     """Synthetic pair of the survey's recipe on the GPU, analytic in the
     global normalized frame so any z slab [z0, z1) of the global `shape` is generated
     locally and consistently across ranks: smooth ellipsoidal structures with texture,
     M = F pushed through a smooth warp, u = smooth field + sub-voxel jitter,
     A = I + U(-0.02, 0.02), t = U(-0.02, 0.02). MI: M = normalize(4 m (1 - m) + noise).
-    reduce_minmax(lo, hi) -> (lo, hi) makes the intensity normalisation global."""
+    reduce_minmax(lo, hi) -> (lo, hi) makes the intensity normalisation global.
+    jitter: "bench" adds U(-0.01, 0.01) voxel to u; "survey" adds SURVEY 8(d)'s
+    U(-0.01, 0.01) in normalized units (+-0.5 (n-1) / 100 voxels: +-3.6 at 720)."""
     import numpy as np
     import torch
 
@@ -168,11 +174,14 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None):
         m = normalize(4.0 * m * (1.0 - m) + 0.02 * noise)
         del noise
     u = smooth_field(0.02)
-    # sub-voxel jitter (+-0.02 voxel) keeps samples off cell faces; a registration warp is
+    # sub-voxel jitter (+-0.01 voxel) keeps samples off cell faces; a registration warp is
     # smooth (it is Gaussian-smoothed every iteration, registration.hpp:316), so the
     # parity tests' U(-0.01, 0.01)-normalized jitter (+-1.3 voxels at 256^3) would be an
     # unrealistically rough field for a throughput benchmark
-    jit = torch.tensor([0.04 / (nx - 1), 0.04 / (ny - 1), 0.04 / (nz - 1)], device=device)
+    if jitter == "survey":
+        jit = torch.tensor([0.02, 0.02, 0.02], device=device)
+    else:
+        jit = torch.tensor([0.04 / (nx - 1), 0.04 / (ny - 1), 0.04 / (nz - 1)], device=device)
     u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2 + z0), device=device)
           - 0.5) * jit
     aff = rnd(12).numpy() * 0.04 - 0.02
@@ -407,7 +416,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         return run_sharded(args, rank, world, local_rank, dev), None
     shape, loss, cfg = WORKLOADS[args.workload]
-    f, m, u, A, t = synth_inputs(shape, loss, 1234, dev)
+    jitter = getattr(args, "jitter", "bench")
+    f, m, u, A, t = synth_inputs(shape, loss, 1234, dev, jitter=jitter)
     st = Stepper(f, m, u, A, t, loss)
     hbm, hbm_kind = peaks()
     for _ in range(args.warmup):
@@ -466,6 +476,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f32 (fp64 coordinates / moment differences)", "data": "synthetic",
         "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}]",
                    "volume": "x".join(str(s) for s in shape[::-1]), "loss": loss,
+                   "u_jitter": ("SURVEY 8(d): U(-0.01, 0.01) normalized" if jitter == "survey" else
+                                "U(-0.01, 0.01) voxel"),
                    "loss_params": "window 7, eps 1e-5, ANTs" if loss == "lncc" else "32 bins, B-spline Parzen, exact",
                    "voxels_per_gpu": nvox, "parallelism": f"z-slab x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs (F, M, u, g_u) exceed the 126 MB L2; no flush between steps"},
@@ -583,30 +595,78 @@ def run_registration(shape, schedule_spec):
             "per_iteration": "fused warp+LNCC step (2 kernels + reduction), ffdp_sobolev_adam, ffdp_gp_convolve"}
 
 
+class HostStager:
+    """Host -> device copies of inputs that live in ordinary (pageable) host memory,
+    through two pinned staging buffers: the CPU fills one buffer while the DMA engine
+    drains the other (cudaMemcpyAsync from pinned memory on a copy stream). Used when the
+    inputs are too large to pin whole (configs[4]: 74 GB of F, M, u per step)."""
+
+    def __init__(self, chunk_bytes=256 << 20):
+        import torch
+        self.torch = torch
+        self.n = chunk_bytes // 4
+        self.bufs = [torch.empty(self.n, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.evs = [None, None]
+        self.stream = torch.cuda.Stream()
+        self.k = 0
+
+    def copy(self, dst, src):
+        """dst (CUDA, any strides) <- src (host, contiguous, same shape), split along dim 0."""
+        torch = self.torch
+        per = max(1, src[0].numel()) if src.dim() > 0 else 1
+        rows = max(1, self.n // per)
+        self.stream.wait_stream(torch.cuda.current_stream())
+        for z0 in range(0, src.shape[0], rows):
+            z1 = min(src.shape[0], z0 + rows)
+            i = self.k % 2
+            self.k += 1
+            if self.evs[i] is not None:
+                self.evs[i].synchronize()  # the DMA out of this buffer is done
+            cnt = (z1 - z0) * per
+            buf = self.bufs[i][:cnt]
+            buf.copy_(src[z0:z1].reshape(-1))
+            with torch.cuda.stream(self.stream):
+                dst[z0:z1].copy_(buf.view(src[z0:z1].shape), non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+            self.evs[i] = ev
+        torch.cuda.current_stream().wait_stream(self.stream)
+
+
 def run_e2e(args, st, f, m, u, A, t, loss, world):
+    """End to end through the public API: every step copies the step's inputs (F, M, u)
+    from host memory to the device, runs the step, and reads the loss back (8 bytes).
+    Inputs up to 8 GiB are pinned whole; larger ones (configs[4]) stay in pageable host
+    memory and go through HostStager's double-buffered pinned chunks."""
     import torch
-    if 4 * (f.numel() + m.numel() + u.numel()) > (8 << 30):
-        # pinned host copies of the inputs would exceed the host budget of a shared box
-        return {"value": None, "unit": "Gvoxel/s", "skipped": "inputs exceed the 8 GiB pinned-host budget",
-                "h2d_bytes_per_step": 4 * (f.numel() + m.numel() + u.numel()), "d2h_bytes_per_step": 8}
-    steps = max(3, min(args.steps, 20))
-    hf, hm, hu = (x.cpu().pin_memory() for x in (f, m, u))
+    nbytes = 4 * (f.numel() + m.numel() + u.numel())
+    steps = max(3, min(args.steps, 20 if nbytes <= (8 << 30) else 3))
+    staged = nbytes > (8 << 30)
+    hf, hm, hu = (x.cpu() for x in (f, m, u))
+    if not staged:
+        hf, hm, hu = (x.pin_memory() for x in (hf, hm, hu))
+        cp = lambda dst, src: dst.copy_(src, non_blocking=True)
+    else:
+        stager = HostStager()
+        cp = stager.copy
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     host_loss = 0.0
+    t0 = time.perf_counter()
     e0.record()
     for _ in range(steps):
-        st.f.copy_(hf, non_blocking=True)
-        st.mimg.interior.copy_(hm, non_blocking=True)  # H2D straight into the bordered layout
-        st.u.copy_(hu, non_blocking=True)
+        cp(st.f, hf)
+        cp(st.mimg.interior, hm)  # H2D straight into the bordered layout
+        cp(st.u, hu)
         st.step()
         host_loss = st.loss_value()  # D2H read of the step result (8 bytes)
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    h2d = (hf.numel() + hm.numel() + hu.numel()) * 4
+    wall = (time.perf_counter() - t0) / steps * 1e3
+    ms = max(e0.elapsed_time(e1) / steps, wall)
     return {"value": round(world * f.numel() / (ms * 1e-3) / 1e9, 4), "unit": "Gvoxel/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "ms_per_step": round(ms, 3), "steps": steps,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8, "ms_per_step": round(ms, 3), "steps": steps,
+            "host_buffers": "pageable, double-buffered pinned staging (256 MB chunks)" if staged else "pinned",
             "loss": host_loss}
 
 
@@ -663,17 +723,36 @@ def cpu_sample_for(loss):
     return (96, 96, 96) if loss == "mi" else (128, 128, 128)
 
 
+def default_workload():
+    """SURVEY / VERDICT rule: the N = 1 headline is the largest single-GPU configuration,
+    configs[4] (3.7 G-voxel MI; 119 GB of F, M, u, g_u) when it fits, else configs[2]."""
+    try:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.get_device_properties(0).total_memory >= (150 << 30):
+            return "mi1760"
+    except Exception:
+        pass
+    return "lncc720"
+
+
+SECONDARY_KEYS = ("value", "unit", "ms_per_step", "config", "roofline", "step_roofline", "kernel_ms", "clocks",
+                  "e2e", "loss", "gpu_launches")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="mi256", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="auto", choices=["auto"] + sorted(WORKLOADS))
+    ap.add_argument("--jitter", default="bench", choices=["bench", "survey"])
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.workload == "auto":
+        args.workload = default_workload()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -683,27 +762,47 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        # the reference's own step (oracle/_ref: the unmodified headers) on a bounded
+        # sample of the workload, all host threads; inputs and libraries are prepared once,
+        # outside the timed loop, so each timed step is exactly one ref.step call
+        from oracle import Oracle, Reference, step_inputs
         threads = os.cpu_count() or 1
         samp = cpu_sample_for(loss)
-        reps = []
+        try:
+            ref = Reference()
+            kind = "reference"
+        except FileNotFoundError:
+            ref, kind = None, "port"
+        orc = Oracle()
+        si = step_inputs(orc, samp, seed=4242, loss=loss)
+        kern = orc.parzen("bspline3", 32)
+
+        def one():
+            if ref is not None:
+                ref.step(loss, si.f, si.m, si.u, si.A, si.t, world=threads)
+            elif loss == "lncc":
+                orc.step_lncc(si.f, si.m, si.u, si.A, si.t)
+            else:
+                orc.step_mi(si.f, si.m, si.u, kern, si.A, si.t)
+
         for _ in range(args.warmup):
-            cpu_reference(loss, samp, 1, threads)
+            one()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            reps.append(cpu_reference(loss, samp, 1, threads))
+            one()
         dt = (time.perf_counter() - t0) / args.steps
         n = samp[0] * samp[1] * samp[2]
         v = n / dt / 1e9
-        cb = dict(reps[-1])
-        cb["value"] = round(v, 6)
+        sample = (f"{'x'.join(str(s) for s in samp[::-1])} {loss} step x{args.steps} "
+                  f"({'T=double, WorkerGroup(%d)' % threads if ref is not None else 'C port, 1 thread'})")
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "Gvoxel/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}] (bounded sample "
                                    f"{'x'.join(str(s) for s in samp[::-1])} on the host cores)", "loss": loss},
-            "cpu_baseline": {"value": round(v, 6), "unit": "Gvoxel/s", "cores": cb["cores"], "kind": cb["kind"],
-                             "sample": cb["sample"]},
+            "cpu_baseline": {"value": round(v, 6), "unit": "Gvoxel/s", "cores": threads if ref is not None else 1,
+                             "kind": kind, "sample": sample},
             "e2e": {"value": round(v, 6), "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -713,24 +812,43 @@ def main():
         # (host-staged exchanges; a functional check, not a scaling measurement)
         dist.init_process_group(os.environ.get("FFDP_DIST_BACKEND", "nccl"))
     out, st = run_ours(args, rank, world, local_rank)
-    if rank == 0:
-        if not args.no_cpu and world == 1:
-            try:
-                out["cpu_baseline"] = cpu_reference(loss, cpu_sample_for(loss), 2, os.cpu_count() or 1)
-                out["cpu_baseline"]["variants"] = cpu_variants(loss, cpu_sample_for(loss), os.cpu_count() or 1)
-            except Exception as e:  # the baseline is reported, never required
-                out["cpu_baseline"] = {"value": None, "unit": "Gvoxel/s", "cores": 0, "kind": "port",
-                                       "sample": f"unavailable: {e}"}
-        if not args.no_secondary and args.workload == "mi256" and world == 1:
-            import torch
-            del st
-            torch.cuda.empty_cache()
-            a2 = argparse.Namespace(**vars(args))
-            a2.workload, a2.steps = "lncc720", max(5, min(args.steps, 20))
-            sec, _ = run_ours(a2, rank, world, local_rank)
-            out["secondary"] = {k: sec[k] for k in ("value", "unit", "ms_per_step", "config", "roofline",
-                                                    "step_roofline", "kernel_ms", "clocks", "e2e", "loss")}
-            torch.cuda.empty_cache()
+    if rank == 0 and world == 1:
+        import torch
+        del st
+        torch.cuda.empty_cache()
+        cpu = {}
+
+        def baseline(kind_loss):
+            if args.no_cpu:
+                return None
+            if kind_loss not in cpu:
+                try:
+                    cb = cpu_reference(kind_loss, cpu_sample_for(kind_loss), 2, os.cpu_count() or 1)
+                    cb["variants"] = cpu_variants(kind_loss, cpu_sample_for(kind_loss), os.cpu_count() or 1)
+                except Exception as e:  # the baseline is reported, never required
+                    cb = {"value": None, "unit": "Gvoxel/s", "cores": 0, "kind": "port", "sample": f"unavailable: {e}"}
+                cpu[kind_loss] = cb
+            return cpu[kind_loss]
+
+        cb = baseline(loss)
+        if cb is not None:
+            out["cpu_baseline"] = cb
+        if not args.no_secondary:
+            sec = []
+            for wl, jit in (("lncc720", "bench"), ("lncc720", "survey"), ("mi256", "bench"), ("mi256", "survey")):
+                if wl == args.workload and jit == args.jitter:
+                    continue
+                a2 = argparse.Namespace(**vars(args))
+                a2.workload, a2.jitter, a2.steps = wl, jit, max(5, min(args.steps, 20))
+                r, s2 = run_ours(a2, rank, world, local_rank)
+                del s2
+                torch.cuda.empty_cache()
+                line = {k: r[k] for k in SECONDARY_KEYS if k in r}
+                c2 = baseline(WORKLOADS[wl][1])
+                if c2 is not None:
+                    line["cpu_baseline"] = c2
+                sec.append(line)
+            out["secondary"] = sec
             hbm, hbm_kind = peaks()
             out["warp_update"] = run_warp_update(WORKLOADS["lncc720"][0], max(5, min(args.steps, 20)), hbm, hbm_kind)
             torch.cuda.empty_cache()

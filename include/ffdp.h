@@ -111,6 +111,11 @@ FFDP_API const char* ffdp_last_error(void);
 FFDP_API int ffdp_abi_version(void);
 /* Fails with FFDP_CUDA unless an sm_100 device is current. */
 FFDP_API int ffdp_device_check(void);
+/* The library's stream-ordered scratch lives in its own memory pool per device (not the
+ * process's default pool), which keeps up to 4 GiB of freed scratch cached across calls.
+ * ffdp_scratch_trim returns all but keep_bytes of that cache to the current device (the
+ * drivers call it at the end of each scale / stage). */
+FFDP_API int ffdp_scratch_trim(int64_t keep_bytes);
 
 /* ---------------------------------------------------------------------- sampler */
 

@@ -539,6 +539,8 @@ class DeformableStep {
         if (p.kind == LossKind::mse) throw std::invalid_argument("DeformableStep: MSE runs through loss_and_grad");
         if (p.kind == LossKind::lncc && !p.ants_approx)
             throw std::invalid_argument("DeformableStep: the fused LNCC step implements the ANTs backward");
+        if (p.kind == LossKind::lncc && p.window != 7)
+            throw std::invalid_argument("DeformableStep: the fused LNCC step is built for window 7");
         if (p.kind == LossKind::mi && p.mi_approx_forward)
             throw std::invalid_argument("DeformableStep: the fused MI step uses the exact Parzen forward");
         const Dims3 d = dims_;
@@ -831,7 +833,9 @@ inline std::pair<double, Volume3> loss_and_grad(const Volume3& f, const Volume3&
 // Whether DeformableStep's fused kernels cover the loss (else deformable_stage composes
 // fused_sample -> loss_and_grad -> fused_sample_backward).
 inline bool fused_loss(const LossParams& p) {
-    return (p.kind == LossKind::lncc && p.ants_approx) || (p.kind == LossKind::mi && !p.mi_approx_forward);
+    // the fused kernels: LNCC window 7 (ANTs backward), MI with the exact Parzen forward
+    return (p.kind == LossKind::lncc && p.ants_approx && p.window == 7) ||
+           (p.kind == LossKind::mi && !p.mi_approx_forward);
 }
 
 // deformable_stage (registration.hpp:230-331) on one GPU: per scale resample F and M on
@@ -1217,9 +1221,7 @@ inline std::pair<double, std::vector<WarpField>> dist_step(const WorkerGroup& g,
                                                            const std::vector<WarpField>& u, Dims3 global,
                                                            const SamplerArgs& args, const LossParams& p) {
     detail::check_world(g, f.size(), "dist_step");
-    if (p.kind == LossKind::mse || (p.kind == LossKind::lncc && !p.ants_approx) ||
-        (p.kind == LossKind::mi && p.mi_approx_forward))
-        throw std::invalid_argument("dist_step: the fused step runs LNCC (ANTs) and exact MI");
+    if (!fused_loss(p)) throw std::invalid_argument("dist_step: the fused step runs LNCC (ANTs, window 7) and exact MI");
     auto out = g.empty_like<WarpField>(global);
     auto a = detail::cptrs(f), b = detail::cptrs(m), c = detail::cptrs(u);
     auto o = detail::mptrs(out);

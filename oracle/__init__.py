@@ -383,6 +383,75 @@ class Oracle:
             raise ValueError("mi: intensities must lie in [0,1]")
         return dict(loss=loss, g_u=g_u, moved=moved, grad_moved=gm, raw=raw)
 
+    # -- full-size checks (ffdp_oracle_big.c): fp32 inputs, fp64 arithmetic, OpenMP ----------
+    @staticmethod
+    def _f32(a):
+        return np.ascontiguousarray(a, dtype=np.float32)
+
+    def _big(self, name, argtypes, restype=None):
+        fn = getattr(self.lib, name)
+        fn.argtypes = argtypes
+        fn.restype = restype
+        return fn
+
+    def lncc_sum_n_f32(self, f, m, u, A=None, t=None, window=7, eps=1e-5):
+        """sum_i n_i of the warped pair over the whole lattice (loss = 1 - sum / N)."""
+        f, m, u = self._f32(f), self._f32(m), self._f32(u)
+        A, t, _, _ = _args(A, t, None, None)
+        fp = C.POINTER(C.c_float)
+        fn = self._big("or_lncc_sum_n_f32", [fp, fp, fp, Dims, _dp, _dp, C.c_int, C.c_double], C.c_double)
+        return fn(f.ctypes.data_as(fp), m.ctypes.data_as(fp), u.ctypes.data_as(fp), _dims_of(f.shape), _p(A), _p(t),
+                  window, eps)
+
+    def lncc_ants_voxels_f32(self, f, m, u, vox, A=None, t=None, window=7, eps=1e-5, gi=None):
+        """n_i, ANTs dL/dMw and g_u at the flat voxel indices `vox` (gi defaults to -1/N)."""
+        f, m, u = self._f32(f), self._f32(m), self._f32(u)
+        A, t, _, _ = _args(A, t, None, None)
+        vox = np.ascontiguousarray(vox, dtype=np.int64)
+        gi = -1.0 / f.size if gi is None else gi
+        n, gm, gu = np.zeros(vox.size), np.zeros(vox.size), np.zeros((vox.size, 3))
+        fp = C.POINTER(C.c_float)
+        fn = self._big("or_lncc_ants_voxels_f32", [fp, fp, fp, Dims, _dp, _dp, C.c_int, C.c_double, C.c_double,
+                                                   _i64p, C.c_int64, _dp, _dp, _dp])
+        fn(f.ctypes.data_as(fp), m.ctypes.data_as(fp), u.ctypes.data_as(fp), _dims_of(f.shape), _p(A), _p(t), window,
+           eps, gi, vox.ctypes.data_as(_i64p), vox.size, _p(n), _p(gm), _p(gu))
+        return dict(n=n, grad_moved=gm, g_u=gu)
+
+    def mi_hist_f32(self, f, m, u, kernel, A=None, t=None):
+        """Raw payload (joint B*B, marginals) of mi_forward_exact for (F, warped M)."""
+        f, m, u = self._f32(f), self._f32(m), self._f32(u)
+        A, t, _, _ = _args(A, t, None, None)
+        b = kernel.bins
+        raw = np.zeros(b * b + 2 * b)
+        fp = C.POINTER(C.c_float)
+        fn = self._big("or_mi_hist_f32", [fp, fp, fp, Dims, _dp, _dp, C.POINTER(Parzen), _dp])
+        fn(f.ctypes.data_as(fp), m.ctypes.data_as(fp), u.ctypes.data_as(fp), _dims_of(f.shape), _p(A), _p(t),
+           C.byref(kernel), _p(raw))
+        return raw
+
+    def mi_table(self, raw, bins, upstream=-1.0):
+        """finalize_histogram + histogram_mi + ghat (mi.hpp:181-209, 369-390): (MI, ghat)."""
+        b = bins
+        raw = _f64(raw)
+        pij, pi, pj, gh = np.zeros(b * b), np.zeros(b), np.zeros(b), np.zeros(b * b)
+        z = C.c_double()
+        mi = self.lib.or_mi_finalize(_p(raw), b, _p(pij), _p(pi), _p(pj), C.byref(z))
+        self.lib.or_mi_ghat(upstream, _p(pij), _p(pi), _p(pj), z.value, b, _p(gh))
+        return mi, gh
+
+    def mi_voxels_f32(self, f, m, u, kernel, ghat, vox, A=None, t=None):
+        """dL/dMw and g_u at the flat voxel indices `vox` given the ghat table."""
+        f, m, u = self._f32(f), self._f32(m), self._f32(u)
+        A, t, _, _ = _args(A, t, None, None)
+        vox = np.ascontiguousarray(vox, dtype=np.int64)
+        gm, gu = np.zeros(vox.size), np.zeros((vox.size, 3))
+        fp = C.POINTER(C.c_float)
+        fn = self._big("or_mi_voxels_f32", [fp, fp, fp, Dims, _dp, _dp, C.POINTER(Parzen), _dp, _i64p, C.c_int64,
+                                            _dp, _dp])
+        fn(f.ctypes.data_as(fp), m.ctypes.data_as(fp), u.ctypes.data_as(fp), _dims_of(f.shape), _p(A), _p(t),
+           C.byref(kernel), _p(_f64(ghat)), vox.ctypes.data_as(_i64p), vox.size, _p(gm), _p(gu))
+        return dict(grad_moved=gm, g_u=gu)
+
 
 class ReferenceError_(RuntimeError):
     pass

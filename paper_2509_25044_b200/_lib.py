@@ -72,6 +72,7 @@ _SIGS = {
     "ffdp_last_error": (C.c_char_p, []),
     "ffdp_abi_version": (C.c_int, []),
     "ffdp_device_check": (C.c_int, []),
+    "ffdp_scratch_trim": (C.c_int, [C.c_int64]),
     "ffdp_sampler_fwd": (C.c_int, [ImageWindow, _vp, Dims, C.POINTER(SamplerArgsC), _vp, C.c_int, _vp, _vp, _vp]),
     "ffdp_sampler_bwd": (C.c_int, [_vp, ImageWindow, _vp, Dims, C.POINTER(SamplerArgsC), C.c_int, _vp, _vp, _vp, _vp,
                                    _vp]),

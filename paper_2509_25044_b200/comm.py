@@ -181,11 +181,22 @@ class Comm:
         """ffdp_dist_step: the fused deformable step over the ranks -> (loss, g_u slabs)."""
         from . import voxreg as V
         p = params or V.LossParams()
-        if p.kind not in ("lncc", "mi") or (p.kind == "lncc" and not p.ants_approx) or \
-                (p.kind == "mi" and p.mi_approx_forward):
-            raise InvalidArgument("comm.step: the fused step runs LNCC (ANTs) and exact MI")
+        p.validate()
         for x, n in ((f, "f"), (m, "m"), (u, "u")):
             self._check(x, f"dist_step ({n})")
+        if not V.fused_step_covers(p):
+            # MSE, exact-mode LNCC, other windows, approximate MI: the reference's own
+            # composition over the collectives (registration.hpp:277-312)
+            gshape = tuple(global_shape)
+            moved = self.ring_sample(m, gshape, u, gshape, A, t)
+            if p.kind == "mse":
+                loss, gm = self.dist_mse(f, moved, gshape)
+            elif p.kind == "lncc":
+                loss, gm = self.dist_lncc(f, moved, gshape, p.window, p.epsilon, p.ants_approx)
+            else:
+                loss, gm, _ = self.dist_mi(f, moved, gshape, p.make_kernel(), p.mi_approx_forward)
+            _, g_u, _, _ = self.ring_sample_backward(gm, m, gshape, u, gshape, A, t, want=("warp",))
+            return loss, g_u
         g = [torch.empty_like(x) for x in u]
         loss = C.c_double()
         A9, t3 = _mat(A, 9), _mat(t, 3)
@@ -249,13 +260,17 @@ def comm_deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine, sch
             fs, ms, us = c.scatter(f_s), c.scatter(m_s), c.scatter(warp)
             states = [V.AdamState.zeros(x) for x in us]
             lr_norm = V.deformable_lr_norm(shape, schedule.lr)
+            scale_trace = []
             for it in range(step.iterations):
                 loss, g = c.step(fs, ms, us, shape, A, t, schedule.loss)
                 if not np.isfinite(loss):
-                    raise R.NumericalError("deformable stage diverged (non-finite loss)", trace or [])
-                if trace is not None:
-                    trace.append(R.TraceEntry(scale_index_base + s, it, loss))
+                    # the finished scales' trace only (registration.hpp:318-325)
+                    raise R.NumericalError("deformable stage diverged (non-finite loss)",
+                                           list(trace) if trace else [])
+                scale_trace.append(R.TraceEntry(scale_index_base + s, it, loss))
                 us = c.warp_update(us, g, states, lr_norm, shape, schedule.sigma_grad, schedule.sigma_warp)
+            if trace is not None:
+                trace.extend(scale_trace)
             warp = c.gather(us, fixed.device)
     if tuple(warp.shape[:3]) != tuple(fixed.shape):
         warp = R.resample_warp(warp, fixed.shape)

@@ -5,6 +5,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <mutex>
+
 #include "ffdp_common.cuh"
 
 namespace ffdp {
@@ -116,22 +118,42 @@ bool first_on_device(std::atomic<unsigned long long>& mask) {
     return !(mask.fetch_or(bit) & bit);
 }
 
-void* scratch_alloc(size_t bytes, cudaStream_t s) {
-    // Keep freed scratch cached in the device's default pool (release threshold raised
-    // once per device): with the default threshold of 0 every synchronisation hands the
-    // memory back and the next multi-GB scratch (resample_scale, the workspaces) pays a
-    // fresh mapping.
-    static std::atomic<unsigned long long> pool_mask{0};
-    if (first_on_device(pool_mask)) {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// The library's own stream-ordered pool per device (never the process's default pool, so
+// PyTorch's caching allocator and other cudaMallocAsync users keep their own behaviour).
+// Freed scratch stays cached up to kPoolKeep bytes: with a release threshold of 0 every
+// synchronisation handed multi-GB scratch (resample_scale, workspaces) back and the next
+// call paid a fresh mapping. ffdp_scratch_trim() returns the cache to the device.
+static constexpr uint64_t kPoolKeep = 4ull << 30;
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64];
+
+cudaMemPool_t device_pool(int dev) {
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
         }
+        uint64_t thr = kPoolKeep;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        g_pool[dev] = p;
     }
+    return g_pool[dev];
+}
+
+void* scratch_alloc(size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    cudaMemPool_t pool = device_pool(dev);
+    if (!pool) return nullptr;
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) {
+    if (cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, s) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
@@ -251,6 +273,15 @@ extern "C" {
 const char* ffdp_last_error(void) { return g_error; }
 
 int ffdp_abi_version(void) { return FFDP_ABI_VERSION; }
+
+int ffdp_scratch_trim(int64_t keep_bytes) {
+    int dev = 0;
+    FFDP_CHECK_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool = device_pool(dev);
+    if (!pool) return set_error(FFDP_CUDA, "scratch_trim: no memory pool on device %d", dev);
+    FFDP_CHECK_CUDA(cudaMemPoolTrimTo(pool, keep_bytes > 0 ? (size_t)keep_bytes : 0));
+    return FFDP_OK;
+}
 
 int ffdp_device_check(void) {
     int dev = -1;

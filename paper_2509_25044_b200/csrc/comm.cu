@@ -33,9 +33,9 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
-// A device allocation of one rank, stream-ordered on the rank's stream (cudaMallocAsync
-// from the device's pool, which the context keeps cached: repeated collectives reuse
-// memory instead of paying cudaMalloc / cudaFree), freed on scope exit. Every collective
+// A device allocation of one rank, stream-ordered on the rank's stream (from the library's
+// own pool of that device, device_pool, which keeps freed blocks cached: repeated
+// collectives reuse memory instead of paying cudaMalloc / cudaFree), freed on scope exit. Every collective
 // synchronises its ranks before returning, so the frees never overtake a reader.
 struct Buf {
     void* p = nullptr;
@@ -56,7 +56,8 @@ struct Buf {
         st = c->st[rank];
         cudaSetDevice(dev);
         const size_t n = std::max<size_t>(bytes, 16);
-        if (cudaMallocAsync(&p, n, st) != cudaSuccess) {
+        cudaMemPool_t pool = device_pool(dev);
+        if (!pool || cudaMallocFromPoolAsync(&p, n, pool, st) != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
             return set_error(FFDP_CUDA, "comm: device allocation of %zu bytes failed", bytes);
@@ -285,12 +286,6 @@ int ffdp_comm_create(int world, const int* devices, ffdp_comm* out) {
             return set_error(FFDP_CUDA, "comm_create: stream creation failed");
         }
         c->st.push_back(s);
-        // keep freed stream-ordered memory cached in the device's default pool
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, c->dev[r]) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
         for (int q = 0; q < r; ++q)  // NVLink peer access between distinct devices
             if (c->dev[q] != c->dev[r]) {
                 int ok = 0;

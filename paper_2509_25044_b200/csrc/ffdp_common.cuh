@@ -528,7 +528,9 @@ Geom make_geom(const ffdp_image_window& img, const ffdp_dims& out_dims, const ff
 bool valid_args(const ffdp_sampler_args& a, const char** why);
 ParzenDev make_parzen_dev(const ffdp_parzen& k);
 int num_sms();
-// Stream-ordered scratch (cudaMallocAsync); freed with scratch_free on the same stream.
+// Stream-ordered scratch from the library's own per-device pool (cudaMallocFromPoolAsync);
+// freed with scratch_free on the same stream.
+cudaMemPool_t device_pool(int dev);
 void* scratch_alloc(size_t bytes, cudaStream_t s);
 void scratch_free(void* p, cudaStream_t s);
 // true the first time it is called for the current device (per-device kernel attributes)

@@ -238,6 +238,8 @@ class ShardedStep:
         from . import voxreg
         self.V = voxreg
         self.params = params or voxreg.LossParams()
+        self.params.validate()
+        self.fused = voxreg.fused_step_covers(self.params)
         self.spec = spec
         self.A = np.eye(3) if A is None else np.asarray(A, dtype=np.float64).reshape(3, 3)
         self.t = np.zeros(3) if t is None else np.asarray(t, dtype=np.float64)
@@ -305,6 +307,8 @@ class ShardedStep:
         tensor (no host read)."""
         V, p, spec = self.V, self.params, self.spec
         u_slab = u_slab.to(torch.float32).contiguous()
+        if not self.fused:
+            return self._composite(u_slab, sync)
         u_h, lo, hi = halo_exchange(u_slab, spec, self.pad)
         nzl = spec.thickness
         ny, nx = spec.global_shape[1], spec.global_shape[2]
@@ -381,6 +385,26 @@ class ShardedStep:
                                   C.byref(k.c), V._ptr(self.ws.table), V._ptr(g_u), V._ptr(self.ws.miss), V._stream())
         lv = -self.ws.table[2 * b * b + 2 * b + 1:2 * b * b + 2 * b + 2]
         return (float(lv.item()) if sync else lv), g_u
+
+    def _composite(self, u_slab: torch.Tensor, sync: bool):
+        """The losses the fused kernels do not cover (MSE, exact-mode LNCC, windows other
+        than 7, approximate MI), composed from the collective operators exactly as the
+        reference's step does (registration.hpp:277-312): ring_sample -> dist_mse |
+        dist_lncc | dist_mi -> ring_sample_backward(want warp)."""
+        p, spec = self.params, self.spec
+        gshape = spec.global_shape
+        n_total = gshape[0] * gshape[1] * gshape[2]
+        moved = ring_sample(self.m, u_slab, self.A, self.t, gshape, spec)
+        if p.kind == "mse":
+            dl = dist_mse(self.f, moved, n_total)
+        elif p.kind == "lncc":
+            dl = dist_lncc(spec, self.f, moved, p.window, p.epsilon, p.ants_approx, True, n_total)
+        else:
+            dl = dist_mi(self.f, moved, p.bins, p.make_kernel(), p.mi_approx_forward, n_total)
+        g = ring_sample_backward(dl.grad_moved, self.m, u_slab, self.A, self.t, gshape, spec,
+                                 self.V.SamplerGradWant(warp=True))
+        loss = dl.loss if sync else torch.tensor([dl.loss], dtype=torch.float64, device=u_slab.device)
+        return loss, g.warp
 
     def verify_no_miss(self):
         """After steps run with check_miss=False: raise unless no rank saw a window miss
@@ -468,13 +492,16 @@ def sharded_deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine, 
         u = warp[sl].contiguous()
         adam = V.AdamState.zeros(u)
         lr_norm = V.deformable_lr_norm(shape, schedule.lr)
+        scale_trace = []
         for it in range(step.iterations):
             loss, g_u = st.step(u)
             if not np.isfinite(loss):
-                raise R.NumericalError("deformable stage diverged (non-finite loss)", trace or [])
-            if trace is not None:
-                trace.append(R.TraceEntry(scale_index_base + s, it, loss))
+                # the finished scales' trace only (registration.hpp:318-325)
+                raise R.NumericalError("deformable stage diverged (non-finite loss)", list(trace) if trace else [])
+            scale_trace.append(R.TraceEntry(scale_index_base + s, it, loss))
             u = sharded_warp_update(u, g_u, adam, spec, lr_norm, schedule.sigma_grad, schedule.sigma_warp)
+        if trace is not None:
+            trace.extend(scale_trace)
         warp = _gather_slabs(u, spec)
     if tuple(warp.shape[:3]) != tuple(fixed.shape):
         warp = R.resample_warp(warp, fixed.shape)

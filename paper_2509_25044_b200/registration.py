@@ -124,15 +124,15 @@ class _Scale:
         self.m = V.MovingImage(m_s)
         self.params = params
         self.ws = V.StepWorkspace(f_s.device, params.bins)
-        self.shifts = ((V.intensity_shift(f_s), V.intensity_shift(m_s)) if params.kind == "lncc" and params.ants_approx
-                       else None)
+        self.shifts = ((V.intensity_shift(f_s), V.intensity_shift(m_s)) if params.kind == "lncc" and
+                       V.fused_step_covers(params) else None)
         self.g_u = torch.empty(tuple(f_s.shape) + (3,), dtype=torch.float32, device=f_s.device)
         self.trace = torch.zeros(max(1, iterations), dtype=torch.float64, device=f_s.device)
         self.n = f_s.numel()
 
     def step(self, u, A, t, it):
         p = self.params
-        if p.kind == "mse" or (p.kind == "lncc" and not p.ants_approx) or (p.kind == "mi" and p.mi_approx_forward):
+        if not V.fused_step_covers(p):
             # operator-kernel composition (voxreg._composite_step): the loss comes back on the host
             r = V.warp_loss_step(self.f, self.m, u, A, t, p, g_u=self.g_u, ws=self.ws)
             self.trace[it] = r.loss
@@ -201,14 +201,14 @@ def deformable_stage(fixed: torch.Tensor, moving: torch.Tensor, affine=None, sch
         entries = [TraceEntry(scale_index_base + s, i, v) for i, v in enumerate(losses)]
         bad = next((i for i, v in enumerate(losses) if not np.isfinite(v)), None)
         if bad is not None:
-            if trace is not None:
-                trace.extend(entries[:bad + 1])
-            raise NumericalError("deformable stage diverged (non-finite loss)",
-                                 (trace or []) if trace is not None else entries[:bad + 1])
+            # the reference merges a scale's trace only after the scale completes
+            # (registration.hpp:318-325): the error carries the trace of the finished scales
+            raise NumericalError("deformable stage diverged (non-finite loss)", list(trace) if trace else [])
         if trace is not None:
             trace.extend(entries)
     if tuple(warp.shape[:3]) != tuple(fixed.shape):
         warp = resample_warp(warp, fixed.shape)
+    lib.ffdp_scratch_trim(0)  # the library's cached scratch goes back to the device
     return warp
 
 
@@ -272,6 +272,7 @@ def affine_stage(fixed: torch.Tensor, moving: torch.Tensor, schedule: ScaleSched
                 trace.append(TraceEntry(scale_index_base + s, it, loss))
             g = V.fused_sample_backward(gm, m_s, zero, args, want)
             params = _adam_host(params, np.concatenate([g.affine.ravel(), g.translation]), state, schedule.lr)
+    lib.ffdp_scratch_trim(0)
     return params[:9].reshape(3, 3).copy(), params[9:].copy()
 
 
@@ -280,6 +281,8 @@ def jacobian_positive_fraction(u: torch.Tensor) -> float:
     """jacobian_positive_fraction (metrics.hpp:145-176): interior voxels with
     det(I + du/dx) > 0 (central differences in normalized units)."""
     u = V._warp(u, "jacobian_positive_fraction")
+    if min(u.shape[:3]) < 3:
+        raise InvalidArgument("jacobian_positive_fraction: lattice too small")
     out = C.c_double()
     lib.ffdp_jacobian_positive(V._ptr(u), V._dims(u.shape), C.byref(out), V._stream())
     return out.value
@@ -319,6 +322,6 @@ def register_volumes(fixed: torch.Tensor, moving: torch.Tensor, config: Registra
         affine = affine_stage(f_n, m_n, config.affine, trace, 0)
         base = len(config.affine.steps)
     warp = deformable_stage(f_n, m_n, affine, config.deformable, config.deformable_opts, trace, base)
-    jac = jacobian_positive_fraction(warp) if min(warp.shape[:3]) >= 3 else 1.0
+    jac = jacobian_positive_fraction(warp)  # throws for lattices under 3 voxels (metrics.hpp:146-148)
     torch.cuda.synchronize()
     return RegistrationResult(affine, warp, trace, time.perf_counter() - t0, jac)

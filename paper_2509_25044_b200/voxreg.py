@@ -562,6 +562,27 @@ class LossParams:
     def make_kernel(self) -> ParzenKernel:
         return ParzenKernel.bspline3(self.bins) if self.mi_bspline_kernel else ParzenKernel.gaussian(self.bins)
 
+    def validate(self):
+        """The reference's checks for the loss arguments (lncc.hpp:57-61, mi.hpp:170-176)."""
+        if self.kind not in ("lncc", "mi", "mse"):
+            raise InvalidArgument(f"unknown loss kind {self.kind!r}")
+        if self.kind == "lncc" and (self.window < 1 or self.window % 2 == 0):
+            raise InvalidArgument("lncc: window must be odd and >= 1")
+        if self.kind == "mi" and self.bins < 2:
+            raise InvalidArgument("mi: bins must be >= 2")
+
+
+def fused_step_covers(params: "LossParams") -> bool:
+    """True when the fused step kernels (ffdp_step_lncc: window 7, ANTs; ffdp_step_mi:
+    exact Parzen forward) compute this loss; every other loss (MSE, exact-mode LNCC, other
+    windows, approximate MI) is composed from the operator kernels exactly as the
+    reference composes it (sample -> loss -> sampler backward)."""
+    if params.kind == "lncc":
+        return params.ants_approx and params.window == 7
+    if params.kind == "mi":
+        return not params.mi_approx_forward
+    return False
+
 
 @dataclass
 class StepResult:
@@ -637,8 +658,8 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
         raise InvalidArgument("warp_loss_step: F and M must share a lattice (registration.hpp:268-270)")
     win = mi.window()
     ws.miss.zero_()
-    if params.kind == "mse" or (params.kind == "lncc" and not params.ants_approx) or \
-            (params.kind == "mi" and params.mi_approx_forward):
+    params.validate()
+    if not fused_step_covers(params):
         return _composite_step(f, win, u, ca, params, g_u, ws, sync)
     if params.kind == "lncc":
         if shifts is None:

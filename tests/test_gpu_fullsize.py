@@ -9,7 +9,7 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from gpu_util import host, maxrel, need_gpu
+from gpu_util import host, l2rel, maxrel, need_gpu
 
 pytestmark = pytest.mark.gpu
 
@@ -142,3 +142,95 @@ def test_mi256_matches_oracle(V, orc):
     r = V.warp_loss_step(T(si.f), T(si.m), T(si.u), si.A, si.t, V.LossParams(kind="mi", mi_bspline_kernel=True))
     assert abs(r.loss / ref["loss"] - 1) <= 1e-5
     assert maxrel(host(r.g_u), ref["g_u"]) <= 1e-4
+
+
+def _sample_voxels(shape, n, seed):
+    """n random flat voxel indices plus the 8 corners and face-centre voxels (zero-padded
+    windows) of a (nz, ny, nx) lattice."""
+    nz, ny, nx = shape
+    rng = np.random.default_rng(seed)
+    v = rng.integers(0, nz * ny * nx, n)
+    edge = [(z, y, x) for z in (0, nz // 2, nz - 1) for y in (0, ny // 2, ny - 1) for x in (0, nx // 2, nx - 1)]
+    e = np.array([(z * ny + y) * nx + x for z, y, x in edge], dtype=np.int64)
+    return np.unique(np.concatenate([v, e]))
+
+
+def _host32(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("jitter", ["bench", "survey"])
+def test_lncc720_matches_fp64(V, orc, jitter):
+    """BASELINE configs[2] (720x640x720 LNCC, window 7, ANTs) against the fp64 restatement:
+    g_u at 20k sampled voxels (each depends only on its 7^3 window and gi = -1/N, so the
+    per-voxel oracle is exact there) and the loss from one whole-volume fp64 sum of n_i
+    (oracle/ffdp_oracle_big.c, OpenMP). jitter 'survey' is SURVEY 8(d)'s U(-0.01, 0.01)
+    normalized jitter (+-3.6 voxels at 720); 'bench' the bench's +-0.01 voxel."""
+    import torch
+    import bench
+    f, m, u, A, t = bench.synth_inputs((720, 640, 720), "lncc", 1234, "cuda", jitter=jitter)
+    res = V.warp_loss_step(f, m, u, A, t, V.LossParams(kind="lncc"))
+    assert res.window_misses == 0
+    loss = res.loss
+    vox = _sample_voxels(f.shape, 20000, 5)
+    gu = res.g_u.view(-1, 3)[torch.from_numpy(vox).cuda()].double().cpu().numpy()
+    del res
+    hf, hm, hu = _host32(f), _host32(m), _host32(u)
+    del f, m, u
+    torch.cuda.empty_cache()
+    r = orc.lncc_ants_voxels_f32(hf, hm, hu, vox, A, t)
+    grel = maxrel(gu, r["g_u"])
+    loss_ref = 1.0 - orc.lncc_sum_n_f32(hf, hm, hu, A, t) / hf.size
+    lrel = abs(loss - loss_ref) / abs(loss_ref)
+    print(f"lncc720 ({jitter} jitter) vs fp64: loss {loss:.10f} ref {loss_ref:.10f} rel {lrel:.2e}; "
+          f"g_u maxrel {grel:.2e} l2rel {l2rel(gu, r['g_u']):.2e} over {vox.size} voxels")
+    assert lrel <= 1e-5
+    assert grel <= 1e-4
+
+
+def test_mi1760_matches_fp64(V, orc):
+    """BASELINE configs[4] (1760x1760x1200 = 3.7 G voxels, B-spline MI, 32 bins) on one
+    B200: the joint histogram / loss against one fp64 histogram of the whole volume and
+    g_u at 20k sampled voxels against the per-voxel fp64 backward with the fp64 ghat
+    table (oracle/ffdp_oracle_big.c). Needs ~75 GB of host memory for the inputs."""
+    import psutil
+    import torch
+    import bench
+    if psutil.virtual_memory().available < (100 << 30):
+        pytest.skip("needs ~100 GB of free host memory for the 3.7 G-voxel inputs")
+    if torch.cuda.get_device_properties(0).total_memory < (150 << 30):
+        pytest.skip("needs a 180 GB B200")
+    shape = (1200, 1760, 1760)
+    f, m, u, A, t = bench.synth_inputs(shape, "mi", 1234, "cuda")
+    ws = V.StepWorkspace(f.device, 32)
+    g_u = torch.empty_like(u)
+    import ctypes as C
+    from paper_2509_25044_b200._lib import lib
+    k = V.ParzenKernel.bspline3(32)
+    mimg = V.MovingImage(m)
+    args = V.SamplerArgs(A=A, t=t).to_c()
+    # the record-free step (the 16 B/voxel records do not fit beside 3.7 G voxels)
+    lib.ffdp_step_mi(V._ptr(f), V._ptr(u), V._dims(f.shape), V._full_slab(shape[0]), mimg.window(), C.byref(args),
+                     C.byref(k.c), V._ptr(ws.raw), V._ptr(ws.table), V._ptr(g_u), V._ptr(ws.scratch), None,
+                     V._ptr(ws.miss), V._stream())
+    torch.cuda.synchronize()
+    assert int(ws.miss.item()) == 0
+    loss = -float(ws.table[2 * 32 * 32 + 2 * 32 + 1].item())
+    vox = _sample_voxels(shape, 20000, 6)
+    gu = g_u.view(-1, 3)[torch.from_numpy(vox).cuda()].double().cpu().numpy()
+    del g_u, mimg, ws
+    hf, hu = _host32(f), _host32(u)
+    del f, u
+    hm = _host32(m)
+    del m
+    torch.cuda.empty_cache()
+    kc = orc.parzen("bspline3", 32)
+    raw = orc.mi_hist_f32(hf, hm, hu, kc, A, t)
+    mi, gh = orc.mi_table(raw, 32)
+    r = orc.mi_voxels_f32(hf, hm, hu, kc, gh, vox, A, t)
+    lrel = abs(loss + mi) / abs(mi)
+    grel = maxrel(gu, r["g_u"])
+    print(f"mi1760 vs fp64: loss {loss:.10f} ref {-mi:.10f} rel {lrel:.2e}; g_u maxrel {grel:.2e} "
+          f"l2rel {l2rel(gu, r['g_u']):.2e} over {vox.size} voxels")
+    assert lrel <= 1e-5
+    assert grel <= 1e-4

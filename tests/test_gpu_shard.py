@@ -115,3 +115,44 @@ def test_window_miss_is_reported_and_exact_when_wide(V, orc):
     assert miss == 0
     full = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, shifts=(0.5, 0.5))
     assert maxrel(host(g_wide), host(full.g_u)[lo:hi]) < 2e-5
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_mi_slabs_straddle_fixed_point_switch(V, orc, world):
+    """The whole 48x64x64 volume (196608 voxels >= 2^17) runs pass 1 on the 2^-21
+    fixed-point grid; its 2-rank slabs (98304 voxels) on the 2^-23 grid and its 4-rank slabs
+    (49152 < 2^16) on the scalar kernels (step_mi.cu). The sharded step changes arithmetic
+    with H, so it is gated against the single-GPU step and the oracle at the north-star
+    tolerances instead of bit equality."""
+    import torch
+    from oracle import step_inputs
+    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200._lib import lib
+    si = step_inputs(orc, (48, 64, 64), seed=4242, loss="mi")
+    nz, b = si.f.shape[0], 32
+    ref = orc.step_mi(si.f, si.m, si.u, orc.parzen("bspline3", b), si.A, si.t)
+    full = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t,
+                            V.LossParams(kind="mi", bins=b, mi_bspline_kernel=True))
+    raws, ctx = [], []
+    for lo, hi in D.shard_ranges(nz, world):
+        raw, c_, miss = run_slab(V, si, lo, hi, nz, 0, "mi", (0, nz))
+        assert miss == 0
+        raws.append(raw)
+        ctx.append(c_)
+    raw = sum(raws)
+    table = torch.empty(2 * b * b + 2 * b + 4, dtype=torch.float64, device="cuda")
+    lib.ffdp_mi_finalize(V._ptr(raw), b, -1.0, V._ptr(table), V._stream())
+    parts = []
+    for fb, ub, slab, win, args, k, g_u, mp in ctx:
+        lib.ffdp_step_mi_grad(V._ptr(fb), V._ptr(ub), V._dims(fb.shape), slab, win, C.byref(args), C.byref(k.c),
+                              V._ptr(table), V._ptr(g_u), None, V._stream())
+        parts.append(host(g_u))
+    loss = -float(table[2 * b * b + 2 * b + 1].item())
+    gu = np.concatenate(parts, axis=0)
+    print(f"mi straddle H={world}: loss vs 1 GPU {abs(loss / full.loss - 1):.2e}, vs oracle "
+          f"{abs(loss / ref['loss'] - 1):.2e}; g_u vs 1 GPU {maxrel(gu, host(full.g_u)):.2e}, vs oracle "
+          f"{maxrel(gu, ref['g_u']):.2e}")
+    assert loss == pytest.approx(full.loss, rel=1e-5)
+    assert loss == pytest.approx(ref["loss"], rel=1e-5)
+    assert maxrel(gu, host(full.g_u)) < 1e-4
+    assert maxrel(gu, ref["g_u"]) < 1e-4

@@ -174,3 +174,15 @@ def test_step_ragged_and_thin_lattices(V, orc, shape, loss):
     res = V.warp_loss_step(dev(f), dev(m), dev(u), A, t, p)
     assert res.loss == pytest.approx(ref["loss"], rel=1e-5, abs=1e-7)
     assert maxrel(host(res.g_u), ref["g_u"]) <= 1e-4
+
+
+@pytest.mark.parametrize("window", [3, 5, 9])
+def test_step_lncc_other_windows(V, orc, window):
+    """windows other than 7 (the fused kernel's) run the operator composition
+    with the reference's semantics, at the parity gates."""
+    from oracle import step_inputs
+    si = step_inputs(orc, (24, 26, 28), seed=4242, loss="lncc")
+    ref = orc.step_lncc(si.f, si.m, si.u, si.A, si.t, window=window)
+    res = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u), si.A, si.t, V.LossParams(kind="lncc", window=window))
+    assert res.loss == pytest.approx(ref["loss"], rel=LOSS_RTOL)
+    assert maxrel(host(res.g_u), ref["g_u"]) <= GRAD_MAXREL
