@@ -38,7 +38,9 @@ WORKLOADS = {
     "lncc1024": ((1024, 1024, 1024), "lncc", 3),
     "mi1760": ((1200, 1760, 1760), "mi", 4),
 }
-BYTES_PER_VOXEL = {"lncc": 32, "mi": 52}  # algorithmic bytes per output voxel
+BYTES_PER_VOXEL = {"lncc": 32, "mi": 52}
+DTYPE = {"lncc": "f32 (fp64 coordinates; exact int32 box sums of 2^-21 fixed-point moments)",
+         "mi": "f32 (fp64 coordinates; integer fixed-point histogram)"}  # algorithmic bytes per output voxel
 METRIC = "Gvoxel/s of fused warp+loss fwd+bwd step (1–8 B200), % of HBM roofline"
 
 
@@ -217,10 +219,16 @@ class Stepper:
         self.win = self.mimg.window()
         self.dims = voxreg._dims(f.shape)
         if loss == "lncc":
-            self.shifts = (voxreg.intensity_shift(f), voxreg.intensity_shift(m))
-            # two-pass step (workspace) unless FFDP_LNCC_FUSED=1 selects the single fused pass
-            self._lws = (None if os.environ.get("FFDP_LNCC_FUSED") == "1"
-                         else self._p(self.ws.lncc_workspace(self.dims, self.slab)))
+            # the one-pass fused step (default) or the round-1 two-pass form (comparison)
+            self.twopass = os.environ.get("FFDP_LNCC_IMPL") == "twopass"
+            if self.twopass:
+                self.shifts = (voxreg.intensity_shift(f), voxreg.intensity_shift(m))
+                n = int(lib.ffdp_step_lncc_passes_workspace_bytes(self.dims, self.slab)) // 4
+                self._lws_t = torch.empty(n, dtype=torch.float32, device=f.device)
+                self._lws = self._p(self._lws_t)
+            else:
+                self.ranges = voxreg.intensity_ranges(f, m)
+                self._lws = self._p(self.ws.lncc_workspace(self.dims, self.slab))
         else:
             self.kernel = voxreg.ParzenKernel.bspline3(bins)
             # the pass-1 records (16 B/voxel) when they fit next to the step's buffers; else
@@ -230,7 +238,7 @@ class Stepper:
         self.kernel_ms = {}
         # lncc: sample, moments, partial-sum reduction (fused: 1); mi: pass 1 (finalize fused
         # into its last CTA) and pass 2 (memsets of the histogram are not kernels of ours)
-        self.launches_per_step = ((1 if self._lws is None else 3) if loss == "lncc" else
+        self.launches_per_step = ((3 if self.twopass else 2) if loss == "lncc" else
                                   2 if self.use_rec else 4)
 
     def _p(self, t):
@@ -245,16 +253,21 @@ class Stepper:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
         if self.loss == "lncc":
             self.ws.sum_n.zero_()
+            if not self.twopass:
+                if record:
+                    ev[0].record()
+                lib.ffdp_step_lncc(self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args),
+                                   7, 1e-5, -1.0 / self.n, self._p(self.ranges), self._p(self.g_u),
+                                   self._p(self.ws.sum_n), None, self._lws, s)
+                if not record:
+                    return None
+                ev[1].record()
+                return [("k_lncc_fused", ev[0], ev[1])]
             a = (self._p(self.f), self._p(self.u), self.dims, self.slab, self.win, C.byref(self.args), 7, 1e-5,
                  -1.0 / self.n, self.shifts[0], self.shifts[1], self._p(self.g_u), self._p(self.ws.sum_n), None)
             if not record:
-                lib.ffdp_step_lncc(*a, self._lws, s)
+                lib.ffdp_step_lncc_passes(*a, self._lws, 3, s)
                 return None
-            if self._lws is None:  # the single fused pass
-                ev[0].record()
-                lib.ffdp_step_lncc(*a, None, s)
-                ev[1].record()
-                return [("k_step_lncc", ev[0], ev[1])]
             ev[0].record()
             lib.ffdp_step_lncc_passes(*a, self._lws, 1, s)
             ev[1].record()
@@ -306,6 +319,13 @@ class Stepper:
             self.step()
         torch.cuda.synchronize()
         return g
+
+    def new_pair(self):
+        if self.loss == "lncc" and not self.twopass:
+            lib, V, C = self.lib, self.V, self.C
+            lib.ffdp_minmax(self._p(self.f), self.f.numel(), self._p(self.ranges), V._stream())
+            pm = self.mimg.padded
+            lib.ffdp_minmax(self._p(pm), pm.numel(), C.c_void_p(self.ranges.data_ptr() + 8), V._stream())
 
     def loss_value(self):
         if self.loss == "lncc":
@@ -385,7 +405,7 @@ def run_sharded(args, rank, world, local_rank, dev):
     return {
         "metric": METRIC, "value": round(value, 3), "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (fp64 coordinates / moment sums)", "data": "synthetic",
+        "vs_baseline": None, "dtype": DTYPE[loss], "data": "synthetic",
         "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}] per GPU, weak scaling",
                    "volume": "x".join(str(s) for s in gshape[::-1]), "loss": loss, "voxels_per_gpu": nloc,
                    "parallelism": f"z-slab x{world} ({dist.get_backend()} halo + allreduce)",
@@ -453,8 +473,9 @@ def run_ours(args, rank, world, local_rank):
     loss_val = st.loss_value()
 
     # dominant kernel roofline (algorithmic bytes per launch / live event duration)
-    if loss == "lncc" and "k_step_lncc" in kern_ms:
-        dom, dom_bytes = "k_step_lncc", 32 * nvox
+    if loss == "lncc" and "k_lncc_fused" in kern_ms:
+        # the one-pass step: the kernel IS the step (32 algorithmic B/voxel: F, u, M, g_u)
+        dom, dom_bytes = "k_lncc_fused", 32 * nvox
     elif loss == "lncc":
         # two passes: algorithmic bytes of the step (32 B/voxel: read F, u, M once, write
         # g_u) split as pass 1 reads u + M (16 B), pass 2 reads F and writes g_u (16 B)
@@ -473,7 +494,7 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (fp64 coordinates / moment differences)", "data": "synthetic",
+        "vs_baseline": None, "dtype": DTYPE[loss], "data": "synthetic",
         "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}]",
                    "volume": "x".join(str(s) for s in shape[::-1]), "loss": loss,
                    "u_jitter": ("SURVEY 8(d): U(-0.01, 0.01) normalized" if jitter == "survey" else
@@ -658,6 +679,7 @@ def run_e2e(args, st, f, m, u, A, t, loss, world):
         cp(st.f, hf)
         cp(st.mimg.interior, hm)  # H2D straight into the bordered layout
         cp(st.u, hu)
+        st.new_pair()  # a new (F, M) pair: the LNCC intensity frame is re-derived on the device
         st.step()
         host_loss = st.loss_value()  # D2H read of the step result (8 bytes)
     e1.record()

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define FFDP_ABI_VERSION 1
+#define FFDP_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define FFDP_API __attribute__((visibility("default")))
@@ -276,41 +276,46 @@ FFDP_API int ffdp_mi_bwd(const float* vi, const float* vj, int64_t n, const ffdp
 /* ------------------------------------------------------------- fused step (★) */
 
 /*
- * The deformable step's hot path (registration.hpp:277-312) for LNCC in ANTs mode:
- * Mw = fused_sample(M, u) for the slab + 3 halo planes, the five LNCC moments, dL/dMw
- * (lncc.hpp:226-280 with ants_approx), and g_u = fused_sample_backward(dL/dMw)
- * (sampler.hpp:221-230).
+ * The deformable step's hot path (registration.hpp:277-312) for LNCC in ANTs mode, in one
+ * streaming pass: Mw = fused_sample(M, u) for the slab + 3 halo planes, the five LNCC
+ * window moments (lncc_forward_fused, lncc.hpp:144-205), dL/dMw (lncc_backward_fused with
+ * ants_approx, lncc.hpp:226-280) and g_u = fused_sample_backward(dL/dMw, want warp)
+ * (sampler.hpp:221-230); only g_u is written.
  *   f, u: buffers described by `slab` (halo planes of radius window/2 included);
  *   g_u: interior planes only (3 floats per voxel);
  *   args: the sampler arguments of the GLOBAL output lattice (buf_dims.nx, buf_dims.ny,
  *     slab.nz_global); voxels are addressed by global lattice index, which is the
  *     ring sampler's per-shard rescale (distops.hpp:120-133) folded into one frame;
  *   gi: dL/dn_i (-1/N_total for the deformable step);
- *   shift_f, shift_m: intensity shifts for the moment accumulation (any value is exact
- *     up to rounding; the mid-range of the data is most accurate);
- *   sum_n: device double, += sum of n_i over the slab interior;
- *   workspace: device buffer of ffdp_step_lncc_workspace_bytes: the step runs as two
- *     streaming passes (warp every voxel once, then the moments), or NULL:
- *     one fused pass that re-samples the warp on every tile halo.
+ *   ranges: device float[4] {F min, F max, M min, M max}: the value ranges of the fixed
+ *     and moving volumes (ffdp_minmax; allreduced over the shards when sharded, so every
+ *     rank uses the same intensity frame). They bound the exact fixed-point moment sums;
+ *     values outside them are an error the kernel does not detect. NULL: computed here on
+ *     every call (one extra read of F and of the moving window);
+ *   sum_n: device double, += sum of n_i over the slab interior (fixed order: the loss is
+ *     bit-reproducible);
+ *   workspace: device buffer of ffdp_step_lncc_workspace_bytes bytes, or NULL for a
+ *     stream-ordered allocation per call (pass one to capture the step in a CUDA graph).
  */
 FFDP_API int ffdp_step_lncc(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab, ffdp_image_window m,
-                   const ffdp_sampler_args* args, int window, double eps, double gi, float shift_f, float shift_m,
+                   const ffdp_sampler_args* args, int window, double eps, double gi, const float* ranges,
                    float* g_u, double* sum_n, int32_t* miss, void* workspace, void* stream);
 
+/* Bytes of the LNCC step workspace: 4 floats of ranges, one double per CTA. */
+FFDP_API int64_t ffdp_step_lncc_workspace_bytes(ffdp_dims buf_dims, ffdp_slab slab);
+
 /*
- * The two passes of ffdp_step_lncc with a workspace, separately (e.g. to time them, or
- * to overlap the warp pass with communication): passes = 1 runs the warp sampling
- * (Mw, dMw/du into the workspace; reads u, M), 2 the moments, dL/dMw and g_u (reads F
- * and the workspace; adds to sum_n), 3 both. Arguments as ffdp_step_lncc.
+ * The round-1 two-pass form of the same step, kept for comparison (bench.py
+ * --lncc-impl twopass): pass 1 warps every voxel once into an HBM workspace (Mw, dMw/du),
+ * pass 2 runs the moments from it (moments in fp32 / fp64 around the intensity shifts
+ * shift_f, shift_m). passes = 1, 2 or 3 (both). workspace:
+ * ffdp_step_lncc_passes_workspace_bytes (required).
  */
 FFDP_API int ffdp_step_lncc_passes(const float* f, const float* u, ffdp_dims buf_dims, ffdp_slab slab,
                                    ffdp_image_window m, const ffdp_sampler_args* args, int window, double eps,
                                    double gi, float shift_f, float shift_m, float* g_u, double* sum_n, int32_t* miss,
                                    void* workspace, int passes, void* stream);
-
-/* Bytes of the two-pass LNCC workspace: Mw for the buffer planes, dMw/du for the interior,
- * one double per CTA for the fixed-order loss reduction. */
-FFDP_API int64_t ffdp_step_lncc_workspace_bytes(ffdp_dims buf_dims, ffdp_slab slab);
+FFDP_API int64_t ffdp_step_lncc_passes_workspace_bytes(ffdp_dims buf_dims, ffdp_slab slab);
 
 /*
  * Fused MI step, pass 1 (registration.hpp:278-299 with dist_mi, distops.hpp:355-373):

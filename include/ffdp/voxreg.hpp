@@ -549,14 +549,10 @@ class DeformableStep {
         miss_ = DeviceArray<std::int32_t>(1);
         sum_ = DeviceArray<double>(1);
         if (p.kind == LossKind::lncc) {
-            DeviceArray<float> mm(2);
-            check(ffdp_minmax(fixed.data.data(), d.voxels(), mm.data(), s));
-            std::vector<float> a = mm.download(s);
-            shift_f_ = 0.5f * (a[0] + a[1]);
-            check(ffdp_minmax(moving.data.data(), d.voxels(), mm.data(), s));
-            a = mm.download(s);
-            shift_m_ = 0.5f * (a[0] + a[1]);
-            // two-pass step: every voxel warped once, then the moments
+            // the step's intensity frame: value ranges of F and M, fixed while F and M are
+            ranges_ = DeviceArray<float>(4);
+            check(ffdp_minmax(fixed.data.data(), d.voxels(), ranges_.data(), s));
+            check(ffdp_minmax(moving.data.data(), d.voxels(), ranges_.data() + 2, s));
             lws_ = DeviceArray<unsigned char>(
                 static_cast<std::size_t>(ffdp_step_lncc_workspace_bytes(d.c(), full_slab(d.nz))));
         } else {
@@ -582,7 +578,7 @@ class DeformableStep {
         if (p_.kind == LossKind::lncc) {
             sum_.zero(stream_);
             check(ffdp_step_lncc(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, p_.window, p_.epsilon,
-                                 -1.0 / static_cast<double>(dims_.voxels()), shift_f_, shift_m_, g_u.data.data(),
+                                 -1.0 / static_cast<double>(dims_.voxels()), ranges_.data(), g_u.data.data(),
                                  sum_.data(), miss_.data(), lws_.data(), stream_));
         } else {
             check(ffdp_step_mi(f_, u.data.data(), dims_.c(), full_slab(dims_.nz), w, &a, &kernel_->c(), raw_.data(),
@@ -618,10 +614,9 @@ class DeformableStep {
     DeviceArray<float> m_pad_;
     DeviceArray<std::int32_t> miss_;
     DeviceArray<double> sum_, raw_, table_;
-    DeviceArray<float> rec_;
+    DeviceArray<float> rec_, ranges_;
     DeviceArray<unsigned char> scratch_, lws_;
     std::optional<ParzenKernel> kernel_;
-    float shift_f_ = 0, shift_m_ = 0;
 };
 
 

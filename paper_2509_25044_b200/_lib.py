@@ -90,11 +90,12 @@ _SIGS = {
     "ffdp_mi_finalize": (C.c_int, [_vp, C.c_int, C.c_double, _vp, _vp]),
     "ffdp_mi_bwd": (C.c_int, [_vp, _vp, C.c_int64, C.POINTER(ParzenC), _vp, _vp, _vp, _vp]),
     "ffdp_step_lncc": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.c_int, C.c_double,
-                                 C.c_double, C.c_float, C.c_float, _vp, _vp, _vp, _vp, _vp]),
+                                 C.c_double, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ffdp_step_lncc_workspace_bytes": (C.c_int64, [Dims, Slab]),
     "ffdp_step_lncc_passes": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.c_int,
                                         C.c_double, C.c_double, C.c_float, C.c_float, _vp, _vp, _vp, _vp, C.c_int,
                                         _vp]),
+    "ffdp_step_lncc_passes_workspace_bytes": (C.c_int64, [Dims, Slab]),
     "ffdp_step_mi_hist": (C.c_int, [_vp, _vp, Dims, Slab, ImageWindow, C.POINTER(SamplerArgsC), C.POINTER(ParzenC),
                                     _vp, _vp, _vp, _vp]),
     "ffdp_step_mi_workspace_bytes": (C.c_int64, [C.c_int]),
@@ -169,7 +170,8 @@ class _Lib:
         lib = self.load()
         fn = getattr(lib, name)
         if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check", "ffdp_step_mi_workspace_bytes",
-                    "ffdp_step_mi_record_bytes", "ffdp_step_lncc_workspace_bytes", "ffdp_comm_world",
+                    "ffdp_step_mi_record_bytes", "ffdp_step_lncc_workspace_bytes",
+                    "ffdp_step_lncc_passes_workspace_bytes", "ffdp_comm_world",
                     "ffdp_comm_device"):
             return fn
 

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["capi.cu", "sampler.cu", "lncc.cu", "mi.cu", "step_lncc.cu", "step_lncc2.cu", "step_mi.cu", "smooth.cu", "resample.cu", "comm.cu"]
+SOURCES = ["capi.cu", "sampler.cu", "lncc.cu", "mi.cu", "step_lncc.cu", "step_lncc2.cu", "step_lncc3.cu", "step_mi.cu", "smooth.cu", "resample.cu", "comm.cu"]
 LIB = os.path.join(HERE, "libffdp.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared"]

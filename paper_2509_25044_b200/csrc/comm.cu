@@ -706,11 +706,10 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
         }
         COMM_TRY(sync_all(c));
     }
-    // LNCC moment shifts: the mid-ranges of F and M over all ranks (part of the arithmetic,
-    // identical on every rank)
-    float sf = 0.f, sm = 0.f;
+    // LNCC intensity frame: the value ranges of F and M over all ranks (identical on every
+    // rank), reduced on the device in rank order and broadcast back by peer copies
+    std::vector<Buf> mm((size_t)w);
     if (lncc) {
-        std::vector<Buf> mm((size_t)w);
         for (int r = 0; r < w; ++r) {
             COMM_TRY(mm[(size_t)r].alloc(c, r, 4 * sizeof(float), false));
             COMM_TRY(ffdp_minmax(f[r], plane * sh[(size_t)r].th(), mm[(size_t)r].as<float>(), c->st[r]));
@@ -726,8 +725,10 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
             g4[0] = std::min(g4[0], v[0]), g4[1] = std::max(g4[1], v[1]);
             g4[2] = std::min(g4[2], v[2]), g4[3] = std::max(g4[3], v[3]);
         }
-        sf = (float)(0.5 * ((double)g4[0] + (double)g4[1]));
-        sm = (float)(0.5 * ((double)g4[2] + (double)g4[3]));
+        for (int r = 0; r < w; ++r) {
+            cudaSetDevice(c->dev[r]);
+            FFDP_CHECK_CUDA(cudaMemcpy(mm[(size_t)r].p, g4, sizeof(g4), cudaMemcpyHostToDevice));
+        }
     }
     const int B = lncc ? 0 : kernel->bins;
     const int64_t nraw = lncc ? 1 : (int64_t)B * B + 2 * B;
@@ -748,7 +749,8 @@ int ffdp_dist_step(ffdp_comm c, int loss_kind, const float* const* f, const floa
         if (lncc) {
             COMM_TRY(ws[(size_t)r].alloc(c, r, (size_t)ffdp_step_lncc_workspace_bytes(bd, sl), false));
             COMM_TRY(ffdp_step_lncc(fh[(size_t)r].as<float>(), uh[(size_t)r].as<float>(), bd, sl, iw, &ga, window, eps,
-                                    -1.0 / (double)n_total, sf, sm, g_u[r], red[(size_t)r].as<double>(),
+                                    -1.0 / (double)n_total, mm[(size_t)r].as<float>(), g_u[r],
+                                    red[(size_t)r].as<double>(),
                                     miss[(size_t)r].as<int32_t>(), ws[(size_t)r].p, c->st[r]));
         } else {
             COMM_TRY(ws[(size_t)r].alloc(c, r, (size_t)ffdp_step_mi_workspace_bytes(B), true));

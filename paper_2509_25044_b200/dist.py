@@ -251,18 +251,18 @@ class ShardedStep:
         self.margin = int(margin_planes)
         self.m_z0 = self.m_z1 = None
         self.window_fetches = 0
-        self.shifts = None
+        self.ranges = None
 
     def reload(self, f_slab: torch.Tensor = None, m_slab: torch.Tensor = None):
         """New image contents of the same geometry (a new pair, or a new scale's resampled
-        images): refreshes the F halo planes, drops the moving window and the moment shift."""
+        images): refreshes the F halo planes, drops the moving window and the intensity ranges."""
         if f_slab is not None:
             self.f.copy_(f_slab)
             self.f_halo, self.hlo, self.hhi = halo_exchange(self.f, self.spec, self.pad)
         if m_slab is not None:
             self.m.copy_(m_slab)
         self.m_z0 = self.m_z1 = None
-        self.shifts = None
+        self.ranges = None
 
     # -- moving window ------------------------------------------------------------------
     def _ensure_window(self, z0: int, z1: int):
@@ -320,14 +320,12 @@ class ShardedStep:
         if self.m_z0 is None:
             a, b = self._affine_z_range(spec.lo - lo, spec.hi + hi)
             self._ensure_window(a - self.margin, b + self.margin)
-        if p.kind == "lncc" and self.shifts is None:
-            # the moment shift must be the same on every rank (it is part of the arithmetic)
-            mm = torch.tensor([self.f.min(), -self.f.max(), self.m.min(), -self.m.max()], dtype=torch.float64,
-                              device=self.f.device)
+        if p.kind == "lncc" and self.ranges is None:
+            # one intensity frame on every rank (it fixes the fixed-point moment arithmetic)
+            mm = torch.stack([self.f.min(), -self.f.max(), self.m.min(), -self.m.max()]).to(torch.float32)
             if spec.world > 1:
                 all_reduce(mm, op=dist.ReduceOp.MIN)
-            v = mm.tolist()
-            self.shifts = (0.5 * (v[0] - v[1]), 0.5 * (v[2] - v[3]))
+            self.ranges = mm * torch.tensor([1.0, -1.0, 1.0, -1.0], device=mm.device)
         from ._lib import lib
         for attempt in range(max_retries + 1):
             if check_miss:
@@ -337,7 +335,7 @@ class ShardedStep:
             if p.kind == "lncc":
                 self.ws.sum_n.zero_()
                 lib.ffdp_step_lncc(V._ptr(self.f_halo), V._ptr(u_h), dims, slab, win, C.byref(args), p.window,
-                                   p.epsilon, -1.0 / n_total, self.shifts[0], self.shifts[1], V._ptr(g_u),
+                                   p.epsilon, -1.0 / n_total, V._ptr(self.ranges), V._ptr(g_u),
                                    V._ptr(self.ws.sum_n), V._ptr(self.ws.miss),
                                    V._ptr(self.ws.lncc_workspace(dims, slab)), stream)
             else:

@@ -124,8 +124,9 @@ class _Scale:
         self.m = V.MovingImage(m_s)
         self.params = params
         self.ws = V.StepWorkspace(f_s.device, params.bins)
-        self.shifts = ((V.intensity_shift(f_s), V.intensity_shift(m_s)) if params.kind == "lncc" and
-                       V.fused_step_covers(params) else None)
+        # the LNCC step's intensity frame: fixed per scale (F_s and M_s are static within it)
+        self.ranges = (V.intensity_ranges(f_s, m_s) if params.kind == "lncc" and V.fused_step_covers(params)
+                       else None)
         self.g_u = torch.empty(tuple(f_s.shape) + (3,), dtype=torch.float32, device=f_s.device)
         self.trace = torch.zeros(max(1, iterations), dtype=torch.float64, device=f_s.device)
         self.n = f_s.numel()
@@ -137,7 +138,7 @@ class _Scale:
             r = V.warp_loss_step(self.f, self.m, u, A, t, p, g_u=self.g_u, ws=self.ws)
             self.trace[it] = r.loss
             return self.g_u
-        V.warp_loss_step(self.f, self.m, u, A, t, self.params, g_u=self.g_u, ws=self.ws, shifts=self.shifts,
+        V.warp_loss_step(self.f, self.m, u, A, t, self.params, g_u=self.g_u, ws=self.ws, ranges=self.ranges,
                          sync=False)
         if self.params.kind == "lncc":
             # loss = 1 - sum_n / N (dist_lncc, distops.hpp:309-318)

@@ -606,8 +606,8 @@ class StepWorkspace:
         self._lncc = None
 
     def lncc_workspace(self, dims: Dims, slab: Slab) -> torch.Tensor:
-        """Workspace of the two-pass LNCC step (Mw of the buffer planes, dMw/du of the
-        interior), kept across steps of the same lattice."""
+        """Workspace of the fused LNCC step (value ranges, one loss partial per CTA), kept
+        across steps of the same lattice."""
         n = int(lib.ffdp_step_lncc_workspace_bytes(dims, slab)) // 4
         if self._lncc is None or self._lncc.numel() < n:
             self._lncc = torch.empty(n, dtype=torch.float32, device=self.device)
@@ -622,6 +622,17 @@ class StepWorkspace:
         return self._rec
 
 
+def intensity_ranges(f: torch.Tensor, m: torch.Tensor) -> torch.Tensor:
+    """Device float[4] {F min, F max, M min, M max} (ffdp_minmax, no host read): the value
+    ranges that fix the LNCC step's intensity frame (ffdp_step_lncc `ranges`)."""
+    out = torch.empty(4, dtype=torch.float32, device=f.device)
+    f = f.contiguous()
+    m = m.contiguous()
+    lib.ffdp_minmax(_ptr(f), f.numel(), _ptr(out), _stream())
+    lib.ffdp_minmax(_ptr(m), m.numel(), _ptr(out[2:]), _stream())
+    return out
+
+
 def intensity_shift(v: torch.Tensor) -> float:
     """Mid-range of a volume (the most accurate moment shift for the fused LNCC step)."""
     mm = torch.empty(2, dtype=torch.float32, device=v.device)
@@ -632,7 +643,7 @@ def intensity_shift(v: torch.Tensor) -> float:
 
 def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=None,
                    params: Optional[LossParams] = None, g_u: Optional[torch.Tensor] = None,
-                   ws: Optional[StepWorkspace] = None, shifts: Optional[Tuple[float, float]] = None,
+                   ws: Optional[StepWorkspace] = None, ranges: Optional[torch.Tensor] = None,
                    sync: bool = True) -> StepResult:
     """One deformable-step evaluation (registration.hpp:277-312 at H = 1):
     moved = fused_sample(M, u; A, t) -> LNCC (ANTs) or Mattes MI -> g_u =
@@ -662,13 +673,12 @@ def warp_loss_step(f: torch.Tensor, m: torch.Tensor, u: torch.Tensor, A=None, t=
     if not fused_step_covers(params):
         return _composite_step(f, win, u, ca, params, g_u, ws, sync)
     if params.kind == "lncc":
-        if shifts is None:
-            shifts = (intensity_shift(f), intensity_shift(mi.interior.contiguous()))
         ws.sum_n.zero_()
         lws = ws.lncc_workspace(_dims(f.shape), slab)
+        # ranges None: the library derives them from F and the moving window on every call
         lib.ffdp_step_lncc(_ptr(f), _ptr(u), _dims(f.shape), slab, win, C.byref(ca), params.window, params.epsilon,
-                           -1.0 / n, shifts[0], shifts[1], _ptr(g_u), _ptr(ws.sum_n), _ptr(ws.miss), _ptr(lws),
-                           _stream())
+                           -1.0 / n, None if ranges is None else _ptr(ranges), _ptr(g_u), _ptr(ws.sum_n),
+                           _ptr(ws.miss), _ptr(lws), _stream())
         if not sync:
             return StepResult(float("nan"), g_u)
         loss = 1.0 - float(ws.sum_n.item()) / n

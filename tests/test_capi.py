@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_no_cpu_fallback():
     so = _lib.lib.load()
-    assert so.ffdp_abi_version() == 1
+    assert so.ffdp_abi_version() == 2
     import torch
     if not torch.cuda.is_available():
         # no device: the library refuses instead of falling back to the CPU

@@ -125,8 +125,7 @@ def test_comm_fused_step_matches_single_gpu(V, orc, loss, world):
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
     f, m, u = T(si.f), T(si.m), T(si.u)
     p = V.LossParams(kind=loss, mi_bspline_kernel=True)
-    shifts = (V.intensity_shift(f), V.intensity_shift(m)) if loss == "lncc" else None
-    ref = V.warp_loss_step(f, m, u, si.A, si.t, p, shifts=shifts)
+    ref = V.warp_loss_step(f, m, u, si.A, si.t, p)
     with Comm(world, [0] * world) as c:
         lv, g = c.step(c.scatter(f), c.scatter(m), c.scatter(u), tuple(f.shape), si.A, si.t, p)
         lv2, g2 = c.step(c.scatter(f), c.scatter(m), c.scatter(u), tuple(f.shape), si.A, si.t, p)

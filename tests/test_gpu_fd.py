@@ -24,8 +24,7 @@ def test_fused_step_directional_fd(orc, loss):
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
     f, m, u = T(si.f), T(si.m), T(si.u)
     p = V.LossParams(kind=loss, mi_bspline_kernel=True, ants_approx=False)
-    shifts = None
-    step = lambda uu: V.warp_loss_step(f, m, uu, si.A, si.t, p, shifts=shifts)
+    step = lambda uu: V.warp_loss_step(f, m, uu, si.A, si.t, p)
     r = step(u)
     g = r.g_u.double().clone()
     gen = torch.Generator(device="cuda").manual_seed(5)

@@ -70,7 +70,7 @@ def test_mi256_deterministic_sharded_and_record_free(V):
                               V._ptr(table), V._ptr(g), None, V._stream())
         parts.append(g)
     loss = -float(table[2 * bins * bins + 2 * bins + 1].item())
-    assert loss == pytest.approx(a.loss, rel=1e-12)
+    assert loss == pytest.approx(a.loss, rel=1e-9)  # fp32 per-thread n_i partials, other order
     assert maxrel(host(torch.cat(parts, 0)), host(g_a)) <= 1e-6
     # the record-free step (pass 2 samples the warp again) equals the records path
     ws = V.StepWorkspace(f.device, bins)
@@ -88,11 +88,11 @@ def test_lncc720_deterministic_and_sharded(V):
     from paper_2509_25044_b200 import dist as D
     from paper_2509_25044_b200._lib import Slab, lib
     f, m, u, A, t = _inputs((720, 640, 720), "lncc")
-    shifts = (V.intensity_shift(f), V.intensity_shift(m))
+    rg = V.intensity_ranges(f, m)
     p = V.LossParams(kind="lncc")
-    a = V.warp_loss_step(f, m, u, A, t, p, shifts=shifts)
+    a = V.warp_loss_step(f, m, u, A, t, p, ranges=rg)
     g_a = a.g_u.clone()
-    b = V.warp_loss_step(f, m, u, A, t, p, shifts=shifts)
+    b = V.warp_loss_step(f, m, u, A, t, p, ranges=rg)
     assert a.loss == b.loss and torch.equal(g_a, b.g_u)  # fixed-order reductions
     del b
     nz = f.shape[0]
@@ -107,14 +107,14 @@ def test_lncc720_deterministic_and_sharded(V):
         sn = torch.zeros(1, dtype=torch.float64, device="cuda")
         ws = torch.empty(int(lib.ffdp_step_lncc_workspace_bytes(V._dims(fb.shape), slab)) // 4, device="cuda")
         lib.ffdp_step_lncc(V._ptr(fb), V._ptr(ub), V._dims(fb.shape), slab, win, C.byref(args), 7, 1e-5,
-                           -1.0 / f.numel(), shifts[0], shifts[1], V._ptr(g), V._ptr(sn), None, V._ptr(ws),
+                           -1.0 / f.numel(), V._ptr(rg), V._ptr(g), V._ptr(sn), None, V._ptr(ws),
                            V._stream())
         total += float(sn.item())
         parts.append(host(g))
         del fb, ub, ws
     loss = 1.0 - total / f.numel()
-    assert loss == pytest.approx(a.loss, rel=1e-7)
-    assert maxrel(np.concatenate(parts, 0), host(g_a)) <= 2e-5
+    assert loss == pytest.approx(a.loss, rel=1e-9)  # fp32 per-thread n_i partials, other order
+    assert np.array_equal(np.concatenate(parts, 0), host(g_a))  # exact integer window sums
 
 
 def test_warp_update_720_sharded_bit_identical(V):

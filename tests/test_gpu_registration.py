@@ -82,7 +82,9 @@ def test_deformable_stage_matches_oracle(R, orc, loss, kind):
 
 
 def test_deformable_stage_raises_numerical_error(R):
-    """A NaN in the fixed image makes the loss non-finite: NumericalError with the trace."""
+    """A NaN in the fixed image makes the loss non-finite: NumericalError carrying the trace
+    as it stood at the start of the failing scale (registration.hpp:300-305: the scale's own
+    entries are merged only after group.run, so a first-scale failure carries [])."""
     import torch
 
     from paper_2509_25044_b200 import voxreg as V
@@ -90,9 +92,13 @@ def test_deformable_stage_raises_numerical_error(R):
     f[3, 4, 5] = float("nan")
     m = torch.rand((12, 13, 14), device="cuda")
     sch = R.ScaleSchedule([R.ScaleStep(1, 2)], loss=V.LossParams(kind="lncc"))
+    prior = [R.TraceEntry(0, 0, 0.5)]
     with pytest.raises(R.NumericalError) as e:
-        R.deformable_stage(f, m, None, sch, trace=[])
-    assert len(e.value.trace) >= 1 and not np.isfinite(e.value.trace[-1].loss)
+        R.deformable_stage(f, m, None, sch, trace=list(prior))
+    assert [(t.scale_index, t.iteration, t.loss) for t in e.value.trace] == [(0, 0, 0.5)]
+    with pytest.raises(R.NumericalError) as e:
+        R.deformable_stage(f, m, None, sch, trace=None)
+    assert e.value.trace == []
 
 
 def test_deformable_stage_gaussian_mi_first_iteration(R, orc):
