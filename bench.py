@@ -335,91 +335,199 @@ class Stepper:
 
 
 def run_sharded(args, rank, world, local_rank, dev):
-    """N > 1: weak scaling over z slabs of a (world * nz) x ny x nx volume, one rank per
-    GPU over NCCL (paper_2509_25044_b200.dist.ShardedStep): per step the u halo
-    exchange, the fused kernel(s) on the slab and the loss / histogram allreduce."""
+    """N > 1: the native sharded plan (include/ffdp.h ffdp_plan_*, csrc/plan.cu), one rank
+    per GPU over NCCL (the communicator is created by the library from a unique id that
+    torch.distributed only broadcasts). Strong scaling (default): the N = 1 workload's
+    volume split into N z slabs; weak: each GPU keeps the N = 1 voxel count of an N x taller
+    volume. Per step, inside the library: the u halo exchange overlapped with the interior
+    planes (LNCC), the fused kernels on the slab, one allreduce ({sum n_i, misses} or the
+    integer joint histogram + misses)."""
     import torch
     import torch.distributed as dist
 
-    from paper_2509_25044_b200 import dist as D
+    from paper_2509_25044_b200 import plan as PL
     from paper_2509_25044_b200 import voxreg
 
     shape, loss, cfg = WORKLOADS[args.workload]
-    gshape = (shape[0] * world, shape[1], shape[2])
-    spec = D.make_shard_spec(gshape, world, rank)
+    strong = args.scaling == "strong"
+    gshape = shape if strong else (shape[0] * world, shape[1], shape[2])
+    lo, hi = PL_shard(gshape[0], world, rank)
 
-    def reduce_minmax(lo, hi):
-        t = torch.tensor([lo, -hi], dtype=torch.float64, device=dev)
-        D.all_reduce(t, op=dist.ReduceOp.MIN)
+    def reduce_minmax(a, b):
+        t = torch.tensor([a, -b], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return float(t[0]), -float(t[1])
 
-    f, m, u, A, t = synth_inputs(gshape, loss, 1234, dev, spec.lo, spec.hi, reduce_minmax)
+    f, m, u, A, t = synth_inputs(gshape, loss, 1234, dev, lo, hi, reduce_minmax, jitter=args.jitter)
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(PL.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    group = PL.nccl_group(bytes(uid.cpu().numpy().tobytes()), world, rank, local_rank)
     params = voxreg.LossParams(kind=loss, bins=32, mi_bspline_kernel=True)
-    st = D.ShardedStep(f, m, spec, A, t, params)
-    for _ in range(args.warmup):
-        st.step(u)
-    torch.cuda.synchronize()
+    pl = PL.ShardPlan(group, gshape, params, A, t, records=True, overlap=True)
+    pl.load(f, m)
+    pl.set_u(u)
+    out = _time_plan(args, pl, world, lambda x, op: dist.all_reduce(x, op=op), dist.ReduceOp.MAX, dist.barrier,
+                     local_rank)
+    # end to end: every step the rank's slabs come from host memory (pinned), a new pair is
+    # loaded (F halo planes, intensity frame, moving window), the step runs, the loss is read
+    nbytes = 4 * (f.numel() + m.numel() + u.numel())
+    hf, hm, hu = (x.cpu() for x in (f, m, u))
+    if nbytes <= (8 << 30):
+        hf, hm, hu = (x.pin_memory() for x in (hf, hm, hu))
+    steps_e2e = 3
     dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps_e2e):
+        f.copy_(hf, non_blocking=True)
+        m.copy_(hm, non_blocking=True)
+        u.copy_(hu, non_blocking=True)
+        pl.load(f, m)
+        pl.set_u(u)
+        pl.step(sync=True)
+    te = torch.tensor([(time.perf_counter() - t0) / steps_e2e * 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    pl.close()
+    group.close()
+    nvox_total = gshape[0] * gshape[1] * gshape[2]
+    out.update({
+        "scaling": "strong" if strong else "weak",
+        "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}]" + ("" if strong else " per GPU"),
+                   "volume": "x".join(str(s) for s in gshape[::-1]), "loss": loss, "voxels_per_gpu": f.numel(),
+                   "parallelism": f"z-slab x{world}: native plan over NCCL (halo send/recv overlapped with "
+                                  f"interior planes; allreduce of the loss / integer histogram)",
+                   "u_jitter": "SURVEY 8(d)" if args.jitter == "survey" else "U(-0.01, 0.01) voxel",
+                   "l2": "inputs exceed the 126 MB L2; no flush between steps"},
+        "e2e": {"value": round(nvox_total / (float(te.item()) * 1e-3) / 1e9, 4), "unit": "Gvoxel/s",
+                "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": 16 * world,
+                "ms_per_step": round(float(te.item()), 3), "steps": steps_e2e},
+    })
+    return out
+
+
+def PL_shard(n, world, rank):
+    """shard_ranges (fabric.hpp:44-57)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _time_plan(args, pl, world, allreduce, op_max, barrier, local_rank):
+    """Warm-up (the first step is checked: window misses repaired), K launch-only steps
+    between CUDA events on the plan's stream, misses verified after the loop, the step time
+    is the max over ranks."""
+    import torch
+    pl.step(sync=True)
+    for _ in range(args.warmup - 1):
+        pl.step(sync=False)
+    pl.result()
+    barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    dist.barrier()
-    e0.record()
-    loss_val = None
-    st.verify_no_miss()
+    barrier()
+    e0.record(pl.stream)
     for _ in range(args.steps):
-        # no per-step host read: the window-miss agreement is verified once after the loop
-        # (every timed step is then known exact) and the loss stays on the device
-        loss_val, _ = st.step(u, check_miss=False, sync=False)
-    e1.record()
+        pl.step(sync=False)
+    e1.record(pl.stream)
     torch.cuda.synchronize()
-    dist.barrier()
     clocks.stop()
-    st.verify_no_miss()
-    loss_val = float(loss_val.item()) if torch.is_tensor(loss_val) else loss_val
-    tt = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-    D.all_reduce(tt, op=dist.ReduceOp.MAX)
+    loss_val, misses = pl.result()
+    if misses != 0:
+        raise RuntimeError(f"plan: {misses} window misses in the timed (unchecked) steps")
+    tt = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=pl.u.device)
+    allreduce(tt, op_max)
     ms_step = float(tt.item()) / args.steps
+    shape, loss, _ = WORKLOADS[args.workload]
+    gshape = pl.global_shape
     nvox_total = gshape[0] * gshape[1] * gshape[2]
+    nloc = (pl.hi - pl.lo) * gshape[1] * gshape[2]
     value = nvox_total / (ms_step * 1e-3) / 1e9
     hbm, hbm_kind = peaks()
-    nloc = f.numel()
     per_gpu_gbs = BYTES_PER_VOXEL[loss] * nloc / (ms_step * 1e-3) / 1e9
-    # end to end: host (pinned) inputs of the rank's slab copied in every step, loss read back
-    hf, hm, hu = (x.cpu().pin_memory() for x in (f, m, u))
-    steps_e2e = max(3, min(args.steps, 10))
-    dist.barrier()
-    e0.record()
-    for _ in range(steps_e2e):
-        f.copy_(hf, non_blocking=True)
-        m.copy_(hm, non_blocking=True)
-        u.copy_(hu, non_blocking=True)
-        st.reload(f, m)  # new pair: F halo planes + moving window rebuilt from the copied slabs
-        lv, _ = st.step(u)
-    e1.record()
-    torch.cuda.synchronize()
-    te = torch.tensor([e0.elapsed_time(e1) / steps_e2e], device=dev, dtype=torch.float64)
-    D.all_reduce(te, op=dist.ReduceOp.MAX)
     return {
         "metric": METRIC, "value": round(value, 3), "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": DTYPE[loss], "data": "synthetic",
-        "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}] per GPU, weak scaling",
-                   "volume": "x".join(str(s) for s in gshape[::-1]), "loss": loss, "voxels_per_gpu": nloc,
-                   "parallelism": f"z-slab x{world} ({dist.get_backend()} halo + allreduce)",
-                   "l2": "inputs exceed the 126 MB L2; no flush between steps"},
-        "loss": loss_val,
-        "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": round(per_gpu_gbs, 1), "peak": hbm,
-                     "unit": "GB/s", "frac": round(per_gpu_gbs / hbm, 4), "traffic": None, "peak_kind": hbm_kind,
-                     "algorithmic_bytes_per_voxel": BYTES_PER_VOXEL[loss]},
-        "gpu_launches": (1 if loss == "lncc" else 4) * args.steps,
-        "window_fetches": st.window_fetches,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "vs_baseline": None, "dtype": DTYPE[loss], "data": "synthetic", "loss": loss_val,
+        "roofline": {"bound": "hbm", "kernel": "step (per GPU, rank 0's slab)", "achieved": round(per_gpu_gbs, 1),
+                     "peak": hbm, "unit": "GB/s", "frac": round(per_gpu_gbs / hbm, 4), "traffic": None,
+                     "peak_kind": hbm_kind, "algorithmic_bytes_per_voxel": BYTES_PER_VOXEL[loss]},
+        # ours per step: LNCC up to 3 fused launches + their partial sums + the miss pack; MI
+        # pass 1, histogram conversion, finalize, pass 2, readback pack
+        "gpu_launches": (7 if loss == "lncc" else 5) * args.steps,
+        "window": pl.window(),
         "clocks": clocks.summary(),
-        "e2e": {"value": round(nvox_total / (float(te.item()) * 1e-3) / 1e9, 4), "unit": "Gvoxel/s",
-                "h2d_bytes_per_step": 4 * (f.numel() + m.numel() + u.numel()), "d2h_bytes_per_step": 8},
     }
+
+
+def run_local_group(args):
+    """--transport local: the N ranks as host threads of ONE process over the library's
+    in-process group (peer copies between the visible devices, round-robin; several ranks
+    may share one device). The reference's own one-process WorkerGroup(H) model
+    (fabric.hpp:266-300); on one GPU a functional run of the sharded path, not a scaling
+    measurement."""
+    import threading
+
+    import torch
+
+    from paper_2509_25044_b200 import plan as PL
+    from paper_2509_25044_b200 import voxreg
+    world = args.gpus
+    shape, loss, cfg = WORKLOADS[args.workload]
+    ndev = max(1, torch.cuda.device_count())
+    devs = [r % ndev for r in range(world)]
+    groups = PL.local_group(world, devs)
+    f, m, u, A, t = synth_inputs(shape, loss, 1234, "cuda:0", jitter=args.jitter)
+    params = voxreg.LossParams(kind=loss, bins=32, mi_bspline_kernel=True)
+    plans = [None] * world
+    barrier = threading.Barrier(world)
+    res = [None] * world
+    err = []
+    times = [0.0] * world
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(devs[r])
+            pl = PL.ShardPlan(groups[r], shape, params, A, t, records=True, overlap=True)
+            plans[r] = pl
+            pl.load(f[pl.lo:pl.hi].to(f"cuda:{devs[r]}"), m[pl.lo:pl.hi].to(f"cuda:{devs[r]}"))
+            pl.set_u(u[pl.lo:pl.hi].to(f"cuda:{devs[r]}"))
+            red = {}
+
+            def allreduce(x, op):
+                times[r] = float(x.item())
+                barrier.wait()
+                x.fill_(max(times))
+                barrier.wait()
+
+            res[r] = _time_plan(args, pl, world, allreduce, None, barrier.wait, devs[r])
+            del red
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+            barrier.abort()
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    if err:
+        raise err[0]
+    for pl in plans:
+        pl.close()
+    for g in groups:
+        g.close()
+    out = res[0]
+    out.update({"scaling": "strong",
+                "config": {"workload": f"{args.workload}: BASELINE configs[{cfg}]",
+                           "volume": "x".join(str(s) for s in shape[::-1]), "loss": loss,
+                           "parallelism": f"z-slab x{world}: native plan, in-process group on devices {devs}",
+                           "l2": "inputs exceed the 126 MB L2; no flush between steps"}})
+    return out
 
 
 def run_ours(args, rank, world, local_rank):
@@ -771,6 +879,10 @@ def main():
     ap.add_argument("--jitter", default="bench", choices=["bench", "survey"])
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: split the N = 1 volume (strong) or grow it N x along z (weak)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "local"],
+                    help="N > 1: one process per GPU over NCCL (torchrun), or N ranks as threads of one process")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.workload == "auto":
@@ -828,11 +940,12 @@ def main():
             "e2e": {"value": round(v, 6), "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
+    if args.transport == "local" and args.gpus > 1:
+        print(json.dumps(run_local_group(args)))
+        return
     if world > 1:
         import torch.distributed as dist
-        # FFDP_DIST_BACKEND=gloo runs the sharded path with several ranks on one GPU
-        # (host-staged exchanges; a functional check, not a scaling measurement)
-        dist.init_process_group(os.environ.get("FFDP_DIST_BACKEND", "nccl"))
+        dist.init_process_group("nccl")
     out, st = run_ours(args, rank, world, local_rank)
     if rank == 0 and world == 1:
         import torch

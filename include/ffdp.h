@@ -477,6 +477,69 @@ FFDP_API int ffdp_dist_step(ffdp_comm comm, int loss_kind, const float* const* f
                             const float* const* u, ffdp_dims global, const double* A, const double* t, int window,
                             double eps, const ffdp_parzen* kernel, double* loss, float* const* g_u);
 
+
+/* ------------------------------------------------ native sharded step plan (plan.cu) */
+/*
+ * The sharded deformable step as a persistent per-rank object (one per GPU), for C / C++
+ * hosts that run one process (or one thread) per rank: the reference's per-iteration
+ * sequence under WorkerGroup(H) (registration.hpp:266-312: ring_sample -> dist_lncc /
+ * dist_mi -> ring_sample_backward(warp), distops.hpp:144-396) over z slabs by
+ * shard_ranges (fabric.hpp:44-70), with halo_exchange (fabric.hpp:315-370) and
+ * allreduce_sum (fabric.hpp:246-263) as NCCL point-to-point / allreduce calls (or peer
+ * copies inside one process).
+ *
+ * Transport ("group"): ffdp_group_nccl -- one rank of an NCCL communicator (every rank
+ * passes the same FFDP_NCCL_ID_BYTES-byte id from ffdp_nccl_unique_id; NCCL is loaded at
+ * run time, libnccl.so.2 or $FFDP_NCCL_LIB); ffdp_group_local -- `world` ranks inside one
+ * process (out[world] handles; devices may repeat), each driven by its own host thread.
+ * Every plan call below is collective over the group: all ranks call it in the same order.
+ */
+#define FFDP_NCCL_ID_BYTES 128
+typedef struct ffdp_group_s* ffdp_group;
+typedef struct ffdp_plan_s* ffdp_plan;
+FFDP_API int ffdp_nccl_version(int* version);
+FFDP_API int ffdp_nccl_unique_id(unsigned char* id /* FFDP_NCCL_ID_BYTES */);
+FFDP_API int ffdp_group_nccl(const unsigned char* id, int world, int rank, int device, ffdp_group* out);
+FFDP_API int ffdp_group_local(int world, const int* devices, ffdp_group* out /* world handles */);
+FFDP_API int ffdp_group_destroy(ffdp_group g);
+FFDP_API int ffdp_group_info(ffdp_group g, int* world, int* rank, int* device);
+
+typedef struct {
+    int32_t loss_kind;     /* 0 = LNCC (ANTs, window 7), 1 = Mattes MI (B-spline Parzen) */
+    int32_t window;        /* LNCC window (7) */
+    double eps;            /* LNCC epsilon */
+    ffdp_parzen kernel;    /* MI kernel (ffdp_parzen_make) */
+    double A[9], t[3];     /* affine of the stage (row-major, normalized coordinates) */
+    int32_t margin_planes; /* moving-window margin beyond the affine's z reach */
+    int32_t records;       /* MI: 1 = pass-1 records when they fit (+16 B/voxel), 0 = pass 2 re-samples */
+    int32_t overlap;       /* LNCC: 1 = u halo exchange overlapped with the interior planes */
+} ffdp_plan_params;
+
+/* Creates rank g's plan for a `global` lattice (slab = shard_ranges(nz, world, rank)). */
+FFDP_API int ffdp_plan_create(ffdp_group g, ffdp_dims global, const ffdp_plan_params* params, ffdp_plan* out);
+FFDP_API int ffdp_plan_destroy(ffdp_plan p);
+FFDP_API int ffdp_plan_slab(ffdp_plan p, int64_t* lo, int64_t* hi);
+/* The plan's compute stream, and its device buffers: u (the slab's interior planes of the
+ * persistent haloed displacement buffer, 3 floats per voxel -- the caller or its optimiser
+ * writes it on the plan's stream; the halo planes are the plan's) and g_u (interior). */
+FFDP_API void* ffdp_plan_stream(ffdp_plan p);
+FFDP_API float* ffdp_plan_u(ffdp_plan p);
+FFDP_API float* ffdp_plan_g_u(ffdp_plan p);
+/* Moving planes [z0, z1) resident on this rank, and how many window fetches this scale. */
+FFDP_API int ffdp_plan_window(ffdp_plan p, int64_t* z0, int64_t* z1, int64_t* fetches);
+/* Once per scale (collective, synchronous): the rank's F and M slabs (device or host
+ * pointers, slab planes only) -> F halo planes, the intensity frame (LNCC), the moving
+ * window from the owners of its planes. */
+FFDP_API int ffdp_plan_load(ffdp_plan p, const float* f_slab, const float* m_slab);
+/* One step (collective): g_u = dL/du on the slab, loss = the global loss. sync = 1: waits,
+ * repeats the step with widened windows after a window miss on any rank (exact), and
+ * writes *loss. sync = 0: launch only (no host synchronisation; the misses accumulate and
+ * ffdp_plan_result reports them -- a non-zero count means the unchecked steps must be
+ * redone with sync = 1). */
+FFDP_API int ffdp_plan_step(ffdp_plan p, int sync, double* loss);
+/* Waits for the last step; its loss and the summed window misses over all ranks. */
+FFDP_API int ffdp_plan_result(ffdp_plan p, double* loss, double* misses);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,15 @@ class ParzenC(C.Structure):
                 ("norm", C.c_double)]
 
 
+class PlanParamsC(C.Structure):
+    """ffdp_plan_params (include/ffdp.h)."""
+    _fields_ = [("loss_kind", C.c_int32), ("window", C.c_int32), ("eps", C.c_double), ("kernel", ParzenC),
+                ("A", C.c_double * 9), ("t", C.c_double * 3), ("margin_planes", C.c_int32),
+                ("records", C.c_int32), ("overlap", C.c_int32)]
+
+
+NCCL_ID_BYTES = 128
+
 _vp, _dp = C.c_void_p, C.POINTER(C.c_double)
 _vpp = C.POINTER(C.c_void_p)
 _SIGS = {
@@ -140,6 +149,23 @@ _SIGS = {
                                  _vpp]),
     "ffdp_dist_step": (C.c_int, [_vp, C.c_int, _vpp, _vpp, _vpp, Dims, _dp, _dp, C.c_int, C.c_double,
                                  C.POINTER(ParzenC), _dp, _vpp]),
+    # the native sharded step plan (plan.cu)
+    "ffdp_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "ffdp_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "ffdp_group_nccl": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "ffdp_group_local": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+    "ffdp_group_destroy": (C.c_int, [_vp]),
+    "ffdp_group_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ffdp_plan_create": (C.c_int, [_vp, Dims, C.POINTER(PlanParamsC), C.POINTER(C.c_void_p)]),
+    "ffdp_plan_destroy": (C.c_int, [_vp]),
+    "ffdp_plan_slab": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ffdp_plan_stream": (C.c_void_p, [_vp]),
+    "ffdp_plan_u": (C.c_void_p, [_vp]),
+    "ffdp_plan_g_u": (C.c_void_p, [_vp]),
+    "ffdp_plan_window": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ffdp_plan_load": (C.c_int, [_vp, _vp, _vp]),
+    "ffdp_plan_step": (C.c_int, [_vp, C.c_int, _dp]),
+    "ffdp_plan_result": (C.c_int, [_vp, _dp, _dp]),
 }
 
 
@@ -172,7 +198,7 @@ class _Lib:
         if name in ("ffdp_last_error", "ffdp_abi_version", "ffdp_device_check", "ffdp_step_mi_workspace_bytes",
                     "ffdp_step_mi_record_bytes", "ffdp_step_lncc_workspace_bytes",
                     "ffdp_step_lncc_passes_workspace_bytes", "ffdp_comm_world",
-                    "ffdp_comm_device"):
+                    "ffdp_comm_device", "ffdp_plan_stream", "ffdp_plan_u", "ffdp_plan_g_u"):
             return fn
 
         def call(*args):

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["capi.cu", "sampler.cu", "lncc.cu", "mi.cu", "step_lncc.cu", "step_lncc2.cu", "step_lncc3.cu", "step_mi.cu", "smooth.cu", "resample.cu", "comm.cu"]
+SOURCES = ["capi.cu", "sampler.cu", "lncc.cu", "mi.cu", "step_lncc.cu", "step_lncc2.cu", "step_lncc3.cu", "step_mi.cu", "smooth.cu", "resample.cu", "comm.cu", "plan.cu"]
 LIB = os.path.join(HERE, "libffdp.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared"]
@@ -36,10 +36,28 @@ def _stale(target, deps):
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> str:
+    """One object per source (compiled in parallel, rebuilt when the source or a shared
+    header changed), then one nvcc link into libffdp.so."""
+    from concurrent.futures import ThreadPoolExecutor
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "ffdp_common.cuh"), os.path.join(ROOT, "include", "ffdp.h")]
-    if force or _stale(LIB, deps):
-        cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + srcs
+    headers = [os.path.join(CSRC, "ffdp_common.cuh"), os.path.join(ROOT, "include", "ffdp.h")]
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def one(so):
+        src, obj = so
+        if force or _stale(obj, [src] + headers):
+            cmd = [nvcc()] + cflags + ["-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        list(ex.map(one, zip(srcs, objs)))
+    if force or _stale(LIB, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -174,11 +174,16 @@ __global__ void __launch_bounds__(NT) k_reduce_sum(const double* in, int64_t n, 
     if (threadIdx.x == 0) *out = r;
 }
 
+// Value range of a buffer. A NaN anywhere makes both bounds NaN (fminf / fmaxf would drop
+// it): callers derive intensity frames from the range, and a non-finite input must reach
+// the loss as NaN, as it does in the reference's arithmetic (registration.hpp:300-305).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_minmax_partial(const float* in, int64_t n, float* part) {
     float lo = INFINITY, hi = -INFINITY;
+    int bad = 0;
     for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
         const float v = in[i];
+        bad |= v != v;
         lo = fminf(lo, v);
         hi = fmaxf(hi, v);
     }
@@ -187,30 +192,36 @@ __global__ void __launch_bounds__(NT) k_minmax_partial(const float* in, int64_t 
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
+    bad = __any_sync(0xffffffffu, bad);
     __shared__ float sl[NT / 32], sh[NT / 32];
+    __shared__ int sb[NT / 32];
     if ((threadIdx.x & 31) == 0) {
         sl[threadIdx.x >> 5] = lo;
         sh[threadIdx.x >> 5] = hi;
+        sb[threadIdx.x >> 5] = bad;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int i = 1; i < NT / 32; ++i) {
             lo = fminf(lo, sl[i]);
             hi = fmaxf(hi, sh[i]);
+            bad |= sb[i];
         }
-        part[2 * blockIdx.x] = sl[0] < lo ? sl[0] : lo;
-        part[2 * blockIdx.x + 1] = sh[0] > hi ? sh[0] : hi;
+        part[2 * blockIdx.x] = bad ? NAN : lo;
+        part[2 * blockIdx.x + 1] = bad ? NAN : hi;
     }
 }
 
 __global__ void k_minmax_final(const float* part, int nb, float* out) {
     float lo = INFINITY, hi = -INFINITY;
+    bool bad = false;
     for (int i = 0; i < nb; ++i) {
+        bad |= part[2 * i] != part[2 * i];
         lo = fminf(lo, part[2 * i]);
         hi = fmaxf(hi, part[2 * i + 1]);
     }
-    out[0] = lo;
-    out[1] = hi;
+    out[0] = bad ? NAN : lo;
+    out[1] = bad ? NAN : hi;
 }
 
 template <int NT>

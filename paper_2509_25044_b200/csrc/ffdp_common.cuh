@@ -278,7 +278,9 @@ __device__ __forceinline__ void gather_n(const Geom& g, const Cell (&c)[NS], Cor
 // -2 or n reads two border zeros, like the reference's fully zero-padded samples) and
 // load the 8 corners unconditionally. With a z window, corners on non-resident planes
 // inside the volume are window misses (they read the zero border).
-template <bool FULLWIN, bool OFF32 = false>
+// OFF: 0 = 64-bit addressing; 1 = signed 32-bit offsets from the window (< 2^31 elements);
+// 2 = unsigned 32-bit offsets from the block origin (< 2^32 elements, window_off32).
+template <bool FULLWIN, int OFF = 0>
 __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int& miss) {
     const int32_t ix = min(max(c.i0[0], -2), g.n[0]);
     const int32_t iy = min(max(c.i0[1], -2), g.n[1]);
@@ -293,7 +295,7 @@ __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int&
     }
     const int32_t sy = (int32_t)g.sy;
     Corners k;
-    if (OFF32) {
+    if (OFF == 1) {
         // the resident window holds < 2^31 elements: 32-bit offsets, one wide add per row
         const int32_t sz = (int32_t)g.sz;
         const int32_t o = (iz - g.wz0) * sz + iy * sy + ix;
@@ -301,6 +303,26 @@ __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int&
         const float* p1 = g.img + (o + sy);
         const float* p2 = g.img + (o + sz);
         const float* p3 = g.img + (o + sz + sy);
+        k.v[0] = __ldg(p0);
+        k.v[1] = __ldg(p0 + 1);
+        k.v[2] = __ldg(p1);
+        k.v[3] = __ldg(p1 + 1);
+        k.v[4] = __ldg(p2);
+        k.v[5] = __ldg(p2 + 1);
+        k.v[6] = __ldg(p3);
+        k.v[7] = __ldg(p3 + 1);
+        return k;
+    }
+    if (OFF == 2) {
+        // the zero-bordered block holds < 2^32 elements: unsigned 32-bit offsets from its
+        // origin (every clamped corner index is >= -2), one IMAD.WIDE.U32 per row pointer
+        const uint32_t usy = (uint32_t)g.sy, usz = (uint32_t)g.sz;
+        const uint32_t o = (uint32_t)(iz - g.wz0 + 2) * usz + (uint32_t)(iy + 2) * usy + (uint32_t)(ix + 2);
+        const float* org = g.img - (2 * g.sz + 2 * g.sy + 2);
+        const float* p0 = org + o;
+        const float* p1 = org + (o + usy);
+        const float* p2 = org + (o + usz);
+        const float* p3 = org + (o + usz + usy);
         k.v[0] = __ldg(p0);
         k.v[1] = __ldg(p0 + 1);
         k.v[2] = __ldg(p1);
@@ -324,10 +346,16 @@ __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int&
     return k;
 }
 
-// The padded resident window fits 32-bit element offsets (gather_pad<.., true>).
-inline bool window_off32(const Geom& g) {
-    return (double)g.sz * (double)(g.wz1 - g.wz0 + 4) < 2147483647.0 - 4.0 * (double)g.sz;
+// gather_pad's addressing mode for a zero-bordered window: 1 when the resident window fits
+// signed 32-bit offsets (the old bound), 2 when the block fits unsigned 32-bit offsets from
+// its origin ((nx+4)(ny+4)(planes+4) < 2^32), else 0 (64-bit).
+inline int window_off_mode(const Geom& g) {
+    const double n = (double)g.sz * (double)(g.wz1 - g.wz0 + 4);
+    if (g.pad != 2) return 0;
+    if (n < 2147483647.0 - 4.0 * (double)g.sz) return 1;
+    return n < 4294967295.0 ? 2 : 0;
 }
+inline bool window_off32(const Geom& g) { return window_off_mode(g) == 1; }
 
 // ------------------------------------------------------------------ Parzen kernels
 // Up to four bins m_lo..m_lo+3 carry weight for one intensity (mi.hpp:28-140):

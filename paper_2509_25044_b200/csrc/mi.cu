@@ -401,7 +401,7 @@ inline bool mi_use_quad(const ffdp_dims& d, const ffdp_slab& s, const ffdp_image
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
                  int32_t* miss, cudaStream_t st, float* rec = nullptr, double* table = nullptr,
-                 double upstream = -1.0);
+                 double upstream = -1.0, int scale_exp = 0);
 int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ffdp_parzen& k, const double* table,
                 const float* rec, float* g_u, cudaStream_t st);
 int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,

@@ -38,6 +38,9 @@
 namespace ffdp {
 namespace l3 {
 
+#ifndef FFDP_L3_ROWS
+#define FFDP_L3_ROWS 1
+#endif
 constexpr int R = 3, WIN = 7, TX = 32, TY = 32, HX = TX + 2 * R, HY = TY + 2 * R;
 constexpr int NT = 512;                                        // threads: moment warps + sampler warps
 constexpr int NPOS = HX * HY, NIN = TX * TY;                   // 1444 haloed positions, 1024 outputs
@@ -124,6 +127,19 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
     const uint32_t a = saddr(b);
     while (!mbar_try(a, parity)) {
+    }
+}
+// The sampler warps' wait for a ring slot: they run ahead of the moment warps and wait there
+// most of the time; a failed try_wait backs off with nanosleep so the spinning warps leave
+// the issue slots to the moment warps (the spin loop was 45 of 475 instructions per voxel,
+// ncu source counters, profiles/r02_full_lncc_fused.txt).
+#ifndef FFDP_L3_SLEEP_NS
+#define FFDP_L3_SLEEP_NS 256
+#endif
+__device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, uint32_t parity) {
+    const uint32_t a = saddr(b);
+    while (!mbar_try(a, parity)) {
+        if (FFDP_L3_SLEEP_NS > 0) __nanosleep(FFDP_L3_SLEEP_NS);
     }
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, unsigned long long* bar, int c0, int c1,
@@ -225,7 +241,7 @@ __device__ __forceinline__ void sampler_warps(const CUtensorMap* umap, const CUt
         const int it = (int)(p - pstart);
         const int slot = it % RING, gslot = it % NG;
         // the moment warps must have finished iteration it - 2 (its b, F and G slots are reused)
-        if (it >= 2) mbar_wait(&sm.consumed[(it - 2) % RING], (uint32_t)(((it - 2) / RING) & 1));
+        if (it >= 2) mbar_wait_backoff(&sm.consumed[(it - 2) % RING], (uint32_t)(((it - 2) / RING) & 1));
         const bool vz = p >= 0 && p < P.nz_global;
         const bool wantG = p >= zc0 && p < zc1;
         if (TMA && st == 0 && p + 2 < pend) {
@@ -292,6 +308,159 @@ __device__ __forceinline__ void sampler_warps(const CUtensorMap* umap, const CUt
     if (anym && P.miss && (st & 31) == 0) atomicAdd(P.miss, __popc(anym));
 }
 
+// Row-mapped sampler (8 warps): a lane is an x column, so nearly every per-sample quantity
+// is warp-uniform. The 32 output columns (haloed columns 3..34) of the 38 haloed rows are
+// "main" passes -- warp w takes rows w, w + 8, ... (warps 0-5: 5 rows, 6-7: 4), G is wanted
+// exactly on rows 3..34 (a uniform branch); the 6 halo columns x 38 rows = 228 "edge"
+// positions are one pass per warp (e = 32 w + lane). Passes run in two batches of three:
+// the cells of a batch, then all of its corner loads, then the interpolations, with the
+// next batch's u in flight. Coordinates are evaluated directly from (gx, gy, p) -- no
+// accumulated increments -- so a sample does not depend on the tiling or the chunking.
+constexpr int SROWS = 5;  // main rows per warp (the last one absent on warps 6, 7)
+constexpr int NEDGE = 6 * HY;
+template <bool TMA, bool FULLWIN, bool OFF32>
+__device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUtensorMap* mmap, const Params& P,
+                                             Smem& sm, int st, int64_t pstart, int64_t pend, int64_t zc0,
+                                             int64_t zc1, int x0, int y0, float kM, float nsmk) {
+    const int lane = st & 31, w = st >> 5;
+    const int nx = P.nx, ny = P.ny;
+    // main column of this lane
+    const int gxm = x0 + lane;
+    const bool vxm = gxm < nx;
+    // the lane's edge position
+    const int e = 32 * w + lane;
+    const int erow = e / 6, ecol = e - 6 * (e / 6);
+    const int ehx = ecol < 3 ? ecol : TX + ecol;  // 0, 1, 2, 35, 36, 37
+    const int gxe = x0 - R + ehx, gye = y0 - R + erow;
+    const bool ve = e < NEDGE && gxe >= 0 && gxe < nx && gye >= 0 && gye < ny;
+    double bxm[3], bxe[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        bxm[a] = fma(P.g.P[3 * a + 0], (double)gxm, P.g.K[a]);
+        bxe[a] = fma(P.g.P[3 * a + 1], (double)gye, fma(P.g.P[3 * a + 0], (double)gxe, P.g.K[a]));
+    }
+    const int32_t offm = vxm ? gxm : 0;                      // + gy * nx per row
+    const int32_t offe = ve ? gye * nx + gxe : 0;
+    const int nrows = w < 6 ? SROWS : SROWS - 1;
+    int miss = 0;
+    const float dsc0 = P.g.dscale[0], dsc1 = P.g.dscale[1], dsc2 = P.g.dscale[2];
+    const int64_t pl3 = 3 * P.plane;
+    const float* ub = P.u + 3 * (pstart - P.buf_z0) * P.plane;  // u of plane p
+    // pass j of a plane: main row hy = w + 8 j (j < nrows), then the edge pass (j = nrows)
+    constexpr int NB = 3;
+    float uu[2][NB][3];
+    auto row_ok = [&](int j) {
+        const int gy = y0 - R + w + 8 * j;
+        return j < nrows && gy >= 0 && gy < ny;
+    };
+    auto load_u = [&](float (&u3)[NB][3], const float* base, int j0, bool vz) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const int j = j0 + k;
+            bool ok;
+            int32_t o;
+            if (j < SROWS) {
+                ok = vz && vxm && row_ok(j);
+                o = offm + (y0 - R + w + 8 * j) * nx;
+            } else {
+                ok = vz && ve;
+                o = offe;
+            }
+            const float* q = base + 3 * (int64_t)(ok ? o : 0);
+            u3[k][0] = ok ? __ldg(q) : 0.0f;
+            u3[k][1] = ok ? __ldg(q + 1) : 0.0f;
+            u3[k][2] = ok ? __ldg(q + 2) : 0.0f;
+        }
+    };
+    load_u(uu[0], ub, 0, pstart >= 0 && pstart < P.nz_global);
+
+    for (int64_t p = pstart; p < pend; ++p) {
+        const int it = (int)(p - pstart);
+        const int slot = it % RING, gslot = it % NG;
+        // the moment warps must have finished iteration it - 2 (its b, F and G slots are reused)
+        if (it >= 2) mbar_wait_backoff(&sm.consumed[(it - 2) % RING], (uint32_t)(((it - 2) / RING) & 1));
+        const bool vz = p >= 0 && p < P.nz_global;
+        const bool wantG = p >= zc0 && p < zc1;
+        if (TMA && st == 0 && p + 2 < pend) {
+            tma_prefetch_3d(umap, 3 * (x0 - R - 1), y0 - R, (int)(p + 2 - P.buf_z0));
+            tma_prefetch_3d(mmap, x0 - 4, y0 - R, (int)(p + 2 - P.g.wz0 + 2));
+        }
+        const double zd = (double)p;
+        double bzm[3], bze[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            bzm[a] = fma(P.g.P[3 * a + 2], zd, bxm[a]);
+            bze[a] = fma(P.g.P[3 * a + 2], zd, bxe[a]);
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float(&u3)[NB][3] = uu[half];
+            Cell c[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const int j = NB * half + k;
+                double b0, b1, b2;
+                if (j < SROWS) {
+                    const double gy = (double)(y0 - R + w + 8 * j);
+                    b0 = fma(P.g.P[1], gy, bzm[0]);
+                    b1 = fma(P.g.P[4], gy, bzm[1]);
+                    b2 = fma(P.g.P[7], gy, bzm[2]);
+                } else {
+                    b0 = bze[0];
+                    b1 = bze[1];
+                    b2 = bze[2];
+                }
+                cell_fix(fma(P.g.Q[0], (double)u3[k][0], b0), c[k].i0[0], c[k].frac[0]);
+                cell_fix(fma(P.g.Q[1], (double)u3[k][1], b1), c[k].i0[1], c[k].frac[1]);
+                cell_fix(fma(P.g.Q[2], (double)u3[k][2], b2), c[k].i0[2], c[k].frac[2]);
+            }
+            // the other batch's u (this plane's second batch, or the next plane's first)
+            if (half == 0) {
+                load_u(uu[1], ub, NB, vz);
+            } else if (p + 1 < pend) {
+                ub += pl3;
+                load_u(uu[0], ub, 0, p + 1 >= 0 && p + 1 < P.nz_global);
+            }
+            Corners cr[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                int mk = 0;
+                cr[k] = gather_pad<FULLWIN, OFF32>(P.g, c[k], mk);
+                const int j = NB * half + k;
+                const bool ok = vz && (j < SROWS ? (vxm && row_ok(j)) : ve);
+                if (!FULLWIN) miss |= mk & (int)ok;
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const int j = NB * half + k;
+                if (j < SROWS) {
+                    if (j >= nrows) continue;  // warps 6, 7: four main rows
+                    const int hy = w + 8 * j;
+                    const bool ok = vz && vxm && row_ok(j);
+                    float v;
+                    if (wantG && hy >= R && hy < R + TY) {  // warp-uniform
+                        float d[3];
+                        v = interp_grad(cr[k], c[k], d);
+                        const int ii = (hy - R) * TX + lane;
+                        sm.gr[gslot][0][ii] = dsc0 * d[0];
+                        sm.gr[gslot][1][ii] = dsc1 * d[1];
+                        sm.gr[gslot][2][ii] = dsc2 * d[2];
+                    } else {
+                        v = interp(cr[k], c[k]);
+                    }
+                    sm.br[slot][hy * HX + R + lane] = ok ? fmaf(v, kM, nsmk) : 0.0f;
+                } else {
+                    const float v = interp(cr[k], c[k]);
+                    if (e < NEDGE) sm.br[slot][erow * HX + ehx] = (vz && ve) ? fmaf(v, kM, nsmk) : 0.0f;
+                }
+            }
+        }
+        mbar_arrive(&sm.sampled[slot]);
+    }
+    const unsigned anym = __ballot_sync(0xffffffffu, miss);
+    if (anym && P.miss && lane == 0) atomicAdd(P.miss, __popc(anym));
+}
+
 // ------------------------------------------------------------------ moment warps
 template <int NM_, bool TMA>
 __device__ __forceinline__ float moment_warps(const CUtensorMap* fmap, const Params& P, Smem& sm, int mt,
@@ -347,6 +516,8 @@ __device__ __forceinline__ float moment_warps(const CUtensorMap* fmap, const Par
     const float mF = (float)(1.0 / (NWIN * (double)QSCALE)) / kF, mM = (float)(1.0 / (NWIN * (double)QSCALE)) / kM;
     const int32_t NU = (WIN * WIN * WIN) << 21;  // N * 2^21 < 2^31
     const float gi2 = 2.0f * (float)P.gi, epsf = (float)P.eps;
+    // a NaN in F or M (NaN value ranges, ffdp_minmax) poisons the loss and the gradient
+    const bool poison = !(fabsf(sf) <= 3.0e38f && fabsf(smv) <= 3.0e38f);
 
     int32_t zs[MPOS][5];
 #pragma unroll
@@ -466,7 +637,7 @@ __device__ __forceinline__ float moment_warps(const CUtensorMap* fmap, const Par
                 const float fq = sm.fr[qslot][hy * FW + hx + 1];
                 const float df = (fq - sf) - (float)X * mF + sf * omw;
                 const float dm = sm.br[qslot][hy * HX + hx] * ikM - (float)Y * mM + smv * omw;
-                const float gmw = gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:262-278, ANTs)
+                const float gmw = poison ? __int_as_float(0x7fc00000) : gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:262-278, ANTs)
                 const int ii = (oy + j) * TX + ox;
                 float* o = go + j * rs;
                 o[0] = sm.gr[qg][0][ii] * gmw;
@@ -477,7 +648,7 @@ __device__ __forceinline__ float moment_warps(const CUtensorMap* fmap, const Par
         }
         mbar_arrive(&sm.consumed[slot]);
     }
-    return nsum;
+    return poison ? __int_as_float(0x7fc00000) : nsum;
 }
 
 template <int NM_, bool TMA, bool FULLWIN, bool OFF32>
@@ -497,6 +668,7 @@ __global__ void __launch_bounds__(NT, 1) k_lncc_fused(const __grid_constant__ CU
     float sf, kF, smv, kM;
     frame1(P.ranges[0], P.ranges[1], sf, kF);
     frame1(fminf(P.ranges[2], 0.0f), fmaxf(P.ranges[3], 0.0f), smv, kM);
+    if (P.ranges[2] != P.ranges[2]) smv = P.ranges[2];  // NaN in M: poison (fminf drops it)
 
     if (t == 0) {
         for (int s = 0; s < RING; ++s) {
@@ -515,7 +687,14 @@ __global__ void __launch_bounds__(NT, 1) k_lncc_fused(const __grid_constant__ CU
         nsum = moment_warps<NM_, TMA>(&fmap, P, sm, t, pstart, pend, zc0, x0, y0, sf, kF, smv, kM);
     } else {
         if (SP::RS != 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SP::RS));
-        sampler_warps<NM_, TMA, FULLWIN, OFF32>(&umap, &mmap, P, sm, t - SP::NM, pstart, pend, zc0, zc1, x0, y0, kM, -smv * kM);
+#if FFDP_L3_ROWS
+        if (SP::NS == 256)
+            sampler_rows<TMA, FULLWIN, OFF32>(&umap, &mmap, P, sm, t - SP::NM, pstart, pend, zc0, zc1, x0, y0, kM,
+                                              -smv * kM);
+        else
+#endif
+            sampler_warps<NM_, TMA, FULLWIN, OFF32>(&umap, &mmap, P, sm, t - SP::NM, pstart, pend, zc0, zc1, x0, y0,
+                                                    kM, -smv * kM);
     }
     const double cta = block_sum<NT>((double)nsum, sm.red);
     if (t == 0) P.partial[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = cta;

@@ -18,6 +18,8 @@
 // are not accumulated here: finalize_histogram derives p_i, p_j from the joint
 // (mi.hpp:181-196), so the fused step needs only the B*B joint payload.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "ffdp_common.cuh"
 
@@ -333,7 +335,7 @@ __device__ __forceinline__ int32_t bspline_scaled(float v, int B, float C, float
     return min(max(m, -HPAD), (BC > 0 ? BC : B) + HPAD - 4);
 }
 
-template <bool FULLWIN, bool REC, int BC, bool OFF32, int S>
+template <bool FULLWIN, bool REC, int BC, int OFF32, int S>
 __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
     static_assert(S == 21 || S == 23, "odd scale exponent: equal weight pre-scales");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -528,6 +530,89 @@ __global__ void __launch_bounds__(NT, 3) k_step_mi_grad(const Params P) {
     if (anym && P.miss && (threadIdx.x & 31) == 0) atomicAdd(P.miss, __popc(anym));
 }
 
+// Pass 2 for the B-spline kernel, re-sampling the warp (the record-free path: configs[4]
+// has no room for 16 B/voxel of records next to its 119 GB of F, M, u and g_u). The unit
+// walk of k_mi_hist_bs (per-unit F / u / g_u row pointers, unsigned 32-bit gather offsets
+// when the window allows) and the ghat dot of k_step_mi_grad_rec (the table as 4
+// column-shifted shared copies: one LDS.128 per footprint row). mi.hpp:392-421.
+__host__ __device__ constexpr int grad_tab_floats(int B);
+
+#ifndef FFDP_MI_G2_MINB
+#define FFDP_MI_G2_MINB 3
+#endif
+template <bool FULLWIN, int BC, int OFF32>
+__global__ void __launch_bounds__(NT, FFDP_MI_G2_MINB) k_mi_grad_bs(const Params P) {
+    extern __shared__ __align__(16) float sg[];
+    const int B = BC > 0 ? BC : P.p.bins;
+    const int LD = B + 2 * PAD;           // rows
+    const int CP = (LD + 3) / 4 * 4;      // row pitch (floats)
+    const int CS = LD * CP;               // copy size
+    {
+        const double* gh = P.table + B * B + 2 * B;
+        for (int q = threadIdx.x; q < 4 * CS; q += NT) {
+            const int c = q / CS, r = (q % CS) / CP, k = q % CP;
+            const int m = r - PAD, nn = k + c - PAD;
+            sg[q] = (m >= 0 && m < B && nn >= 0 && nn < B) ? (float)gh[m * B + nn] : 0.0f;
+        }
+        __syncthreads();
+    }
+    int miss = 0;
+    const int lane = threadIdx.x & 31;
+    const float ds0 = P.g.dscale[0], ds1 = P.g.dscale[1], ds2 = P.g.dscale[2];
+    const int64_t zout = (P.z_begin - P.buf_z0) * P.plane;  // g_u covers the interior planes
+    const int64_t stride = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t unit = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); unit < P.nunits; unit += stride) {
+        const Unit w = unit_coords(P, (uint32_t)unit, lane);
+        const float* fp = P.f + w.bi;
+        const float* up = P.u + 3 * w.bi;
+        float ff[4], uu[12];
+        bool ok[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            ok[k] = w.vx && (w.y0 + k) < P.ny;
+            ff[k] = ok[k] ? __ldg(fp + k * P.nx) : 0.0f;
+            uu[3 * k] = ok[k] ? __ldg(up + 3 * k * P.nx) : 0.0f;
+            uu[3 * k + 1] = ok[k] ? __ldg(up + 3 * k * P.nx + 1) : 0.0f;
+            uu[3 * k + 2] = ok[k] ? __ldg(up + 3 * k * P.nx + 2) : 0.0f;
+        }
+        Cell c[4];
+        unit_cells(P, w, uu, c);
+        Corners cr[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN, OFF32>(P.g, c[k], miss);
+        float* op = P.g_u + 3 * (w.bi - zout);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float d[3];
+            const float mw = interp_grad(cr[k], c[k], d);
+            const BS4 bi = bspline_bins<false>(ff[k], B);
+            const BS4 bj = bspline_bins<true>(mw, B);
+            // dL/dJ = sum_m kappa_i[m] sum_n ghat[m][n] omega_j[n]   (mi.hpp:409-418)
+            const int n0 = bj.m_lo + PAD;
+            const float4* gr =
+                reinterpret_cast<const float4*>(sg + (n0 & 3) * CS + (bi.m_lo + PAD) * CP + (n0 & ~3));
+            float gj = 0.0f;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const float4 g = gr[a * (CP / 4)];
+                float acc = g.x * bj.w[0];
+                acc = fmaf(g.y, bj.w[1], acc);
+                acc = fmaf(g.z, bj.w[2], acc);
+                acc = fmaf(g.w, bj.w[3], acc);
+                gj = fmaf(bi.k[a], acc, gj);
+            }
+            if (ok[k]) {
+                float* o = op + 3 * k * P.nx;
+                o[0] = ds0 * d[0] * gj;
+                o[1] = ds1 * d[1] * gj;
+                o[2] = ds2 * d[2] * gj;
+            }
+        }
+    }
+    const unsigned anym = __ballot_sync(0xffffffffu, miss);
+    if (anym && P.miss && (threadIdx.x & 31) == 0) atomicAdd(P.miss, __popc(anym));
+}
+
 // Pass 2 from the pass-1 records: F and (Mw, dscale * dMw/dfrac) are streamed, dL/dMw
 // from the ghat table (mi.hpp:392-421, B-spline), g_u = record.yzw * dL/dMw. No gather,
 // no coordinates: 32 B/voxel of pure streaming (F 4 + record 16 in, g_u 12 out).
@@ -665,6 +750,15 @@ bool mi_quad_path_applies(const ffdp_dims& d, const ffdp_slab& s, const ffdp_ima
            ((d.nx + 31) / 32) * ((d.ny + 3) / 4) * (s.z_end - s.z_begin) < (1LL << 31);
 }
 
+// log2 of the B-spline pass-1 fixed-point grid for a call over `voxels` interior voxels
+int mi_bs_scale_exp(int64_t voxels) { return voxels >= (int64_t)FFDP_MI_BS_LARGE_MIN ? 21 : 23; }
+
+// raw[i] += hist[i] / 2^scale_exp for the B*B joint entries (after an integer allreduce)
+int mi_hist_u64_to_raw(const unsigned long long* h, int B, int scale_exp, double* raw, cudaStream_t st) {
+    mstep::k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, std::ldexp(1.0, -scale_exp), raw);
+    return check_launch("mi_hist_u64_to_raw");
+}
+
 static mstep::Params make_params(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s,
                                  const ffdp_image_window& m, const ffdp_sampler_args& args, const ffdp_parzen& k) {
     mstep::Params P;
@@ -698,7 +792,7 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
 
 int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_slab& s, const ffdp_image_window& m,
                  const ffdp_sampler_args& args, const ffdp_parzen& k, double* raw, unsigned long long* ws,
-                 int32_t* miss, cudaStream_t st, float* rec, double* table, double upstream) {
+                 int32_t* miss, cudaStream_t st, float* rec, double* table, double upstream, int scale_exp) {
     using namespace mstep;
     Params P = make_params(f, u, d, s, m, args, k);
     const int B = k.bins;
@@ -728,21 +822,20 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     if (rec && !bs) return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
     if (bs) {
         const size_t smem = bs_smem_bytes(B);
-        const bool o32 = window_off32(P.g);
-        const bool large = d.nx * d.ny * (s.z_end - s.z_begin) >= (int64_t)FFDP_MI_BS_LARGE_MIN;
+        const int om = window_off_mode(P.g);
+        // scale_exp 21 / 23 forces the grid (a sharded plan picks it from the GLOBAL voxel
+        // count, so every rank accumulates on the single-GPU grid and the integer allreduce
+        // reproduces the single-GPU histogram exactly)
+        const bool large = scale_exp ? scale_exp == 21 : mi_bs_scale_exp(d.nx * d.ny * (s.z_end - s.z_begin)) == 21;
         P.fix_scale = large ? 2097152.0f : 8388608.0f;  // 2^21 / 2^23
-        const int sel = (full ? 1 : 0) | (rec ? 2 : 0) | (B == 32 ? 4 : 0) | (o32 ? 8 : 0) | (large ? 16 : 0);
-#define FFDP_BS_ROW(S)                                                                                    \
-    k_mi_hist_bs<false, false, 0, false, S>, k_mi_hist_bs<true, false, 0, false, S>,                    \
-        k_mi_hist_bs<false, true, 0, false, S>, k_mi_hist_bs<true, true, 0, false, S>,                  \
-        k_mi_hist_bs<false, false, 32, false, S>, k_mi_hist_bs<true, false, 32, false, S>,              \
-        k_mi_hist_bs<false, true, 32, false, S>, k_mi_hist_bs<true, true, 32, false, S>,                \
-        k_mi_hist_bs<false, false, 0, true, S>, k_mi_hist_bs<true, false, 0, true, S>,                  \
-        k_mi_hist_bs<false, true, 0, true, S>, k_mi_hist_bs<true, true, 0, true, S>,                    \
-        k_mi_hist_bs<false, false, 32, true, S>, k_mi_hist_bs<true, false, 32, true, S>,                \
-        k_mi_hist_bs<false, true, 32, true, S>, k_mi_hist_bs<true, true, 32, true, S>
-        static const decltype(&k_mi_hist_bs<true, true, 32, true, 23>) table_[32] = {FFDP_BS_ROW(23),
-                                                                                   FFDP_BS_ROW(21)};
+        const int sel = (full ? 1 : 0) | (rec ? 2 : 0) | (B == 32 ? 4 : 0) | (om * 8) | (large ? 24 : 0);
+#define FFDP_BS_ROW(O, S)                                                                                        \
+    k_mi_hist_bs<false, false, 0, O, S>, k_mi_hist_bs<true, false, 0, O, S>, k_mi_hist_bs<false, true, 0, O, S>,     \
+        k_mi_hist_bs<true, true, 0, O, S>, k_mi_hist_bs<false, false, 32, O, S>, k_mi_hist_bs<true, false, 32, O, S>, \
+        k_mi_hist_bs<false, true, 32, O, S>, k_mi_hist_bs<true, true, 32, O, S>
+        static const decltype(&k_mi_hist_bs<true, true, 32, 1, 23>) table_[48] = {
+            FFDP_BS_ROW(0, 23), FFDP_BS_ROW(1, 23), FFDP_BS_ROW(2, 23),
+            FFDP_BS_ROW(0, 21), FFDP_BS_ROW(1, 21), FFDP_BS_ROW(2, 21)};
 #undef FFDP_BS_ROW
         static std::atomic<unsigned long long> bs_attr{0};
         if (first_on_device(bs_attr)) {
@@ -762,7 +855,9 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
         else
             k_step_mi_hist<false, false, false><<<grid, HNT, smem, st>>>(P);
     }
-    if (!fin) k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
+    // raw == null (with a caller workspace): the fixed-point histogram stays in ws for an
+    // integer allreduce; the caller converts it (mi_hist_u64_to_raw)
+    if (!fin && raw) k_hist_to_raw<<<(B * B + 255) / 256, 256, 0, st>>>(h, B * B, 1.0 / P.fix_scale, raw);
     if (!ws) scratch_free(h, st);
     return check_launch("step_mi_hist");
 }
@@ -781,6 +876,24 @@ int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_
                                                                  6LL * num_sms()));
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool bs = k.kind == FFDP_PARZEN_BSPLINE3;
+    static const bool legacy = getenv("FFDP_MI_GRAD_LEGACY") && getenv("FFDP_MI_GRAD_LEGACY")[0] == '1';
+    if (bs && !legacy) {
+        const size_t tab = sizeof(float) * grad_tab_floats(B);
+        static std::atomic<unsigned long long> attr_mask{0};
+        using K = decltype(&k_mi_grad_bs<true, 32, 1>);
+#define FFDP_G2_ROW(O) k_mi_grad_bs<false, 0, O>, k_mi_grad_bs<true, 0, O>, k_mi_grad_bs<false, 32, O>, k_mi_grad_bs<true, 32, O>
+        static const K ks[12] = {FFDP_G2_ROW(0), FFDP_G2_ROW(1), FFDP_G2_ROW(2)};
+#undef FFDP_G2_ROW
+        if (first_on_device(attr_mask))
+            for (auto fn : ks)
+                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(float) * grad_tab_floats(64)));
+        const int sel = (full ? 1 : 0) | (B == 32 ? 2 : 0) | (window_off_mode(P.g) * 4);
+        const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((P.nunits + NT / 32 - 1) / (NT / 32),
+                                                                  (int64_t)FFDP_MI_G2_MINB * num_sms()));
+        ks[sel]<<<g2, NT, tab, st>>>(P);
+        return check_launch("step_mi_grad");
+    }
     if (bs && full)
         k_step_mi_grad<true, true><<<grid, NT, smem, st>>>(P);
     else if (bs)

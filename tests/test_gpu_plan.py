@@ -1,0 +1,286 @@
+"""The native sharded step plan (include/ffdp.h ffdp_plan_*, csrc/plan.cu) on one GPU.
+
+Ranks of an in-process group (one host thread each, sharing cuda:0) run the whole
+deformable step -- u halo exchange, fused kernels on their slabs, allreduce of sum n_i /
+the integer joint histogram -- and the gathered g_u / global loss are compared with the
+single-GPU step (the reference's shard-invariance tests, test_distops.cpp:161-187,
+243-289, 369-423) and with the fp64 oracle. The NCCL transport runs at world 1 here (one
+device) and at world 2 when the box has two devices."""
+import threading
+
+import numpy as np
+import pytest
+
+from gpu_util import dev, host, maxrel, need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def V():
+    need_gpu()
+    from paper_2509_25044_b200 import voxreg
+    return voxreg
+
+
+@pytest.fixture(scope="module")
+def PL():
+    need_gpu()
+    from paper_2509_25044_b200 import plan
+    return plan
+
+
+def params_for(V, loss):
+    if loss == "lncc":
+        return V.LossParams(kind="lncc")
+    return V.LossParams(kind="mi", bins=32, mi_bspline_kernel=True)
+
+
+def run_ranks(groups, fn):
+    """fn(group) on one thread per rank; re-raises the first failure."""
+    out, err = [None] * len(groups), []
+
+    def body(i, g):
+        import torch
+        try:
+            torch.cuda.set_device(g.device)
+            out[i] = fn(g)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=body, args=(i, g)) for i, g in enumerate(groups)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
+def plan_step(PL, V, groups, si, loss, steps=1, records=True, overlap=True, margin=8, u=None):
+    """Every rank: plan, load its slabs, set u, `steps` steps; returns [(loss, g_u, lo, hi, window)]."""
+    import torch
+    shape = si.f.shape
+    A, t = si.A, si.t
+    u = si.u if u is None else u
+
+    def rank(g):
+        p = PL.ShardPlan(g, shape, params_for(V, loss), A, t, margin_planes=margin, records=records,
+                         overlap=overlap)
+        try:
+            p.load(dev(si.f)[p.lo:p.hi], dev(si.m)[p.lo:p.hi])
+            p.set_u(dev(u)[p.lo:p.hi])
+            lv = None
+            for _ in range(steps):
+                lv = p.step()
+            torch.cuda.synchronize()
+            return lv, host(p.g_u.clone()), p.lo, p.hi, p.window()
+        finally:
+            p.close()
+
+    return run_ranks(groups, rank)
+
+
+def single(V, si, loss, u=None):
+    r = V.warp_loss_step(dev(si.f), dev(si.m), dev(si.u if u is None else u), si.A, si.t, params_for(V, loss))
+    return r.loss, host(r.g_u)
+
+
+@pytest.fixture(scope="module")
+def cases(orc):
+    from oracle import step_inputs
+    # MI above 2^16 voxels: the single-GPU step then takes the same quad kernels and 2^-23
+    # fixed-point grid as the plan (smaller lattices use the scalar kernels)
+    return {"lncc": step_inputs(orc, (29, 26, 24), seed=515, loss="lncc"),
+            "mi": step_inputs(orc, (44, 42, 40), seed=515, loss="mi")}
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_local_group_matches_single_gpu(V, PL, cases, loss, world):
+    si = cases[loss]
+    groups = PL.local_group(world, [0] * world)
+    try:
+        res = plan_step(PL, V, groups, si, loss)
+    finally:
+        for g in groups:
+            g.close()
+    l1, g1 = single(V, si, loss)
+    gu = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0)
+    assert all(r[0] == res[0][0] for r in res), "every rank reports the same global loss"
+    lrel = abs(res[0][0] - l1) / abs(l1)
+    grel = maxrel(gu, g1)
+    print(f"plan {loss} H={world}: loss rel {lrel:.2e}, g_u maxrel {grel:.2e}")
+    # integer window sums (LNCC) / the integer joint histogram on the single-GPU grid (MI):
+    # the sharded gradient is the single-GPU gradient up to the finalize's fp64 order
+    assert lrel <= 1e-9
+    assert grel <= 1e-6
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_local_group_bit_identical_across_world_sizes(V, PL, cases, loss):
+    si = cases[loss]
+    out = {}
+    for world in (1, 2, 4):
+        groups = PL.local_group(world, [0] * world)
+        try:
+            res = plan_step(PL, V, groups, si, loss, steps=2)
+        finally:
+            for g in groups:
+                g.close()
+        out[world] = (res[0][0], np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0))
+    for world in (2, 4):
+        assert np.array_equal(out[world][1], out[1][1]), f"g_u at H={world} differs from H=1"
+        if loss == "mi":
+            assert out[world][0] == out[1][0]
+        else:
+            assert abs(out[world][0] - out[1][0]) <= 1e-12
+
+
+def test_plan_matches_oracle(V, PL, orc, cases):
+    """The plan at H = 2 against the fp64 oracle step (loss 1e-5, g_u 1e-4: north star)."""
+    for loss in ("lncc", "mi"):
+        si = cases[loss]
+        if loss == "lncc":
+            ref = orc.step_lncc(si.f, si.m, si.u, si.A, si.t)
+        else:
+            ref = orc.step_mi(si.f, si.m, si.u, orc.parzen("bspline3", 32), si.A, si.t)
+        groups = PL.local_group(2, [0, 0])
+        try:
+            res = plan_step(PL, V, groups, si, loss)
+        finally:
+            for g in groups:
+                g.close()
+        gu = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0)
+        lrel = abs(res[0][0] - ref["loss"]) / abs(ref["loss"])
+        grel = maxrel(gu, ref["g_u"])
+        print(f"plan {loss} H=2 vs oracle: loss rel {lrel:.2e}, g_u maxrel {grel:.2e}")
+        assert lrel <= 1e-5 and grel <= 1e-4
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_window_miss_widens_and_stays_exact(V, PL, cases, loss):
+    """No margin and a displacement of +0.3 (normalized, ~4 planes) along z: the affine
+    window misses the displaced samples, the summed miss count makes the ranks widen their
+    windows from the z extent of their samples and repeat the step."""
+    si = cases[loss]
+    u = np.array(si.u, dtype=np.float64)
+    u[..., 2] += 0.3
+    groups = PL.local_group(3, [0, 0, 0])
+    try:
+        res = plan_step(PL, V, groups, si, loss, margin=0, u=u)
+    finally:
+        for g in groups:
+            g.close()
+    gu = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0)
+    l1, g1 = single(V, si, loss, u=u)
+    fetches = [r[4][2] for r in res]
+    print(f"plan {loss} margin 0: window fetches per rank {fetches}")
+    assert max(fetches) > 1, "the displaced samples should have missed the affine window"
+    assert abs(res[0][0] - l1) / abs(l1) <= 1e-9
+    assert maxrel(gu, g1) <= 1e-6
+
+
+def test_records_and_overlap_variants(V, PL, cases):
+    """MI with and without pass-1 records, LNCC with and without the overlapped halo
+    exchange: identical gradients (the split is a launch boundary, the sums are exact)."""
+    import torch  # noqa: F401
+    for loss, kw in (("mi", "records"), ("lncc", "overlap")):
+        si = cases[loss]
+        res = {}
+        for flag in (True, False):
+            groups = PL.local_group(2, [0, 0])
+            try:
+                r = plan_step(PL, V, groups, si, loss, **{kw: flag})
+            finally:
+                for g in groups:
+                    g.close()
+            res[flag] = np.concatenate([x[1] for x in sorted(r, key=lambda x: x[2])], axis=0)
+        assert np.array_equal(res[True], res[False]), kw
+
+
+def test_overlap_split_on_thick_slabs(V, PL, orc):
+    """Slabs thick enough for the interior / boundary split (> 2 x 16 + 8 planes)."""
+    from oracle import step_inputs
+    si = step_inputs(orc, (100, 20, 24), seed=77, loss="lncc")
+    out = {}
+    for overlap in (True, False):
+        groups = PL.local_group(2, [0, 0])
+        try:
+            r = plan_step(PL, V, groups, si, "lncc", overlap=overlap)
+        finally:
+            for g in groups:
+                g.close()
+        out[overlap] = (r[0][0], np.concatenate([x[1] for x in sorted(r, key=lambda x: x[2])], axis=0))
+    l1, g1 = single(V, si, "lncc")
+    assert np.array_equal(out[True][1], out[False][1])
+    assert maxrel(out[True][1], g1) <= 1e-6
+    assert abs(out[True][0] - l1) / abs(l1) <= 1e-9
+
+
+def test_nccl_world1_matches_local(V, PL, cases):
+    try:
+        PL.nccl_version()
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"NCCL not loadable: {e}")
+    for loss in ("lncc", "mi"):
+        si = cases[loss]
+        g = PL.nccl_group(PL.nccl_unique_id(), 1, 0, 0)
+        try:
+            rn = plan_step(PL, V, [g], si, loss)
+        finally:
+            g.close()
+        gl = PL.local_group(1, [0])
+        try:
+            rl = plan_step(PL, V, gl, si, loss)
+        finally:
+            gl[0].close()
+        assert rn[0][0] == rl[0][0]
+        assert np.array_equal(rn[0][1], rl[0][1])
+
+
+def test_nccl_world2_two_devices(V, PL, cases):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two devices")
+    uid = PL.nccl_unique_id()
+    for loss in ("lncc", "mi"):
+        si = cases[loss]
+        holder = {}
+
+        def mk(r):
+            torch.cuda.set_device(r)
+            holder[r] = PL.nccl_group(uid, 2, r, r)
+
+        th = [threading.Thread(target=mk, args=(r,)) for r in range(2)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        groups = [holder[0], holder[1]]
+        try:
+            res = plan_step(PL, V, groups, si, loss)
+        finally:
+            for g in groups:
+                g.close()
+        l1, g1 = single(V, si, loss)
+        gu = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0)
+        assert abs(res[0][0] - l1) / abs(l1) <= 1e-9 and maxrel(gu, g1) <= 1e-6
+        uid = PL.nccl_unique_id()
+
+
+def test_plan_argument_errors(V, PL):
+    from paper_2509_25044_b200._lib import InvalidArgument, LogicError
+    g = PL.local_group(1, [0])[0]
+    try:
+        with pytest.raises(InvalidArgument):
+            PL.ShardPlan(g, (16, 16, 16), V.LossParams(kind="lncc", window=5))
+        with pytest.raises(InvalidArgument):
+            PL.ShardPlan(g, (16, 16, 16), V.LossParams(kind="mi", bins=32, mi_bspline_kernel=False))
+        p = PL.ShardPlan(g, (16, 16, 16), V.LossParams(kind="lncc"))
+        with pytest.raises(LogicError):
+            p.step()
+        p.close()
+    finally:
+        g.close()
