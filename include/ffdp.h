@@ -218,14 +218,14 @@ FFDP_API int ffdp_lncc_fwd(const float* f, const float* m, ffdp_dims buf_dims, f
                   double* state, float* ncc_map, double* sum_n, void* stream);
 
 /*
- * First half of lncc_backward_fused (lncc.hpp:359-374): rewrites state in place as the
+ * First half of lncc_backward_fused (lncc.hpp:234-247): rewrites state in place as the
  * gamma family (gamma, gamma_AB, gamma_AC, gamma_FM, gamma_MF) with gi = dL/dn_i
- * (= -upstream/N, lncc.hpp:361; -1/N_total in dist_lncc, distops.hpp:320).
+ * (= -upstream/N, lncc.hpp:234; -1/N_total in dist_lncc, distops.hpp:320).
  */
 FFDP_API int ffdp_lncc_gamma(double* state, int64_t voxels, double eps, double gi, void* stream);
 
 /*
- * Second half (lncc.hpp:376-406): exact mode (ants == 0) box-filters the gamma family
+ * Second half (lncc.hpp:249-278): exact mode (ants == 0) box-filters the gamma family
  * (gamma buffer described by `slab`, halo planes included) before the combination;
  * ANTs mode uses it as is. grad_f may be NULL. f, m, grad_f, grad_m cover the interior.
  */
@@ -233,7 +233,7 @@ FFDP_API int ffdp_lncc_combine(const double* gamma, ffdp_dims buf_dims, ffdp_sla
                       const float* f, const float* m, float* grad_f, float* grad_m, void* stream);
 
 /* lncc_backward_fused (lncc.hpp:226-280) of a whole volume in one call: the gamma family
- * (gi = -upstream / N, lncc.hpp:361) then the combination; `state` (from ffdp_lncc_fwd
+ * (gi = -upstream / N, lncc.hpp:234) then the combination; `state` (from ffdp_lncc_fwd
  * over the whole volume) is consumed, as the reference rewrites LnccState in place. */
 FFDP_API int ffdp_lncc_bwd(double upstream, double* state, const float* f, const float* m, ffdp_dims dims,
                            int window, double eps, int ants, float* grad_f, float* grad_m, void* stream);

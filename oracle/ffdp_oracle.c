@@ -867,7 +867,7 @@ static void rasterize_ellipsoids(or_rng* r, or_dims d, int k, uint16_t* lab) { /
 }
 
 static void random_smooth_warp(or_rng* r, or_dims d, double max_norm, double sigma, double rms_fraction,
-                               double* w) { /* synth.hpp:134-168 */
+                               double* w) { /* synth.hpp:80-114 */
     const int64_t n = dims_voxels(d);
     for (int64_t i = 0; i < 3 * n; ++i) w[i] = or_rng_normal(r);
     or_gaussian_smooth(w, d, 3, sigma);
@@ -896,7 +896,7 @@ static void random_smooth_warp(or_rng* r, or_dims d, double max_norm, double sig
 }
 
 /*
- * synth_pair (synth.hpp:170-189) without the label outputs: fixed, moving (N each),
+ * synth_pair (synth.hpp:116-137) without the label outputs: fixed, moving (N each),
  * true_warp (3N). Returns 0 or 1 (invalid_argument).
  */
 OR_API int or_synth_pair(uint64_t seed, or_dims d, int k, double max_disp, double* fixed, double* moving,

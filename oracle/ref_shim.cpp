@@ -225,7 +225,7 @@ int ref_parzen_eval(int kind, int bins, double sigma_bins, const double* x, int6
     });
 }
 
-// synth_pair (synth.hpp:170): fixed, moving (N) and the ground-truth warp (3N).
+// synth_pair (synth.hpp:116-137): fixed, moving (N) and the ground-truth warp (3N).
 int ref_synth_pair(uint64_t seed, const int64_t* dims, int k, double max_disp, double* fixed, double* moving,
                    double* true_warp) {
     return guarded([&] {

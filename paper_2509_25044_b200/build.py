@@ -96,10 +96,18 @@ def build_cpp_tests(force: bool = False, verbose: bool = False) -> str:
     return CPP_TEST_BIN
 
 
+def build_ref_backend(verbose: bool = False) -> None:
+    """The reference's own driver linked through integration/voxreg/ffdp_backend.hpp
+    (oracle/_ref/test_ref_backend; test infrastructure, needs /root/reference)."""
+    if os.path.isdir("/root/reference/proj/include"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref-backend"], check=True)
+
+
 def build_all(verbose: bool = False) -> None:
     build_lib(verbose=verbose)
     build_oracle(verbose=verbose)
     build_cpp_tests(verbose=verbose)
+    build_ref_backend(verbose=verbose)
 
 
 if __name__ == "__main__":

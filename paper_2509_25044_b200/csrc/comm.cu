@@ -618,7 +618,7 @@ int ffdp_dist_lncc(ffdp_comm c, const float* const* f, const float* const* moved
             continue;
         }
         // exact: the gamma family on the slab +- r planes (inside the lattice), box-filtered
-        // again (lncc.hpp:376-406); the 2r halo holds their windows
+        // again (lncc.hpp:249-263); the 2r halo holds their windows
         const int64_t nz_g = sync ? global.nz : th, g_lo = sync ? sh[(size_t)r].lo : 0;
         const int64_t nb = th + lo[(size_t)r] + hi[(size_t)r];
         const int64_t e0 = std::max<int64_t>(0, g_lo - rad), e1 = std::min<int64_t>(nz_g, g_lo + th + rad);

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kNT) k_lncc_gamma(double* __restrict__ st, int
     }
 }
 
-// Final combination (lncc.hpp:392-405). gam: planar 5 x n interior voxels.
+// Final combination (lncc.hpp:265-278). gam: planar 5 x n interior voxels.
 __global__ void __launch_bounds__(kNT) k_lncc_combine(const double* __restrict__ gam, int64_t n,
                                                        const float* __restrict__ f, const float* __restrict__ m,
                                                        float* __restrict__ gf, float* __restrict__ gm) {
@@ -258,7 +258,7 @@ int ffdp_lncc_combine(const double* gamma, ffdp_dims d, ffdp_slab s, int window,
 
 int ffdp_lncc_bwd(double upstream, double* state, const float* f, const float* m, ffdp_dims d, int window, double eps,
                   int ants, float* grad_f, float* grad_m, void* stream) {
-    // lncc_backward_fused (lncc.hpp:226-280): gi = -upstream / N (lncc.hpp:361)
+    // lncc_backward_fused (lncc.hpp:226-280): gi = -upstream / N (lncc.hpp:234)
     if (!state || !f || !m || !grad_m) return set_error(FFDP_INVALID_ARGUMENT, "lncc_backward: null pointer");
     const int64_t n = d.nx * d.ny * d.nz;
     if (n < 1) return set_error(FFDP_INVALID_ARGUMENT, "lncc_backward: empty volume");

@@ -9,7 +9,7 @@
 //           Reads u 12 + M 4, writes Mw 4 + G 12 bytes per voxel.
 //   pass 2  k_lncc_moments: the five window moments of (F, Mw) by separable box sums
 //           (x, y running sums per plane in shared memory, z by fp64 telescoping over
-//           the z march), ANTs dL/dMw (lncc.hpp:392-405) and g_u = G * dL/dMw.
+//           the z march), ANTs dL/dMw (lncc.hpp:265-278) and g_u = G * dL/dMw.
 //           Reads F 4 + Mw 4 + G 12, writes g_u 12 bytes per voxel; the x/y halo of F
 //           and Mw comes from L2 (neighbouring tiles read the same planes).
 //
@@ -329,7 +329,7 @@ __device__ __forceinline__ void mplane(const MParams& P, typename Tile<TX, TY>::
             const float omwf = (float)(1.0 - W);
             const float df = (fm.x - mf) + P.sf * omwf;    // F - mean_F
             const float dm = (fm.y - mm) + P.sm * omwf;    // Mw - mean_M
-            const float gmw = gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:404, ANTs)
+            const float gmw = gamma * fmaf(-dm, rab, df);  // dL/dMw (lncc.hpp:277, ANTs)
             float* o = P.g_u + qoff + out_off[j];
             o[0] = G[j][0] * gmw;
             o[1] = G[j][1] * gmw;

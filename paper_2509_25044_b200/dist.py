@@ -713,7 +713,7 @@ def dist_lncc(spec: ShardSpec, f_shard: torch.Tensor, moved_shard: torch.Tensor,
                               V._ptr(f), V._ptr(m), None, V._ptr(g), V._stream())
         return DistLoss(loss, g)
     # exact: the gamma family on the slab +- r planes (inside the lattice; the 2r halo holds
-    # their windows), box-filtered again (lncc.hpp:376-406). One exchange of 2r planes where
+    # their windows), box-filtered again (lncc.hpp:249-263). One exchange of 2r planes where
     # the reference exchanges r planes twice (neighbours must be >= 2r planes thick).
     e0 = max(0, g_lo - r)
     e1 = min(nz_g, g_lo + f.shape[0] + r)

@@ -111,7 +111,7 @@ def _convolve_axis(v: np.ndarray, axis: int, taps: np.ndarray) -> np.ndarray:
 
 
 def gaussian_smooth(v: np.ndarray, sigma: float) -> np.ndarray:
-    """gaussian_smooth (smoothing.hpp:107-128): x, then y, then z, renormalized edges;
+    """gaussian_smooth (smoothing.hpp:107-127): x, then y, then z, renormalized edges;
     a warp (trailing axis 3) is smoothed per component."""
     if not math.isfinite(sigma) or sigma < 0:
         raise InvalidArgument("gaussian_smooth: sigma must be finite and >= 0")

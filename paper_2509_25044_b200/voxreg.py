@@ -401,7 +401,7 @@ def lncc_forward_fused(f: torch.Tensor, m: torch.Tensor, window: int = 7, eps: f
 def lncc_backward_fused(upstream: float, state: LnccState, f: torch.Tensor, m: torch.Tensor,
                         ants_approx: bool) -> Tuple[torch.Tensor, torch.Tensor]:
     """lncc_backward_fused (lncc.hpp:226-280). The state is consumed (rewritten in place
-    as the gamma family, lncc.hpp:350-351)."""
+    as the gamma family, lncc.hpp:236-247)."""
     f, m = _vol(f, "lncc"), _vol(m, "lncc")
     if tuple(state.channels.shape[1:]) != tuple(f.shape) or tuple(f.shape) != tuple(m.shape):
         raise InvalidArgument("lncc_backward_fused: lattice mismatch")

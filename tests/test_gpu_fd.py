@@ -5,7 +5,7 @@ smooth direction v of a few hundredths of a voxel, on the survey's synthetic pai
 interpolant is piecewise linear: voxels whose samples cross a cell face in +-v bend the
 difference). MI runs the fused B-spline step; LNCC runs the exact backward (the
 operator composition): the fused LNCC step implements the ANTs backward, which by design
-drops the window terms of the gradient (lncc.hpp:392-405) and is not the loss's gradient."""
+drops the window terms of the gradient (lncc.hpp:265-278) and is not the loss's gradient."""
 import numpy as np
 import pytest
 
