@@ -119,7 +119,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ synthetic inputs
-def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, jitter="bench"):
+def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, jitter="bench", chunk=32):
     """Synthetic pair of the survey's recipe on the GPU, analytic in the
     global normalized frame so any z slab [z0, z1) of the global `shape` is generated
     locally and consistently across ranks: smooth ellipsoidal structures with texture,
@@ -127,7 +127,10 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, j
     A = I + U(-0.02, 0.02), t = U(-0.02, 0.02). MI: M = normalize(4 m (1 - m) + noise).
     reduce_minmax(lo, hi) -> (lo, hi) makes the intensity normalisation global.
     jitter: "bench" adds U(-0.01, 0.01) voxel to u; "survey" adds SURVEY 8(d)'s
-    U(-0.01, 0.01) in normalized units (+-0.5 (n-1) / 100 voxels: +-3.6 at 720)."""
+    U(-0.01, 0.01) in normalized units (+-0.5 (n-1) / 100 voxels: +-3.6 at 720).
+    The outputs are allocated first and filled `chunk` planes at a time (the noise streams
+    are seeded per chunk), so no volume-sized temporary fragments the device memory: at
+    configs[4] (119 GB of F, M, u, g_u) the step's 16 B/voxel records must still fit."""
     import numpy as np
     import torch
 
@@ -137,10 +140,17 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, j
     z1 = nz if z1 is None else z1
     lshape = (z1 - z0, ny, nx)
     ax = lambda n: torch.linspace(-1.0, 1.0, n, device=device, dtype=torch.float32)
-    z, y, x = ax(nz)[z0:z1].view(-1, 1, 1), ax(ny).view(1, ny, 1), ax(nx).view(1, 1, nx)
+    zax, y, x = ax(nz), ax(ny).view(1, ny, 1), ax(nx).view(1, 1, nx)
     blobs = [((rnd(3) * 1.2 - 0.6).tolist(), (rnd(3) * 0.3 + 0.2).tolist(), float(rnd(1) * 0.7 + 0.3))
              for _ in range(6)]
     tex = [((rnd(3) * 12 + 4).tolist(), (rnd(3) * 6.28).tolist()) for _ in range(3)]
+
+    def modes(amp):
+        return [[((rnd(3) * 3 + 0.5).tolist(), (rnd(3) * 6.28).tolist(), float(rnd(1) * 2 - 1) * amp)
+                 for _ in range(3)] for _ in range(3)]
+
+    modes_true, modes_u = modes(0.04), modes(0.02)
+    aff = rnd(12).numpy() * 0.04 - 0.02
 
     def f_at(X, Y, Z):
         out = torch.zeros(torch.broadcast_shapes(X.shape, Y.shape, Z.shape), dtype=torch.float32, device=device)
@@ -151,47 +161,54 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, j
             out += 0.04 * torch.sin(k[0] * X + ph[0]) * torch.sin(k[1] * Y + ph[1]) * torch.sin(k[2] * Z + ph[2])
         return out
 
-    def smooth_field(amp):
-        modes = [[((rnd(3) * 3 + 0.5).tolist(), (rnd(3) * 6.28).tolist(), float(rnd(1) * 2 - 1) * amp)
-                  for _ in range(3)] for _ in range(3)]
-        u = torch.zeros(lshape + (3,), dtype=torch.float32, device=device)
+    def field(md, z, out):
         for cpt in range(3):
-            for k, ph, a in modes[cpt]:
-                u[..., cpt] += a * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(
-                    k[2] * z + ph[2])
-        return u
+            acc = out[..., cpt]
+            acc.zero_()
+            for k, ph, a in md[cpt]:
+                acc += a * torch.sin(k[0] * x + ph[0]) * torch.sin(k[1] * y + ph[1]) * torch.sin(k[2] * z + ph[2])
 
-    def normalize(v):
+    def normalize_(v):
         lo, hi = float(v.min()), float(v.max())
         if reduce_minmax is not None:
             lo, hi = reduce_minmax(lo, hi)
-        return ((v - lo) / (hi - lo)).clamp_(0.0, 1.0)
+        v.sub_(lo).div_(hi - lo).clamp_(0.0, 1.0)
 
-    f = normalize(f_at(x, y, z))
-    u_true = smooth_field(0.04)
-    m = normalize(f_at(x + u_true[..., 0], y + u_true[..., 1], z + u_true[..., 2]))
-    del u_true
-    if loss == "mi":
-        noise = torch.randn(lshape, generator=torch.Generator(device=device).manual_seed(seed + 1 + z0), device=device)
-        m = normalize(4.0 * m * (1.0 - m) + 0.02 * noise)
-        del noise
-    u = smooth_field(0.02)
-    # sub-voxel jitter (+-0.01 voxel) keeps samples off cell faces; a registration warp is
-    # smooth (it is Gaussian-smoothed every iteration, registration.hpp:316), so the
-    # parity tests' U(-0.01, 0.01)-normalized jitter (+-1.3 voxels at 256^3) would be an
-    # unrealistically rough field for a throughput benchmark
     if jitter == "survey":
         jit = torch.tensor([0.02, 0.02, 0.02], device=device)
     else:
+        # sub-voxel jitter (+-0.01 voxel) keeps samples off cell faces; a registration warp
+        # is smooth (it is Gaussian-smoothed every iteration, registration.hpp:316)
         jit = torch.tensor([0.04 / (nx - 1), 0.04 / (ny - 1), 0.04 / (nz - 1)], device=device)
-    u += (torch.rand(u.shape, generator=torch.Generator(device=device).manual_seed(seed + 2 + z0), device=device)
-          - 0.5) * jit
-    aff = rnd(12).numpy() * 0.04 - 0.02
+    f = torch.empty(lshape, dtype=torch.float32, device=device)
+    m = torch.empty(lshape, dtype=torch.float32, device=device)
+    u = torch.empty(lshape + (3,), dtype=torch.float32, device=device)
+    ut = torch.empty((min(chunk, lshape[0]), ny, nx, 3), dtype=torch.float32, device=device)
+    for c0 in range(0, lshape[0], chunk):
+        c1 = min(lshape[0], c0 + chunk)
+        z = zax[z0 + c0:z0 + c1].view(-1, 1, 1)
+        f[c0:c1] = f_at(x, y, z)
+        t3 = ut[:c1 - c0]
+        field(modes_true, z, t3)
+        m[c0:c1] = f_at(x + t3[..., 0], y + t3[..., 1], z + t3[..., 2])
+        field(modes_u, z, u[c0:c1])
+        gj = torch.Generator(device=device).manual_seed(seed + 2 + z0 + c0)
+        u[c0:c1] += (torch.rand((c1 - c0, ny, nx, 3), generator=gj, device=device) - 0.5) * jit
+    del ut
+    normalize_(f)
+    normalize_(m)
+    if loss == "mi":
+        for c0 in range(0, lshape[0], chunk):
+            c1 = min(lshape[0], c0 + chunk)
+            gn = torch.Generator(device=device).manual_seed(seed + 1 + z0 + c0)
+            mc = m[c0:c1]
+            mc.copy_(4.0 * mc * (1.0 - mc) + 0.02 * torch.randn((c1 - c0, ny, nx), generator=gn, device=device))
+        normalize_(m)
     A = np.eye(3) + aff[:9].reshape(3, 3)
     t = aff[9:]
     if torch.device(device).type == "cuda":
         torch.cuda.synchronize()
-    return f.contiguous(), m.contiguous(), u.contiguous(), A, t
+    return f, m, u, A, t
 
 
 # ------------------------------------------------------------------ the GPU arm
@@ -233,15 +250,25 @@ class Stepper:
                 self._lws = self._p(self.ws.lncc_workspace(self.dims, self.slab))
         else:
             self.kernel = voxreg.ParzenKernel.bspline3(bins)
-            # the pass-1 records (16 B/voxel) when they fit next to the step's buffers; else
-            # pass 2 samples the warp again (ffdp_step_mi without records)
-            free, _ = torch.cuda.mem_get_info()
-            self.use_rec = free > 16 * self.n + (4 << 30)
+            self.choose_records()
         self.kernel_ms = {}
         # lncc: sample, moments, partial-sum reduction (fused: 1); mi: pass 1 (finalize fused
         # into its last CTA) and pass 2 (memsets of the histogram are not kernels of ours)
         self.launches_per_step = ((3 if self.twopass else 2) if loss == "lncc" else
                                   2 if self.use_rec else 4)
+
+    def choose_records(self):
+        """MI: the pass-1 records (16 B/voxel) when they fit next to the step's buffers
+        with 4 GiB to spare; else pass 2 samples the warp again (ffdp_step_mi without
+        records). Re-evaluated once the caller has released its own copy of M."""
+        if self.loss != "mi":
+            return
+        free, _ = self.torch.cuda.mem_get_info()
+        need = 16 * self.n + (4 << 30)
+        self.use_rec = free > need
+        self.launches_per_step = 2 if self.use_rec else 4
+        self.records_note = {"used": self.use_rec, "device_free_bytes": int(free), "needed_bytes": int(need),
+                             "torch_reserved_bytes": int(self.torch.cuda.memory_reserved())}
 
     def _p(self, t):
         return self.C.c_void_p(t.data_ptr())
@@ -553,6 +580,7 @@ def run_ours(args, rank, world, local_rank):
     st = Stepper(f, m, u, A, t, loss)
     del m
     torch.cuda.empty_cache()
+    st.choose_records()
     hbm, hbm_kind = peaks()
     for _ in range(args.warmup):
         st.step()
@@ -624,6 +652,7 @@ def run_ours(args, rank, world, local_rank):
         "step_roofline": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / hbm, 4),
                           "bytes_per_voxel": BYTES_PER_VOXEL[loss]},
         "kernel_ms": {k: round(v, 5) for k, v in kern_ms.items()},
+        "mi_records": getattr(st, "records_note", None),
         "gpu_launches": st.launches_per_step * args.steps,
         "clocks": clocks.summary(),
         "e2e": e2e,

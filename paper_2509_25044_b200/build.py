@@ -103,10 +103,31 @@ def build_ref_backend(verbose: bool = False) -> None:
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref-backend"], check=True)
 
 
+CPP_PLAN_SRC = os.path.join(ROOT, "tests", "cpp", "test_plan.cpp")
+CPP_PLAN_BIN = os.path.join(ROOT, "tests", "cpp", "test_plan")
+
+
+def build_cpp_plan_test(force: bool = False, verbose: bool = False) -> str:
+    """The native sharded plan from C++ with one std::thread per rank (tests/cpp/test_plan.cpp)."""
+    cuda = os.path.dirname(os.path.dirname(nvcc()))
+    deps = [CPP_PLAN_SRC, os.path.join(ROOT, "include", "ffdp", "voxreg.hpp"), os.path.join(ROOT, "include", "ffdp.h"),
+            LIB]
+    if force or _stale(CPP_PLAN_BIN, deps):
+        cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-I" + os.path.join(ROOT, "include"),
+               "-I" + os.path.join(cuda, "include"), CPP_PLAN_SRC, "-o", CPP_PLAN_BIN, "-L" + HERE,
+               "-L" + os.path.join(cuda, "lib64"), "-lffdp", "-lcudart", "-lpthread",
+               "-Wl,-rpath,$ORIGIN/../../paper_2509_25044_b200:" + os.path.join(cuda, "lib64")]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return CPP_PLAN_BIN
+
+
 def build_all(verbose: bool = False) -> None:
     build_lib(verbose=verbose)
     build_oracle(verbose=verbose)
     build_cpp_tests(verbose=verbose)
+    build_cpp_plan_test(verbose=verbose)
     build_ref_backend(verbose=verbose)
 
 

@@ -41,6 +41,17 @@ namespace l3 {
 #ifndef FFDP_L3_ROWS
 #define FFDP_L3_ROWS 1
 #endif
+// L2 prefetch of the moving image (bulk tensor prefetch, one box per plane and CTA): the
+// box of the zero-bordered window starting MPF_X / MPF_Y before the tile (bordered
+// coordinates; the start column stays 16-byte aligned), MPF_W x MPF_H, MPF_D planes ahead
+#ifndef FFDP_L3_MPF_D
+#define FFDP_L3_MPF_D 2
+#endif
+#ifndef FFDP_L3_MPF_PAD
+#define FFDP_L3_MPF_PAD 1
+#endif
+constexpr int MPF_D = FFDP_L3_MPF_D, MPF_X = 4 + 4 * FFDP_L3_MPF_PAD, MPF_Y = 3 + 4 * FFDP_L3_MPF_PAD;
+constexpr int MPF_W = 48 + 8 * FFDP_L3_MPF_PAD, MPF_H = 32 + 10 + 8 * FFDP_L3_MPF_PAD;
 constexpr int R = 3, WIN = 7, TX = 32, TY = 32, HX = TX + 2 * R, HY = TY + 2 * R;
 constexpr int NT = 512;                                        // threads: moment warps + sampler warps
 constexpr int NPOS = HX * HY, NIN = TX * TY;                   // 1444 haloed positions, 1024 outputs
@@ -248,7 +259,7 @@ __device__ __forceinline__ void sampler_warps(const CUtensorMap* umap, const CUt
             // u and the moving planes of plane p + 2 into L2 (bulk tensor prefetches): the batch
             // loads and, for moderate displacements, the corner gathers then hit L2, not HBM
             tma_prefetch_3d(umap, 3 * (x0 - R - 1), y0 - R, (int)(p + 2 - P.buf_z0));
-            tma_prefetch_3d(mmap, x0 - 4, y0 - R, (int)(p + 2 - P.g.wz0 + 2));
+            tma_prefetch_3d(mmap, x0 - MPF_X, y0 - MPF_Y, (int)(p + MPF_D - P.g.wz0 + 2));
         }
         const double zd = (double)p;
         double cb[3];  // coordinate base of position i (advanced per i)
@@ -383,7 +394,7 @@ __device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUte
         const bool wantG = p >= zc0 && p < zc1;
         if (TMA && st == 0 && p + 2 < pend) {
             tma_prefetch_3d(umap, 3 * (x0 - R - 1), y0 - R, (int)(p + 2 - P.buf_z0));
-            tma_prefetch_3d(mmap, x0 - 4, y0 - R, (int)(p + 2 - P.g.wz0 + 2));
+            tma_prefetch_3d(mmap, x0 - MPF_X, y0 - MPF_Y, (int)(p + MPF_D - P.g.wz0 + 2));
         }
         const double zd = (double)p;
         double bzm[3], bze[3];
@@ -825,7 +836,7 @@ int lncc3_step(const float* f, const float* u, const ffdp_dims& d, const ffdp_sl
         };
         const cuuint64_t mx = m.dims.nx + 4, my = m.dims.ny + 4, mz = m.z_end - m.z_begin + 4;
         tma = tma && make(&map[0], f, d.nx, d.ny, d.nz, FW, HY) && make(&map[1], u, 3 * d.nx, d.ny, d.nz, 3 * FW, HY) &&
-              make(&map[2], m.data, mx, my, mz, 48, HY + 4);
+              make(&map[2], m.data, mx, my, mz, MPF_W, MPF_H);
     }
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
     const bool o32 = window_off32(P.g);

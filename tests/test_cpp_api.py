@@ -24,3 +24,18 @@ def test_cpp_mirror_parity_suite():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
+
+
+def test_cpp_plan_test_compiles():
+    assert os.path.exists(build.build_cpp_plan_test())
+
+
+@pytest.mark.gpu
+def test_cpp_sharded_plan_threads_and_nccl():
+    """ffdp_plan_* from C++: in-process groups of 1-4 ranks (threads sharing cuda:0) and
+    NCCL at world 1 (world 2 with two devices) against the single-GPU step, bit for bit."""
+    b = build.build_cpp_plan_test()
+    r = subprocess.run([b], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
