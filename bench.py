@@ -807,7 +807,12 @@ def run_e2e(args, st, f, u, A, t, loss, world):
     nbytes = 4 * (f.numel() + m.numel() + u.numel())
     steps = max(3, min(args.steps, 20 if nbytes <= (8 << 30) else 3))
     staged = nbytes > (8 << 30)
-    hf, hm, hu = (x.cpu().contiguous() for x in (f, m, u))
+    hf, hu = f.cpu(), u.cpu()
+    # M's host copy from the bordered layout a few planes at a time (a strided view: a whole-
+    # volume device temporary would not fit next to configs[4]'s records)
+    hm = torch.empty(tuple(m.shape), dtype=torch.float32)
+    for z0 in range(0, m.shape[0], 16):
+        hm[z0:z0 + 16].copy_(m[z0:z0 + 16])
     if not staged:
         hf, hm, hu = (x.pin_memory() for x in (hf, hm, hu))
         cp = lambda dst, src: dst.copy_(src, non_blocking=True)
