@@ -26,7 +26,7 @@ from ncu_raw_summary import WANT  # noqa: E402
 
 OURS = re.compile(r"k_step_|k_hist_to_raw|k_mi_finalize|k_zero|k_reduce|k_pad|k_sampler|k_lncc|k_mi_|k_conv|"
                   r"k_add_partials|k_smooth|k_trilinear|k_normalize|k_mse|k_jacobian")
-VOXELS = {"mi256": 256 ** 3, "lncc720": 720 * 640 * 720, "wu720": 720 * 640 * 720}
+VOXELS = {"mi256": 256 ** 3, "lncc720": 720 * 640 * 720, "wu720": 720 * 640 * 720, "mi1760": 1760 * 1760 * 1200}
 
 
 def short(name):
@@ -101,7 +101,9 @@ def main(tag, d):
         traffic = json.load(open(tp))
     for p in sorted(glob.glob(os.path.join(d, "full_*.ncu-rep"))):
         k = os.path.basename(p)[len("full_"):-len(".ncu-rep")]
-        wl = "lncc720" if "lncc" in k else "wu720" if k.startswith("wu") else "mi256"  # full_<kernel>
+        # full_<kernel>[_<workload>] or full_<workload>
+        wl = next((w for w in VOXELS if w in k), None) or (
+            "lncc720" if "lncc" in k else "wu720" if k.startswith("wu") else "mi256")
         for name, v in full(p, f"profiles/{tag}_full_{k}.txt", wl).items():
             v["round"] = tag
             traffic[name] = v
