@@ -539,11 +539,18 @@ def run_local_group(args):
             err.append(e)
             barrier.abort()
 
-    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    th = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(world)]
     for x in th:
         x.start()
-    for x in th:
-        x.join()
+    # a rank that fails leaves its peers inside a collective: report it instead of waiting
+    while any(x.is_alive() for x in th):
+        for x in th:
+            x.join(timeout=0.5)
+        if err:
+            import traceback
+            traceback.print_exception(err[0], file=sys.stderr)
+            sys.stderr.flush()
+            os._exit(1)
     if err:
         raise err[0]
     for pl in plans:

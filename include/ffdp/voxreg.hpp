@@ -517,6 +517,7 @@ struct LossParams {
     int bins = 32;
     bool mi_bspline_kernel = false;  // the reference default (registration.hpp:40)
     bool mi_approx_forward = false;
+    bool lncc_naive_backend = false;  // registration.hpp:38: same values as the fused path here
 };
 
 struct StepResult {
@@ -946,10 +947,26 @@ inline AffineMap affine_stage(const Volume3& fixed, const Volume3& moving, const
     return map;
 }
 
+// DeformableOptions (registration.hpp:221-226): shards > 1 runs the stage z-sharded over a
+// WorkerGroup (one rank per visible device, round robin); gp_sync = false is the
+// reference's halo-free smoothing ablation.
+struct DeformableOptions {
+    int shards = 1;
+    bool gp_sync = true;
+};
+
+// deformable_stage with the reference's parameter order (registration.hpp:230-234), the
+// stream as a trailing extra; defined after the sharded context below.
+inline WarpField deformable_stage(const Volume3& fixed, const Volume3& moving, const AffineMap& affine,
+                                  const ScaleSchedule& schedule, const DeformableOptions& opts,
+                                  std::vector<TraceEntry>* trace = nullptr, int scale_index_base = 0,
+                                  std::vector<std::int64_t>* worker_peak_bytes = nullptr, cudaStream_t s = nullptr);
+
 // RegistrationConfig / RegistrationResult / register_volumes (registration.hpp:333-368).
 struct RegistrationConfig {
     ScaleSchedule affine;
     ScaleSchedule deformable;
+    DeformableOptions deformable_opts;
     bool skip_affine = false;
 };
 
@@ -969,7 +986,8 @@ inline RegistrationResult register_volumes(const Volume3& fixed, const Volume3& 
         res.affine = affine_stage(f_n, m_n, config.affine, &res.trace, 0, s);
         base = static_cast<int>(config.affine.steps.size());
     }
-    res.warp = deformable_stage(f_n, m_n, res.affine, config.deformable, &res.trace, base, s);
+    res.warp = deformable_stage(f_n, m_n, res.affine, config.deformable, config.deformable_opts, &res.trace, base,
+                                nullptr, s);
     const Dims3 d = res.warp.dims;
     if (d.nx >= 3 && d.ny >= 3 && d.nz >= 3) res.jacobian_positive_fraction = jacobian_positive_fraction(res.warp, s);
     return res;
@@ -1228,6 +1246,120 @@ inline std::pair<double, std::vector<WarpField>> dist_step(const WorkerGroup& g,
                          args.A.m, args.t.v, p.window, p.epsilon, p.kind == LossKind::mi ? &kc : nullptr, &loss,
                          o.data()));
     return {loss, std::move(out)};
+}
+
+// deformable_stage (registration.hpp:230-331) with DeformableOptions. shards == 1: the
+// single-GPU stage above. shards > 1: per scale F_s, M_s and the carried warp are scattered
+// into z slabs (shard_ranges), and per iteration every rank runs the reference's sequence
+// over the group: the fused step (ffdp_dist_step) for LNCC / exact MI, else ring_sample ->
+// dist_mse | dist_lncc | dist_mi -> ring_sample_backward(warp); then gp_convolve(g_u) (halo'd,
+// or not with gp_sync = false), adam_step per rank and gp_convolve(u). worker_peak_bytes
+// receives each rank device's used memory at the end of each scale.
+inline WarpField deformable_stage(const Volume3& fixed, const Volume3& moving, const AffineMap& affine,
+                                  const ScaleSchedule& schedule, const DeformableOptions& opts,
+                                  std::vector<TraceEntry>* trace, int scale_index_base,
+                                  std::vector<std::int64_t>* worker_peak_bytes, cudaStream_t s) {
+    schedule.validate();
+    if (opts.shards < 1) throw std::invalid_argument("deformable_stage: shards must be >= 1");
+    if (schedule.loss.lncc_naive_backend && opts.shards > 1)
+        throw std::invalid_argument("deformable_stage: the naive LNCC backend is single-worker");
+    if (opts.shards == 1) {
+        WarpField w = deformable_stage(fixed, moving, affine, schedule, trace, scale_index_base, s);
+        if (worker_peak_bytes) {
+            std::size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            worker_peak_bytes->push_back(static_cast<std::int64_t>(tot - fr));
+        }
+        return w;
+    }
+    if (!fixed.same_lattice(moving))
+        throw std::invalid_argument("deformable_stage: F and M must share a lattice (registration.hpp:268-270)");
+    int ndev = 1;
+    check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    std::vector<int> devices;
+    for (int r = 0; r < opts.shards; ++r) devices.push_back(r % std::max(1, ndev));
+    WorkerGroup g(opts.shards, devices);
+    const SamplerArgs args = [&] {
+        SamplerArgs a;
+        a.A = affine.matrix;
+        a.t = affine.translation;
+        return a;
+    }();
+    const auto taps_grad = gaussian_taps(schedule.sigma_grad), taps_warp = gaussian_taps(schedule.sigma_warp);
+    std::optional<WarpField> warp;
+    for (std::size_t sc = 0; sc < schedule.steps.size(); ++sc) {
+        const auto& step = schedule.steps[sc];
+        const double factor = 1.0 / step.downsample;
+        std::optional<Volume3> fr, mr;
+        if (factor != 1.0) {
+            fr.emplace(resample_scale(fixed, factor, s));
+            mr.emplace(resample_scale(moving, factor, s));
+        }
+        const Volume3& f_s = fr ? *fr : fixed;
+        const Volume3& m_s = mr ? *mr : moving;
+        warp = warp ? resample_warp(*warp, f_s.dims, s) : WarpField::zeros(f_s.dims, s);
+        check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        const Dims3 d = f_s.dims;
+        if (d.nz < opts.shards) throw std::invalid_argument("deformable_stage: fewer planes than shards");
+        const double pitch = (2.0 / static_cast<double>(d.nx - 1) + 2.0 / static_cast<double>(d.ny - 1) +
+                              2.0 / static_cast<double>(d.nz - 1)) / 3.0;
+        const double lr_norm = schedule.lr * pitch;
+        const std::vector<Volume3> f_sh = g.scatter(f_s), m_sh = g.scatter(m_s);
+        std::vector<WarpField> u_sh = g.scatter(*warp);
+        std::vector<AdamState> adam;
+        for (int r = 0; r < opts.shards; ++r) {
+            DeviceScope ds(g.device(r));
+            adam.push_back(AdamState::zeros(u_sh[(std::size_t)r].data.size()));
+        }
+        std::vector<TraceEntry> scale_trace;
+        for (int it = 0; it < step.iterations; ++it) {
+            double loss = 0;
+            std::vector<WarpField> g_u;
+            if (fused_loss(schedule.loss)) {
+                auto r = dist_step(g, f_sh, m_sh, u_sh, d, args, schedule.loss);
+                loss = r.first;
+                g_u = std::move(r.second);
+            } else {
+                const auto moved = ring_sample(g, m_sh, d, u_sh, d, args.A, args.t);
+                DistLoss dl;
+                const LossParams& p = schedule.loss;
+                if (p.kind == LossKind::mse)
+                    dl = dist_mse(g, f_sh, moved, d);
+                else if (p.kind == LossKind::lncc)
+                    dl = dist_lncc(g, f_sh, moved, d, p.window, p.epsilon, p.ants_approx, opts.gp_sync);
+                else
+                    dl = dist_mi(g, f_sh, moved, d,
+                                 p.mi_bspline_kernel ? ParzenKernel::bspline3(p.bins) : ParzenKernel::gaussian(p.bins),
+                                 p.mi_approx_forward);
+                loss = dl.loss;
+                SamplerGradWant want;
+                want.warp = true;
+                g_u = std::move(*ring_sample_backward(g, dl.grad_moved, m_sh, d, u_sh, d, args.A, args.t, want).warp);
+            }
+            if (!std::isfinite(loss))
+                throw NumericalError("deformable stage diverged (non-finite loss)",
+                                     trace ? *trace : std::vector<TraceEntry>{});
+            scale_trace.push_back({scale_index_base + static_cast<int>(sc), it, loss});
+            // registration.hpp:313-317 on the slabs: smoothed gradient (halo'd), Adam, smoothed warp
+            auto g_s = gp_convolve(g, g_u, d, taps_grad, EdgeMode::renormalize, opts.gp_sync);
+            for (int r = 0; r < opts.shards; ++r) {
+                DeviceScope ds(g.device(r));
+                adam_step(u_sh[(std::size_t)r], g_s[(std::size_t)r], adam[(std::size_t)r], lr_norm);
+            }
+            u_sh = gp_convolve(g, u_sh, d, taps_warp, EdgeMode::renormalize, opts.gp_sync);
+        }
+        warp = g.gather(u_sh, d);
+        if (trace) trace->insert(trace->end(), scale_trace.begin(), scale_trace.end());
+        if (worker_peak_bytes)
+            for (int r = 0; r < opts.shards; ++r) {
+                DeviceScope ds(g.device(r));
+                std::size_t fr2 = 0, tot = 0;
+                cudaMemGetInfo(&fr2, &tot);
+                worker_peak_bytes->push_back(static_cast<std::int64_t>(tot - fr2));
+            }
+    }
+    if (warp->dims != fixed.dims) warp = resample_warp(*warp, fixed.dims, s);
+    return std::move(*warp);
 }
 
 }  // namespace voxreg

@@ -302,6 +302,9 @@ constexpr int HDUMMY = HPAD == 2 ? 4 : 0;  // dummy rows per copy (HPAD 2)
 // of few voxels: measured against the oracle, g_u agrees to 1.4e-6 (140k voxels) ..
 // 2.5e-6 (96^3) at either scale, while 4k-voxel slabs of the sharded step drift past the
 // 1e-5 loss gate over a multi-iteration stage at 2^21.
+#ifndef FFDP_REC_STREAM
+#define FFDP_REC_STREAM 0
+#endif
 #ifndef FFDP_MI_BS_LARGE_MIN
 #define FFDP_MI_BS_LARGE_MIN (1 << 17)
 #endif
@@ -402,7 +405,15 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
                 if (REC) {
                     float d[3];
                     mw = interp_grad(cr[k], c[k], d);
-                    if (ok[k]) *rp = make_float4(mw, P.g.dscale[0] * d[0], P.g.dscale[1] * d[1], P.g.dscale[2] * d[2]);
+                    if (ok[k]) {
+                        const float4 rv = make_float4(mw, P.g.dscale[0] * d[0], P.g.dscale[1] * d[1], P.g.dscale[2] * d[2]);
+                        // FFDP_REC_STREAM: evict-first stores (the records are read once, by pass 2),
+                        // so the streaming 16 B/voxel do not push the moving image's lines out of L2
+                        if (FFDP_REC_STREAM)
+                            __stcs(rp, rv);
+                        else
+                            *rp = rv;
+                    }
                     rp += P.nx;
                 } else {
                     mw = interp(cr[k], c[k]);

@@ -638,6 +638,45 @@ static void comm_tests() {
             EXPECT_TRUE(rel(ds.first, r1.loss) <= 1e-5);
             EXPECT_TRUE(maxrel_f(g.gather(ds.second, d).to_host(), g1.to_host()) <= 1e-4);
         }
+        // deformable_stage with DeformableOptions (the reference's parameter order): shards 2 / 3
+        // over a WorkerGroup sharing device 0 against the single-GPU stage, every loss kind
+        for (int kind = 0; kind < 3; ++kind) {
+            Pair p = make_pair(22, 20, 18, 4242, kind == 2);
+            V::ScaleSchedule sch;
+            sch.steps = {V::ScaleStep{2, 2}, V::ScaleStep{1, 2}};
+            sch.loss.kind = kind == 0 ? V::LossKind::lncc : kind == 1 ? V::LossKind::mse : V::LossKind::mi;
+            sch.loss.mi_bspline_kernel = true;
+            sch.lr = 0.1;
+            V::AffineMap aff;
+            for (int i = 0; i < 9; ++i) aff.matrix.m[i] = p.A[i];
+            for (int i = 0; i < 3; ++i) aff.translation[i] = p.t[i];
+            const auto F = V::Volume3::from_host(dims(p.d), p.f.data()), M = V::Volume3::from_host(dims(p.d), p.m.data());
+            std::vector<V::TraceEntry> t1;
+            const auto w1 = V::deformable_stage(F, M, aff, sch, V::DeformableOptions{}, &t1).to_host();
+            for (int shards : {2, 3}) {
+                std::vector<V::TraceEntry> tn;
+                std::vector<std::int64_t> peaks;
+                V::DeformableOptions o;
+                o.shards = shards;
+                const auto wn = V::deformable_stage(F, M, aff, sch, o, &tn, 0, &peaks).to_host();
+                double tr = 0;
+                for (size_t i = 0; i < t1.size(); ++i) tr = std::max(tr, rel(tn[i].loss, t1[i].loss));
+                std::printf("  sharded stage kind %d H=%d: trace rel %.3g, warp maxrel %.3g\n", kind, shards, tr,
+                            maxrel_f(wn, w1));
+                EXPECT_TRUE(tn.size() == t1.size() && tr <= 1e-5);
+                EXPECT_TRUE(maxrel_f(wn, w1) <= 1e-3);
+                EXPECT_TRUE(peaks.size() == size_t(2 * shards));
+            }
+        }
+        {
+            V::DeformableOptions bad;
+            bad.shards = 0;
+            V::ScaleSchedule sch;
+            sch.steps = {V::ScaleStep{1, 1}};
+            EXPECT_THROW(V::deformable_stage(V::Volume3::zeros(V::Dims3{8, 8, 8}), V::Volume3::zeros(V::Dims3{8, 8, 8}),
+                                             V::AffineMap{}, sch, bad),
+                         std::invalid_argument);
+        }
         EXPECT_THROW(V::WorkerGroup(2, std::vector<int>{0}), std::invalid_argument);
         EXPECT_THROW(V::WorkerGroup(2, std::vector<int>{0, 99}), std::invalid_argument);
         V::WorkerGroup g3(3, std::vector<int>(3, 0));
