@@ -839,7 +839,7 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
         // reproduces the single-GPU histogram exactly)
         const bool large = scale_exp ? scale_exp == 21 : mi_bs_scale_exp(d.nx * d.ny * (s.z_end - s.z_begin)) == 21;
         P.fix_scale = large ? 2097152.0f : 8388608.0f;  // 2^21 / 2^23
-        const int sel = (full ? 1 : 0) | (rec ? 2 : 0) | (B == 32 ? 4 : 0) | (om * 8) | (large ? 24 : 0);
+        const int sel = (full ? 1 : 0) + (rec ? 2 : 0) + (B == 32 ? 4 : 0) + om * 8 + (large ? 24 : 0);
 #define FFDP_BS_ROW(O, S)                                                                                        \
     k_mi_hist_bs<false, false, 0, O, S>, k_mi_hist_bs<true, false, 0, O, S>, k_mi_hist_bs<false, true, 0, O, S>,     \
         k_mi_hist_bs<true, true, 0, O, S>, k_mi_hist_bs<false, false, 32, O, S>, k_mi_hist_bs<true, false, 32, O, S>, \
@@ -899,7 +899,7 @@ int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_
             for (auto fn : ks)
                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(sizeof(float) * grad_tab_floats(64)));
-        const int sel = (full ? 1 : 0) | (B == 32 ? 2 : 0) | (window_off_mode(P.g) * 4);
+        const int sel = (full ? 1 : 0) + (B == 32 ? 2 : 0) + window_off_mode(P.g) * 4;
         const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((P.nunits + NT / 32 - 1) / (NT / 32),
                                                                   (int64_t)FFDP_MI_G2_MINB * num_sms()));
         ks[sel]<<<g2, NT, tab, st>>>(P);
