@@ -111,11 +111,9 @@ int num_sms() {
     return cached;
 }
 
-bool first_on_device(std::atomic<unsigned long long>& mask) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const unsigned long long bit = 1ull << (dev & 63);
-    return !(mask.fetch_or(bit) & bit);
+std::mutex& once_mutex() {
+    static std::mutex m;
+    return m;
 }
 
 // The library's own stream-ordered pool per device (never the process's default pool, so

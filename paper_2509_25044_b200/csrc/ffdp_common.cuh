@@ -9,6 +9,7 @@
 #pragma once
 
 #include <atomic>
+#include <mutex>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -561,8 +562,21 @@ int num_sms();
 cudaMemPool_t device_pool(int dev);
 void* scratch_alloc(size_t bytes, cudaStream_t s);
 void scratch_free(void* p, cudaStream_t s);
-// true the first time it is called for the current device (per-device kernel attributes)
-bool first_on_device(std::atomic<unsigned long long>& mask);
+// Runs setup() once per device per call site (per-device kernel attributes), thread-safe:
+// a second host thread driving the same device (a sharded plan's ranks) waits until the
+// first has set the attributes instead of launching before them.
+std::mutex& once_mutex();
+template <class F>
+void once_per_device(std::atomic<unsigned long long>& mask, F&& setup) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    std::lock_guard<std::mutex> lock(once_mutex());
+    if (mask.load(std::memory_order_relaxed) & bit) return;
+    setup();
+    mask.fetch_or(bit, std::memory_order_release);
+}
 
 }  // namespace ffdp
 

@@ -298,13 +298,13 @@ int launch(Params P, cudaStream_t st) {
     const size_t smem = sizeof(Smem<R, CH>);
     static std::atomic<unsigned long long> attr_mask{0};
     static int per_sm = 1;
-    if (first_on_device(attr_mask)) {
+    once_per_device(attr_mask, [&] {
         for (auto fn : {k_smooth<R, CH, ADAM, true>, k_smooth<R, CH, ADAM, false>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int p = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, k_smooth<R, CH, ADAM, true>, NT, smem);
         per_sm = std::max(p, 1);
-    }
+    });
     const bool v16 = ((uintptr_t)P.in & 15) == 0 && (P.nx * CH) % 4 == 0;
     const int64_t tx = (P.nx + TX - 1) / TX, ty = (P.ny + TY - 1) / TY;
     const int64_t nzs = P.z_end - P.z_begin;

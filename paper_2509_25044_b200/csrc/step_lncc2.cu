@@ -497,13 +497,13 @@ int lncc2_step(const float* f, const float* u, const ffdp_dims& d, const ffdp_sl
     M.sm = shift_m;
     static std::atomic<unsigned long long> attr_mask{0};
     static int per_sm = 1;
-    if (first_on_device(attr_mask)) {
+    once_per_device(attr_mask, [&] {
         cudaFuncSetAttribute(k_lncc_moments<TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(typename T::Smem));
         int p = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, k_lncc_moments<TX, TY>, T::NT, sizeof(typename T::Smem));
         per_sm = std::max(p, 1);
-    }
+    });
     const int64_t tx = (d.nx + TX - 1) / TX, ty = (d.ny + TY - 1) / TY;
     const int64_t nzs = s.z_end - s.z_begin;
     M.zchunk = pick_zchunk(tx * ty, nzs, (int64_t)per_sm * num_sms());

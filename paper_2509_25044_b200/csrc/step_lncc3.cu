@@ -752,9 +752,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <int NM_, bool T_, bool F_, bool O_>
 static void launch_fused(const CUtensorMap (&map)[3], const l3::Params& P, dim3 grid, cudaStream_t st) {
     static std::atomic<unsigned long long> attr_mask{0};
-    if (first_on_device(attr_mask))
+    once_per_device(attr_mask, [] {
         cudaFuncSetAttribute(l3::k_lncc_fused<NM_, T_, F_, O_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(l3::Smem));
+    });
     l3::k_lncc_fused<NM_, T_, F_, O_><<<grid, l3::NT, sizeof(l3::Smem), st>>>(map[0], map[1], map[2], P);
 }
 

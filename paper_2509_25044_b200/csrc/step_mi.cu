@@ -822,10 +822,10 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
     P.miss = miss;
     P.rec = reinterpret_cast<float4*>(rec);
     static std::atomic<unsigned long long> attr_mask{0};  // opt in to > 48 KB dynamic shared memory
-    if (first_on_device(attr_mask)) {
+    once_per_device(attr_mask, [&] {
         for (auto fn : {k_step_mi_hist<false, true, false>, k_step_mi_hist<false, false, false>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
-    }
+    });
     const int64_t chunks = (P.nunits + HNT / 32 - 1) / (HNT / 32);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (int64_t)num_sms()));
     const bool full = m.z_begin == 0 && m.z_end == m.dims.nz;
@@ -849,7 +849,7 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
             FFDP_BS_ROW(0, 21), FFDP_BS_ROW(1, 21), FFDP_BS_ROW(2, 21)};
 #undef FFDP_BS_ROW
         static std::atomic<unsigned long long> bs_attr{0};
-        if (first_on_device(bs_attr)) {
+        once_per_device(bs_attr, [&] {
             // the smallest shared-memory carve-out that holds the histogram: the rest is L1,
             // which the gather needs (percent of the 228 KB maximum, rounded up)
             const int pct = (int)std::min<size_t>(100, (smem + 2048) * 100 / (228 * 1024) + 1);
@@ -857,7 +857,7 @@ int mi_quad_hist(const float* f, const float* u, const ffdp_dims& d, const ffdp_
                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxHistSmem);
                 cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             }
-        }
+        });
         table_[sel]<<<grid, HNT, smem, st>>>(P);
     } else {
         const size_t smem = hist_smem_bytes(B);
@@ -895,10 +895,11 @@ int mi_quad_grad(const float* f, const float* u, const ffdp_dims& d, const ffdp_
 #define FFDP_G2_ROW(O) k_mi_grad_bs<false, 0, O>, k_mi_grad_bs<true, 0, O>, k_mi_grad_bs<false, 32, O>, k_mi_grad_bs<true, 32, O>
         static const K ks[12] = {FFDP_G2_ROW(0), FFDP_G2_ROW(1), FFDP_G2_ROW(2)};
 #undef FFDP_G2_ROW
-        if (first_on_device(attr_mask))
+        once_per_device(attr_mask, [&] {
             for (auto fn : ks)
                 cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(sizeof(float) * grad_tab_floats(64)));
+        });
         const int sel = (full ? 1 : 0) + (B == 32 ? 2 : 0) + window_off_mode(P.g) * 4;
         const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((P.nunits + NT / 32 - 1) / (NT / 32),
                                                                   (int64_t)FFDP_MI_G2_MINB * num_sms()));
@@ -926,10 +927,10 @@ int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ff
     const int64_t n = d.nx * d.ny * (s.z_end - s.z_begin);
     const size_t smem = sizeof(float) * grad_tab_floats(B);
     static std::atomic<unsigned long long> attr_mask{0};  // B up to 64: the 4 table copies may exceed 48 KB
-    if (first_on_device(attr_mask)) {
+    once_per_device(attr_mask, [&] {
         for (auto fn : {k_step_mi_grad_rec<true>, k_step_mi_grad_rec<false>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * grad_tab_floats(64)));
-    }
+    });
     const bool vec = (((uintptr_t)fi | (uintptr_t)rec | (uintptr_t)g_u) & 15) == 0;
     const int64_t work = vec ? n / 4 : n;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)FFDP_GR_CTAS * num_sms()));

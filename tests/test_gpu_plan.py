@@ -284,3 +284,38 @@ def test_plan_argument_errors(V, PL):
         p.close()
     finally:
         g.close()
+
+
+def test_first_use_from_many_threads_in_a_fresh_process():
+    """Kernel attributes are set lazily per device on first use: 4 rank threads reaching the
+    same launch sites at once in a fresh process must all launch after the setup (a race
+    here failed with 'invalid argument' on the > 48 KB shared-memory kernels)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, threading, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "from oracle import Oracle, step_inputs\n"
+        "from paper_2509_25044_b200 import plan as PL, voxreg as V\n"
+        "orc = Oracle()\n"
+        "for loss in ('mi', 'lncc'):\n"
+        "    si = step_inputs(orc, (64, 40, 36), seed=11, loss=loss)\n"
+        "    p = V.LossParams(kind=loss, bins=32, mi_bspline_kernel=True)\n"
+        "    d = lambda a: torch.from_numpy(np.asarray(a, dtype=np.float32)).cuda()\n"
+        "    gs = PL.local_group(4, [0] * 4); out = [None] * 4; err = []\n"
+        "    def rank(r):\n"
+        "        try:\n"
+        "            torch.cuda.set_device(0)\n"
+        "            pl = PL.ShardPlan(gs[r], si.f.shape, p, si.A, si.t)\n"
+        "            pl.load(d(si.f)[pl.lo:pl.hi], d(si.m)[pl.lo:pl.hi]); pl.set_u(d(si.u)[pl.lo:pl.hi])\n"
+        "            out[r] = pl.step(); pl.close()\n"
+        "        except Exception as e:\n"
+        "            err.append(repr(e)); import os; os._exit(3)\n"
+        "    th = [threading.Thread(target=rank, args=(r,)) for r in range(4)]\n"
+        "    [t.start() for t in th]; [t.join() for t in th]\n"
+        "    assert len(set(out)) == 1, out\n"
+        "print('ok')\n") % root
+    for _ in range(3):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
