@@ -577,7 +577,7 @@ def run_ours(args, rank, world, local_rank):
     so = lib.load()
     if so.ffdp_device_check() != 0:
         raise RuntimeError(so.ffdp_last_error().decode())
-    if world > 1:
+    if world > 1 or getattr(args, "force_plan", False):
         return run_sharded(args, rank, world, local_rank, dev), None
     shape, loss, cfg = WORKLOADS[args.workload]
     jitter = getattr(args, "jitter", "bench")
@@ -931,6 +931,8 @@ def main():
                     help="N > 1: split the N = 1 volume (strong) or grow it N x along z (weak)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "local"],
                     help="N > 1: one process per GPU over NCCL (torchrun), or N ranks as threads of one process")
+    ap.add_argument("--force-plan", action="store_true",
+                    help="run the native sharded plan over NCCL even at one rank (a functional check of the N > 1 path)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.workload == "auto":
@@ -991,11 +993,11 @@ def main():
     if args.transport == "local" and args.gpus > 1:
         print(json.dumps(run_local_group(args)))
         return
-    if world > 1:
+    if world > 1 or args.force_plan:
         import torch.distributed as dist
         dist.init_process_group("nccl")
     out, st = run_ours(args, rank, world, local_rank)
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.force_plan:
         import torch
         del st
         torch.cuda.empty_cache()
@@ -1036,7 +1038,7 @@ def main():
             out["warp_update"] = run_warp_update(WORKLOADS["lncc720"][0], max(5, min(args.steps, 20)), hbm, hbm_kind)
             torch.cuda.empty_cache()
             out["registration"] = run_registration(WORKLOADS["lncc720"][0], [(4, 20), (2, 20), (1, 10)])
-    if world > 1:
+    if world > 1 or args.force_plan:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
