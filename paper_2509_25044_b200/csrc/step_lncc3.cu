@@ -41,6 +41,10 @@ namespace l3 {
 #ifndef FFDP_L3_ROWS
 #define FFDP_L3_ROWS 1
 #endif
+// FFDP_L3_MROWS = 1: the moment warps' z stage in the row layout too (moment_rows)
+#ifndef FFDP_L3_MROWS
+#define FFDP_L3_MROWS 0
+#endif
 // L2 prefetch of the moving image (bulk tensor prefetch, one box per plane and CTA): the
 // box of the zero-bordered window starting MPF_X / MPF_Y before the tile (bordered
 // coordinates; the start column stays 16-byte aligned), MPF_W x MPF_H, MPF_D planes ahead
@@ -662,6 +666,181 @@ __device__ __forceinline__ float moment_warps(const CUtensorMap* fmap, const Par
     return poison ? __int_as_float(0x7fc00000) : nsum;
 }
 
+// Row-mapped moment warps (FFDP_L3_MROWS): the z stage takes the positions of the row
+// sampler's layout (main rows w + 8 j at column 3 + lane, edge position 32 w + lane), so
+// every shared-memory offset is a row base plus the lane (no per-position decode to keep in
+// registers), and x jobs decode as (row-of-channel j >> 3, run j & 7). The handshake with
+// the samplers and the y stage / finalize are those of moment_warps.
+template <bool TMA>
+__device__ __forceinline__ float moment_rows(const CUtensorMap* fmap, const Params& P, Smem& sm, int mt,
+                                             int64_t pstart, int64_t pend, int64_t zc0, int x0, int y0, float sf,
+                                             float kF, float smv, float kM) {
+    constexpr int NM = 256, OUTR = NIN / NM, MR = SROWS, NJ = MR + 1;
+    const int lane = mt & 31, w = mt >> 5;
+    const float nsfk = -sf * kF, ikM = 1.0f / kM;
+    auto issue = [&](int64_t p, int s) {
+        mbar_expect_tx(&sm.fbar[s], FW * HY * 4);
+        tma_load_3d(&sm.fr[s][0], fmap, &sm.fbar[s], x0 - R - 1, y0 - R, (int)(p - P.buf_z0));
+    };
+    if (TMA && mt == 0) issue(pstart, 0);
+    const int nx = P.nx, ny = P.ny;
+    const int nrows = w < 6 ? SROWS : SROWS - 1;
+    const bool vxm = x0 + lane < nx;
+    const int e = 32 * w + lane;
+    const int erow = e / 6, ecol = e - 6 * (e / 6);
+    const int ehx = ecol < 3 ? ecol : TX + ecol;
+    const bool ehas = e < NEDGE;
+    const bool ve = ehas && x0 - R + ehx >= 0 && x0 - R + ehx < nx && y0 - R + erow >= 0 && y0 - R + erow < ny;
+    const float* fsrc = P.f + (pstart - P.buf_z0) * P.plane;  // LDG path: F of plane p
+    const int ox = lane, oy = OUTR * w;
+    const int gx = x0 + ox;
+    bool vout[OUTR];
+    int cxy[OUTR];
+#pragma unroll
+    for (int j = 0; j < OUTR; ++j) {
+        vout[j] = gx < nx && y0 + oy + j < ny;
+        cxy[j] = win_count(gx, nx) * win_count(y0 + oy + j, ny);
+    }
+    const int64_t pl3 = 3 * P.plane;
+    float* go = P.g_u + 3 * ((zc0 - P.z_begin) * P.plane + (vout[0] ? (int64_t)(y0 + oy) * nx + gx : 0));
+    const int rs = 3 * nx;
+    const float cAB = (float)(1.0 / (NWIN * NWIN * (double)QSCALE * (double)QSCALE));
+    const float cA = cAB / (kF * kM), cB = cAB / (kF * kF), cC = cAB / (kM * kM);
+    const float mF = (float)(1.0 / (NWIN * (double)QSCALE)) / kF, mM = (float)(1.0 / (NWIN * (double)QSCALE)) / kM;
+    const int32_t NU = (WIN * WIN * WIN) << 21;
+    const float gi2 = 2.0f * (float)P.gi, epsf = (float)P.eps;
+    const bool poison = !(fabsf(sf) <= 3.0e38f && fabsf(smv) <= 3.0e38f);
+
+    int32_t zs[NJ][5];
+#pragma unroll
+    for (int i = 0; i < NJ; ++i)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) zs[i][c] = 0;
+    float nsum = 0.0f;
+
+    for (int64_t p = pstart; p < pend; ++p) {
+        const int it = (int)(p - pstart);
+        const int slot = it % RING;
+        const uint32_t par = (uint32_t)((it / RING) & 1);
+        if (TMA && mt == 0 && p + 1 < pend) issue(p + 1, (it + 1) % RING);
+        const bool vz = p >= 0 && p < P.nz_global;
+        const bool vzo = it >= WIN && p - WIN >= 0 && p - WIN < P.nz_global;
+        const int oslot = (it + RING - WIN) % RING;
+        const bool warm = p < zc0 + R;
+        if (!TMA) {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const bool main = j < MR;
+                if (main ? (j >= nrows) : !ve) continue;
+                const int hy = main ? w + 8 * j : erow, hx = main ? R + lane : ehx;
+                const int gy = y0 - R + hy, gxx = x0 - R + hx;
+                if (main && !(vxm && gy >= 0 && gy < ny)) continue;
+                sm.fr[slot][hy * FW + hx + 1] = vz ? __ldg(fsrc + (int64_t)gy * nx + gxx) : 0.0f;
+            }
+            fsrc += P.plane;
+        }
+        mbar_wait(&sm.sampled[slot], par);
+        if (TMA) mbar_wait(&sm.fbar[slot], par);
+        // ---- z stage: + plane p, - plane p-7 (exact integer sums)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const bool main = j < MR;
+            if (main ? (j >= nrows) : !ehas) continue;
+            const int hy = main ? w + 8 * j : erow, hx = main ? R + lane : ehx;
+            const int gy = y0 - R + hy;
+            const bool ok = main ? (vxm && gy >= 0 && gy < ny) : ve;
+            const int fo = hy * FW + hx + 1, bo = hy * HX + hx;
+            const float an = (ok && vz) ? fmaf(sm.fr[slot][fo], kF, nsfk) : 0.0f;
+            const float ao = (ok && vzo) ? fmaf(sm.fr[oslot][fo], kF, nsfk) : 0.0f;
+            const float bn = sm.br[slot][bo];
+            const float bo_ = it >= WIN ? sm.br[oslot][bo] : 0.0f;
+            int32_t qn[5], qo[5];
+            quant(an, bn, qn);
+            quant(ao, bo_, qo);
+#pragma unroll
+            for (int ch = 0; ch < 5; ++ch) zs[j][ch] += qn[ch] - qo[ch];
+            if (!warm) {
+                int32_t* zb = &sm.zb[0][hy][hx];
+#pragma unroll
+                for (int ch = 0; ch < 5; ++ch) zb[ch * HY * ZP] = zs[j][ch];
+            }
+        }
+        moment_sync<NM>();
+        if (!warm) {
+#pragma unroll
+            for (int i = 0; i < (XJOBS + NM - 1) / NM; ++i) {
+                const int j = mt + NM * i;
+                if (j >= XJOBS) break;
+                const int rowch = j >> 3, run = j & 7;
+                const int4* zr = reinterpret_cast<const int4*>(&sm.zb[0][0][0] + rowch * ZP + 4 * run);
+                const int4 a = zr[0], b = zr[1], c4 = zr[2];
+                const int32_t s0 = a.x + a.y + a.z + a.w + b.x + b.y + b.z;
+                const int32_t s1 = s0 + b.w - a.x;
+                const int32_t s2 = s1 + c4.x - a.y;
+                const int32_t s3 = s2 + c4.y - a.z;
+                *reinterpret_cast<int4*>(&sm.xb[0][0][0] + rowch * TX + 4 * run) = make_int4(s0, s1, s2, s3);
+            }
+            moment_sync<NM>();
+            const int64_t q = p - R;
+            const int qslot = (it + RING - R) % RING, qg = (it + NG - R) % NG;
+            int32_t S[OUTR][5];
+#pragma unroll
+            for (int ch = 0; ch < 5; ++ch) {
+                int32_t r[OUTR + 2 * R];
+#pragma unroll
+                for (int k = 0; k < OUTR + 2 * R; ++k) r[k] = sm.xb[ch][oy + k][ox];
+                S[0][ch] = r[0] + r[1] + r[2] + r[3] + r[4] + r[5] + r[6];
+#pragma unroll
+                for (int j = 1; j < OUTR; ++j) S[j][ch] = S[j - 1][ch] + r[j + 2 * R] - r[j - 1];
+            }
+            const int cz = win_count(q, P.nz_global);
+#pragma unroll
+            for (int j = 0; j < OUTR; ++j) {
+                if (!vout[j]) continue;
+                const int32_t X = S[j][0], Y = S[j][1];
+                const int64_t TA = (int64_t)NU * S[j][4] - (int64_t)X * Y;
+                const int64_t TB = (int64_t)NU * S[j][2] - (int64_t)X * X;
+                const int64_t TC = (int64_t)NU * S[j][3] - (int64_t)Y * Y;
+                const int cw = cxy[j] * cz;
+                float a, b, cc, omw;
+                if (cw == WIN * WIN * WIN) {
+                    a = (float)TA * cA;
+                    b = (float)TB * cB;
+                    cc = (float)TC * cC;
+                    omw = 0.0f;
+                } else {
+                    const double U = (double)QSCALE, iUF = 1.0 / (U * (double)kF), iUM = 1.0 / (U * (double)kM);
+                    const double omc = NWIN - (double)cw, sfd = sf, smd = smv, cwd = cw, Xd = X, Yd = Y;
+                    const double invN2 = 1.0 / (NWIN * NWIN);
+                    a = (float)(((double)TA * (iUF * iUM) + omc * (smd * Xd * iUF + sfd * Yd * iUM + sfd * smd * cwd)) *
+                                invN2);
+                    b = (float)(((double)TB * (iUF * iUF) + omc * (2.0 * sfd * Xd * iUF + sfd * sfd * cwd)) * invN2);
+                    cc = (float)(((double)TC * (iUM * iUM) + omc * (2.0 * smd * Yd * iUM + smd * smd * cwd)) * invN2);
+                    omw = (float)(omc * (1.0 / NWIN));
+                }
+                const float D = fmaf(b, cc, epsf);
+                const float invD = __fdividef(1.0f, D);
+                nsum += a * a * invD;
+                const float gamma = gi2 * a * invD;
+                const float rab = a * b * invD;
+                const int hy = oy + j + R, hx = ox + R;
+                const float fq = sm.fr[qslot][hy * FW + hx + 1];
+                const float df = (fq - sf) - (float)X * mF + sf * omw;
+                const float dm = sm.br[qslot][hy * HX + hx] * ikM - (float)Y * mM + smv * omw;
+                const float gmw = poison ? __int_as_float(0x7fc00000) : gamma * fmaf(-dm, rab, df);
+                const int ii = (oy + j) * TX + ox;
+                float* o = go + j * rs;
+                o[0] = sm.gr[qg][0][ii] * gmw;
+                o[1] = sm.gr[qg][1][ii] * gmw;
+                o[2] = sm.gr[qg][2][ii] * gmw;
+            }
+            go += pl3;
+        }
+        mbar_arrive(&sm.consumed[slot]);
+    }
+    return poison ? __int_as_float(0x7fc00000) : nsum;
+}
+
 template <int NM_, bool TMA, bool FULLWIN, bool OFF32>
 __global__ void __launch_bounds__(NT, 1) k_lncc_fused(const __grid_constant__ CUtensorMap fmap,
                                                       const __grid_constant__ CUtensorMap umap,
@@ -695,7 +874,12 @@ __global__ void __launch_bounds__(NT, 1) k_lncc_fused(const __grid_constant__ CU
     float nsum = 0.0f;
     if (t < SP::NM) {
         if (SP::RM != 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SP::RM));
-        nsum = moment_warps<NM_, TMA>(&fmap, P, sm, t, pstart, pend, zc0, x0, y0, sf, kF, smv, kM);
+#if FFDP_L3_ROWS && FFDP_L3_MROWS
+        if (SP::NM == 256)
+            nsum = moment_rows<TMA>(&fmap, P, sm, t, pstart, pend, zc0, x0, y0, sf, kF, smv, kM);
+        else
+#endif
+            nsum = moment_warps<NM_, TMA>(&fmap, P, sm, t, pstart, pend, zc0, x0, y0, sf, kF, smv, kM);
     } else {
         if (SP::RS != 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SP::RS));
 #if FFDP_L3_ROWS
