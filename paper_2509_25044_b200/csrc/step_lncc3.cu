@@ -43,7 +43,7 @@ namespace l3 {
 #endif
 // FFDP_L3_MROWS = 1: the moment warps' z stage in the row layout too (moment_rows)
 #ifndef FFDP_L3_MROWS
-#define FFDP_L3_MROWS 0
+#define FFDP_L3_MROWS 1
 #endif
 // L2 prefetch of the moving image (bulk tensor prefetch, one box per plane and CTA): the
 // box of the zero-bordered window starting MPF_X / MPF_Y before the tile (bordered
