@@ -41,6 +41,10 @@ namespace l3 {
 #ifndef FFDP_L3_ROWS
 #define FFDP_L3_ROWS 1
 #endif
+// FFDP_L3_NB: sampler passes per batch (3 or 6)
+#ifndef FFDP_L3_NB
+#define FFDP_L3_NB 3
+#endif
 // FFDP_L3_MROWS = 1: the moment warps' z stage in the row layout too (moment_rows)
 #ifndef FFDP_L3_MROWS
 #define FFDP_L3_MROWS 1
@@ -362,8 +366,10 @@ __device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUte
     const int64_t pl3 = 3 * P.plane;
     const float* ub = P.u + 3 * (pstart - P.buf_z0) * P.plane;  // u of plane p
     // pass j of a plane: main row hy = w + 8 j (j < nrows), then the edge pass (j = nrows)
-    constexpr int NB = 3;
-    float uu[2][NB][3];
+    // NB passes per batch: 3 (two batches per plane, the second's u in flight during the
+    // first's gathers) or 6 (one batch, all 48 corner loads of a lane in flight at once)
+    constexpr int NB = FFDP_L3_NB, NBATCH = 6 / NB;
+    float uu[NBATCH][NB][3];
     auto row_ok = [&](int j) {
         const int gy = y0 - R + w + 8 * j;
         return j < nrows && gy >= 0 && gy < ny;
@@ -408,7 +414,7 @@ __device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUte
             bze[a] = fma(P.g.P[3 * a + 2], zd, bxe[a]);
         }
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < NBATCH; ++half) {
             float(&u3)[NB][3] = uu[half];
             Cell c[NB];
 #pragma unroll
@@ -430,8 +436,8 @@ __device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUte
                 cell_fix(fma(P.g.Q[2], (double)u3[k][2], b2), c[k].i0[2], c[k].frac[2]);
             }
             // the other batch's u (this plane's second batch, or the next plane's first)
-            if (half == 0) {
-                load_u(uu[1], ub, NB, vz);
+            if (half == 0 && NBATCH == 2) {
+                load_u(uu[NBATCH - 1], ub, NB, vz);
             } else if (p + 1 < pend) {
                 ub += pl3;
                 load_u(uu[0], ub, 0, p + 1 >= 0 && p + 1 < P.nz_global);
