@@ -23,6 +23,11 @@
 
 #include "ffdp_common.cuh"
 
+// FFDP_MI_ZORDER = 1: z-major unit order (see unit_coords)
+#ifndef FFDP_MI_ZORDER
+#define FFDP_MI_ZORDER 0
+#endif
+
 namespace ffdp {
 namespace mstep {
 
@@ -43,8 +48,9 @@ struct Params {
     double* raw_out;           // fused finalize: raw joint histogram out (may be null)
     double upstream;
     int32_t* miss;
-    int32_t nx, ny, nxb, nyq;  // lattice, 32-wide x blocks, 4-row groups
-    FastDiv div_nxb, div_nyq;
+    int32_t nx, ny, nxb, nyq, nzs;  // lattice, 32-wide x blocks, 4-row groups, interior planes
+    FastDiv div_nxb, div_nyq, div_nzs;
+    int32_t zorder;                 // z-major unit order (unit_coords)
     int64_t plane, z_begin, buf_z0;
     int64_t nunits;
     float fix_scale;           // 2^23 or 2^21 (bspline, k_mi_hist_bs) / 2^22 (gaussian) / 2^21 (delta)
@@ -110,8 +116,21 @@ __device__ __forceinline__ Unit unit_coords(const Params& P, uint32_t unit, int 
     Unit w;
     const uint32_t r1 = fdiv(unit, P.div_nxb);
     const int32_t xb = (int32_t)(unit - r1 * P.nxb);
-    const uint32_t zz = fdiv(r1, P.div_nyq);
-    const int32_t yq = (int32_t)(r1 - zz * P.nyq);
+    uint32_t zz;
+    int32_t yq;
+    if (P.zorder) {
+        // units ordered x block, then z, then 4-row group: the two output planes that share a
+        // moving-image plane (the trilinear z corners) are processed back to back, so its
+        // lines come from L2 the second time (plane-major order re-reads them from HBM a
+        // whole plane of traffic later once a plane outgrows the L2: 1760^2 planes, 81 vs
+        // 92 GB read per pass 1 at configs[4])
+        const uint32_t yqu = fdiv(r1, P.div_nzs);
+        zz = r1 - yqu * (uint32_t)P.nzs;
+        yq = (int32_t)yqu;
+    } else {
+        zz = fdiv(r1, P.div_nyq);
+        yq = (int32_t)(r1 - zz * P.nyq);
+    }
     w.x = xb * 32 + lane;
     w.y0 = yq * 4;
     w.z = (int32_t)zz + (int32_t)P.z_begin;
@@ -793,6 +812,11 @@ static mstep::Params make_params(const float* f, const float* u, const ffdp_dims
     P.nyq = (int32_t)((d.ny + 3) / 4);
     P.div_nxb = make_fastdiv((uint32_t)P.nxb);
     P.div_nyq = make_fastdiv((uint32_t)P.nyq);
+    P.nzs = (int32_t)std::max<int64_t>(1, s.z_end - s.z_begin);
+    P.div_nzs = make_fastdiv((uint32_t)P.nzs);
+    // z-major order once a plane of F + u + M traffic no longer fits the L2 several times
+    // over (FFDP_MI_ZORDER forces it on)
+    P.zorder = FFDP_MI_ZORDER || d.nx * d.ny >= ((int64_t)1 << 21);
     P.plane = d.nx * d.ny;
     P.z_begin = s.z_begin;
     P.buf_z0 = s.buf_z0;
