@@ -319,3 +319,29 @@ def test_first_use_from_many_threads_in_a_fresh_process():
     for _ in range(3):
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_thin_slabs_rotation_and_translation(V, PL, orc, loss):
+    """Five ranks on 21 planes (slabs of 4-5 planes, halos of 3 from thin neighbours), a
+    rotated / scaled affine with a z translation (every rank's moving window differs from
+    its slab), ragged x / y: the plan equals the single-GPU step."""
+    from oracle import step_inputs
+    si = step_inputs(orc, (21, 33, 37), seed=29, loss=loss)
+    th = 0.12
+    A = np.array([[np.cos(th), -np.sin(th), 0.0], [np.sin(th), np.cos(th), 0.05], [0.02, -0.03, 0.97]])
+    t = np.array([0.01, -0.02, 0.08])
+    import copy
+    si = copy.copy(si)
+    si.A, si.t = A, t
+    groups = PL.local_group(5, [0] * 5)
+    try:
+        res = plan_step(PL, V, groups, si, loss, margin=2)
+    finally:
+        for g in groups:
+            g.close()
+    gu = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0)
+    l1, g1 = single(V, si, loss)
+    print(f"plan {loss} H=5 thin slabs: windows {[r[4] for r in res]}")
+    assert abs(res[0][0] - l1) / abs(l1) <= 1e-9
+    assert maxrel(gu, g1) <= 1e-6
