@@ -23,6 +23,10 @@
 
 #include "ffdp_common.cuh"
 
+// FFDP_MI_GB: corner-gather batch of the B-spline pass 1 (k_mi_hist_bs)
+#ifndef FFDP_MI_GB
+#define FFDP_MI_GB 4
+#endif
 // FFDP_MI_ZORDER = 1: z-major unit order (see unit_coords)
 #ifndef FFDP_MI_ZORDER
 #define FFDP_MI_ZORDER 0
@@ -412,18 +416,23 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
             float4* rp = P.rec + (w.bi - zrec);
             Cell c[4];
             unit_cells(P, w, L.uu, c);
-            Corners cr[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) cr[k] = gather_pad<FULLWIN, OFF32>(P.g, c[k], miss);
+            // FFDP_MI_GB voxels' corners are gathered at once (4: all of the unit's 32 loads in
+            // flight; 2: half the corner registers live)
+            Corners cr[FFDP_MI_GB];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+                if (k % FFDP_MI_GB == 0) {
+#pragma unroll
+                    for (int q = 0; q < FFDP_MI_GB; ++q) cr[q] = gather_pad<FULLWIN, OFF32>(P.g, c[k + q], miss);
+                }
+                const Corners& ck = cr[k % FFDP_MI_GB];
                 // Fixed point by a denormal product: with both weights pre-scaled by
                 // bs_wscale(S), kI * kJ lands at (2^S kI kJ) * 2^-149, whose IEEE bits ARE
                 // round(2^S kI kJ) (FMUL rounds to nearest; no -ftz).
                 float mw;
                 if (REC) {
                     float d[3];
-                    mw = interp_grad(cr[k], c[k], d);
+                    mw = interp_grad(ck, c[k], d);
                     if (ok[k]) {
                         const float4 rv = make_float4(mw, P.g.dscale[0] * d[0], P.g.dscale[1] * d[1], P.g.dscale[2] * d[2]);
                         // FFDP_REC_STREAM: evict-first stores (the records are read once, by pass 2),
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(HNT, 1) k_mi_hist_bs(const Params P) {
                     }
                     rp += P.nx;
                 } else {
-                    mw = interp(cr[k], c[k]);
+                    mw = interp(ck, c[k]);
                 }
                 float kI[4], kJ[4];
                 const int32_t mi = bspline_scaled<BC>(ff[k], B, bs_wscale(S), kI);

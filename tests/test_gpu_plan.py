@@ -325,9 +325,10 @@ def test_first_use_from_many_threads_in_a_fresh_process():
 def test_thin_slabs_rotation_and_translation(V, PL, orc, loss):
     """Five ranks on 21 planes (slabs of 4-5 planes, halos of 3 from thin neighbours), a
     rotated / scaled affine with a z translation (every rank's moving window differs from
-    its slab), ragged x / y: the plan equals the single-GPU step."""
+    its slab), ragged x / y (62 x 57): the plan equals the single-GPU step."""
     from oracle import step_inputs
-    si = step_inputs(orc, (21, 33, 37), seed=29, loss=loss)
+    # > 2^16 voxels: the single-GPU MI step then uses the quad kernels and grid the plan uses
+    si = step_inputs(orc, (21, 62, 57), seed=29, loss=loss)
     th = 0.12
     A = np.array([[np.cos(th), -np.sin(th), 0.0], [np.sin(th), np.cos(th), 0.05], [0.02, -0.03, 0.97]])
     t = np.array([0.01, -0.02, 0.08])
