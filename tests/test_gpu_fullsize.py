@@ -159,16 +159,18 @@ def _host32(t):
     return t.detach().cpu().numpy()
 
 
-@pytest.mark.parametrize("jitter", ["bench", "survey"])
-def test_lncc720_matches_fp64(V, orc, jitter):
+@pytest.mark.parametrize("shape,jitter", [((720, 640, 720), "bench"), ((720, 640, 720), "survey"),
+                                          ((1024, 1024, 1024), "bench")])
+def test_lncc720_matches_fp64(V, orc, shape, jitter):
     """BASELINE configs[2] (720x640x720 LNCC, window 7, ANTs) against the fp64 restatement:
     g_u at 20k sampled voxels (each depends only on its 7^3 window and gi = -1/N, so the
     per-voxel oracle is exact there) and the loss from one whole-volume fp64 sum of n_i
     (oracle/ffdp_oracle_big.c, OpenMP). jitter 'survey' is SURVEY 8(d)'s U(-0.01, 0.01)
-    normalized jitter (+-3.6 voxels at 720); 'bench' the bench's +-0.01 voxel."""
+    normalized jitter (+-3.6 voxels at 720); 'bench' the bench's +-0.01 voxel. The 1024^3
+    case is BASELINE configs[3]'s volume on one GPU."""
     import torch
     import bench
-    f, m, u, A, t = bench.synth_inputs((720, 640, 720), "lncc", 1234, "cuda", jitter=jitter)
+    f, m, u, A, t = bench.synth_inputs(shape, "lncc", 1234, "cuda", jitter=jitter)
     res = V.warp_loss_step(f, m, u, A, t, V.LossParams(kind="lncc"))
     assert res.window_misses == 0
     loss = res.loss
@@ -182,7 +184,8 @@ def test_lncc720_matches_fp64(V, orc, jitter):
     grel = maxrel(gu, r["g_u"])
     loss_ref = 1.0 - orc.lncc_sum_n_f32(hf, hm, hu, A, t) / hf.size
     lrel = abs(loss - loss_ref) / abs(loss_ref)
-    print(f"lncc720 ({jitter} jitter) vs fp64: loss {loss:.10f} ref {loss_ref:.10f} rel {lrel:.2e}; "
+    print(f"lncc {'x'.join(map(str, shape[::-1]))} ({jitter} jitter) vs fp64: loss {loss:.10f} ref {loss_ref:.10f} "
+          f"rel {lrel:.2e}; "
           f"g_u maxrel {grel:.2e} l2rel {l2rel(gu, r['g_u']):.2e} over {vox.size} voxels")
     assert lrel <= 1e-5
     assert grel <= 1e-4
