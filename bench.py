@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -119,7 +120,8 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ synthetic inputs
-def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, jitter="bench", chunk=32):
+def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, jitter="bench", chunk=32,
+                 fine=None):
     """Synthetic pair of the survey's recipe on the GPU, analytic in the
     global normalized frame so any z slab [z0, z1) of the global `shape` is generated
     locally and consistently across ranks: smooth ellipsoidal structures with texture,
@@ -130,7 +132,10 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, j
     U(-0.01, 0.01) in normalized units (+-0.5 (n-1) / 100 voxels: +-3.6 at 720).
     The outputs are allocated first and filled `chunk` planes at a time (the noise streams
     are seeded per chunk), so no volume-sized temporary fragments the device memory: at
-    configs[4] (119 GB of F, M, u, g_u) the step's 16 B/voxel records must still fit."""
+    configs[4] (119 GB of F, M, u, g_u) the step's 16 B/voxel records must still fit.
+    fine = (wavelength in voxels, amplitude, true-warp amplitude): adds a texture at the LNCC
+    window's scale and sets the true deformation's amplitude (the registration demo: the
+    smooth pair alone leaves every 7^3 window nearly constant, so LNCC is epsilon-dominated)."""
     import numpy as np
     import torch
 
@@ -149,8 +154,10 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, j
         return [[((rnd(3) * 3 + 0.5).tolist(), (rnd(3) * 6.28).tolist(), float(rnd(1) * 2 - 1) * amp)
                  for _ in range(3)] for _ in range(3)]
 
-    modes_true, modes_u = modes(0.04), modes(0.02)
+    modes_true, modes_u = modes(0.04 if fine is None else fine[2]), modes(0.02)
     aff = rnd(12).numpy() * 0.04 - 0.02
+    # fine texture: k_a = pi (n_a - 1) / wavelength rad per normalized unit
+    kf = None if fine is None else [math.pi * (n - 1) / fine[0] for n in (nx, ny, nz)]
 
     def f_at(X, Y, Z):
         out = torch.zeros(torch.broadcast_shapes(X.shape, Y.shape, Z.shape), dtype=torch.float32, device=device)
@@ -159,6 +166,8 @@ def synth_inputs(shape, loss, seed, device, z0=0, z1=None, reduce_minmax=None, j
                                                  ((Z - c[2]) / r[2]) ** 2)) * 10.0)
         for k, ph in tex:
             out += 0.04 * torch.sin(k[0] * X + ph[0]) * torch.sin(k[1] * Y + ph[1]) * torch.sin(k[2] * Z + ph[2])
+        if kf is not None:
+            out += fine[1] * torch.sin(kf[0] * X + 0.3) * torch.sin(kf[1] * Y + 1.1) * torch.sin(kf[2] * Z + 0.7)
         return out
 
     def field(md, z, out):
@@ -730,9 +739,11 @@ def run_registration(shape, schedule_spec):
 
     from paper_2509_25044_b200 import registration as R
     from paper_2509_25044_b200 import voxreg as V
-    # the pair differs by the synthetic smooth deformation; the deformable stage starts from
-    # the identity affine (the affine stage's job is not part of this config)
-    f, m, _, _, _ = synth_inputs(shape, "lncc", 1234, "cuda")
+    # the pair differs by a smooth deformation of ~4 voxels and carries texture at the
+    # window's scale (32-voxel wavelength), so LNCC sees structure and the registration has
+    # something to recover; the deformable stage starts from the identity affine (the affine
+    # stage's job is not part of this config)
+    f, m, _, _, _ = synth_inputs(shape, "lncc", 1234, "cuda", fine=(32.0, 0.25, 0.012))
     sch = R.ScaleSchedule([R.ScaleStep(d, n) for d, n in schedule_spec], loss=V.LossParams(kind="lncc"))
     # warm-up: one iteration per scale (allocations, attributes)
     R.deformable_stage(f, m, None, R.ScaleSchedule([R.ScaleStep(d, 1) for d, _ in schedule_spec],
@@ -763,7 +774,8 @@ def run_registration(shape, schedule_spec):
                                                                     e.iteration == 0), 6),
                                 "last": round([e.loss for e in trace if e.scale_index == i][-1], 6)}
                                for i, (d, _) in enumerate(schedule_spec)],
-            "per_iteration": "fused warp+LNCC step (2 kernels + reduction), ffdp_sobolev_adam, ffdp_gp_convolve"}
+            "per_iteration": "the one-pass fused warp+LNCC step (k_lncc_fused + its partial-sum reduction), "
+                             "ffdp_sobolev_adam, ffdp_gp_convolve"}
 
 
 class HostStager:
