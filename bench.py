@@ -389,7 +389,7 @@ def run_sharded(args, rank, world, local_rank, dev):
     shape, loss, cfg = WORKLOADS[args.workload]
     strong = args.scaling == "strong"
     gshape = shape if strong else (shape[0] * world, shape[1], shape[2])
-    lo, hi = PL_shard(gshape[0], world, rank)
+    lo, hi = _shard_range(gshape[0], world, rank)
 
     def reduce_minmax(a, b):
         t = torch.tensor([a, -b], dtype=torch.float64, device=dev)
@@ -445,7 +445,7 @@ def run_sharded(args, rank, world, local_rank, dev):
     return out
 
 
-def PL_shard(n, world, rank):
+def _shard_range(n, world, rank):
     """shard_ranges (fabric.hpp:44-57)."""
     base, extra = divmod(n, world)
     lo = rank * base + min(rank, extra)

@@ -399,7 +399,6 @@ struct DevGuard {
 int halo_swap(ffdp_plan_s* P, float* buf, int ch, cudaStream_t st) {
     const int64_t pl = P->plane * ch;
     std::vector<P2P> ops;
-    const size_t hb = sizeof(float) * pl * (size_t)std::max<int64_t>(P->hlo, P->hhi);
     if (P->hlo > 0) {
         ops.push_back({true, buf + P->hlo * pl, sizeof(float) * pl * P->hlo, P->rank - 1});
         ops.push_back({false, buf, sizeof(float) * pl * P->hlo, P->rank - 1});
@@ -408,7 +407,6 @@ int halo_swap(ffdp_plan_s* P, float* buf, int ch, cudaStream_t st) {
         ops.push_back({true, buf + (P->hlo + P->th() - P->hhi) * pl, sizeof(float) * pl * P->hhi, P->rank + 1});
         ops.push_back({false, buf + (P->hlo + P->th()) * pl, sizeof(float) * pl * P->hhi, P->rank + 1});
     }
-    (void)hb;
     return P->tr->p2p(ops, st);
 }
 
