@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(256) k_add_partials3(const double* partial, in
 // Planes per z chunk: the fewest (waves x (planes + half-cost warm-up planes)).
 inline int32_t pick_zchunk(int64_t tiles, int64_t nzs, int64_t capacity) {
     int64_t best = 1, best_cost = INT64_MAX;
-    for (int64_t ch = 1; ch <= std::min<int64_t>(nzs, 256); ++ch) {
+    for (int64_t ch = 1; ch <= std::min<int64_t>(nzs, std::max<int64_t>(256, (nzs + 255) / 256)); ++ch) {
         const int64_t zc = (nzs + ch - 1) / ch;
         if (zc > 256) continue;  // measured: 1024^3 runs 2 % faster in 256-plane chunks than in one
         const int64_t n = (nzs + zc - 1) / zc;
