@@ -952,7 +952,9 @@ static void launch_fused(const CUtensorMap (&map)[3], const l3::Params& P, dim3 
 
 static int64_t lncc3_max_ctas(const ffdp_dims& d, const ffdp_slab& s) {
     const int64_t tx = (d.nx + l3::TX - 1) / l3::TX, ty = (d.ny + l3::TY - 1) / l3::TY;
-    return tx * ty * std::min<int64_t>(std::max<int64_t>(1, s.z_end - s.z_begin), 256);
+    // pick_zchunk's chunk count never exceeds this bound
+    const int64_t nzs = std::max<int64_t>(1, s.z_end - s.z_begin);
+    return tx * ty * std::min<int64_t>(nzs, std::max<int64_t>(256, (nzs + 255) / 256));
 }
 
 // workspace: 4 floats of value ranges (when computed here), then one double per CTA
