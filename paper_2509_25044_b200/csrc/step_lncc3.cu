@@ -1038,7 +1038,12 @@ int lncc3_step(const float* f, const float* u, const ffdp_dims& d, const ffdp_sl
     const int64_t nzs = s.z_end - s.z_begin;
     // planes per CTA (FFDP_LNCC_ZCHUNK overrides the wave model, for measurements)
     static const int zc_env = getenv("FFDP_LNCC_ZCHUNK") ? atoi(getenv("FFDP_LNCC_ZCHUNK")) : 0;
-    P.zchunk = zc_env > 0 ? (int32_t)std::min<int64_t>(zc_env, std::max<int64_t>(1, nzs)) : pick_zchunk(tx * ty, nzs, num_sms());
+    P.zchunk = pick_zchunk(tx * ty, nzs, num_sms());
+    if (zc_env > 0) {
+        const int64_t nzs1 = std::max<int64_t>(1, nzs);
+        const int64_t max_chunks = std::min<int64_t>(nzs1, std::max<int64_t>(256, (nzs1 + 255) / 256));
+        P.zchunk = (int32_t)std::max<int64_t>(std::min<int64_t>(zc_env, nzs1), (nzs1 + max_chunks - 1) / max_chunks);
+    }
     const int64_t chunks = (nzs + P.zchunk - 1) / P.zchunk;
     if (ty > 65535 || chunks > 65535) return set_error(FFDP_INVALID_ARGUMENT, "step_lncc: grid too large");
     const dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)chunks);
