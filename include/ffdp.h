@@ -513,6 +513,8 @@ typedef struct {
     int32_t margin_planes; /* moving-window margin beyond the affine's z reach */
     int32_t records;       /* MI: 1 = pass-1 records when they fit (+16 B/voxel), 0 = pass 2 re-samples */
     int32_t overlap;       /* LNCC: 1 = u halo exchange overlapped with the interior planes */
+    int32_t warp_halo;     /* > 0: the plan also runs the warp update (ffdp_plan_warp_update) with taps of
+                              radius <= warp_halo (3 for the default sigmas 1.0 / 0.5); 0: step only */
 } ffdp_plan_params;
 
 /* Creates rank g's plan for a `global` lattice (slab = shard_ranges(nz, world, rank)). */
@@ -537,6 +539,14 @@ FFDP_API int ffdp_plan_load(ffdp_plan p, const float* f_slab, const float* m_sla
  * ffdp_plan_result reports them -- a non-zero count means the unchecked steps must be
  * redone with sync = 1). */
 FFDP_API int ffdp_plan_step(ffdp_plan p, int sync, double* loss);
+/* The warp update of the iteration on the plan's slab (registration.hpp:313-317, collective):
+ * the halo planes of g_u exchanged, gp_convolve(g_u, taps_grad, renormalize) fused with
+ * adam_step on u (ffdp_sobolev_adam; beta 0.9 / 0.999, eps 1e-8, the plan holds the moments and
+ * the step counter, reset by ffdp_plan_load), the halo planes of u exchanged, u =
+ * gp_convolve(u, taps_warp, renormalize). Odd tap counts of radius <= warp_halo (host doubles,
+ * gaussian_taps). Afterwards ffdp_plan_u points at the smoothed field (re-query it). */
+FFDP_API int ffdp_plan_warp_update(ffdp_plan p, double lr_norm, const double* taps_grad, int ntaps_grad,
+                                   const double* taps_warp, int ntaps_warp);
 /* Waits for the last step; its loss and the summed window misses over all ranks. */
 FFDP_API int ffdp_plan_result(ffdp_plan p, double* loss, double* misses);
 

@@ -70,7 +70,7 @@ class PlanParamsC(C.Structure):
     """ffdp_plan_params (include/ffdp.h)."""
     _fields_ = [("loss_kind", C.c_int32), ("window", C.c_int32), ("eps", C.c_double), ("kernel", ParzenC),
                 ("A", C.c_double * 9), ("t", C.c_double * 3), ("margin_planes", C.c_int32),
-                ("records", C.c_int32), ("overlap", C.c_int32)]
+                ("records", C.c_int32), ("overlap", C.c_int32), ("warp_halo", C.c_int32)]
 
 
 NCCL_ID_BYTES = 128
@@ -166,6 +166,7 @@ _SIGS = {
     "ffdp_plan_load": (C.c_int, [_vp, _vp, _vp]),
     "ffdp_plan_step": (C.c_int, [_vp, C.c_int, _dp]),
     "ffdp_plan_result": (C.c_int, [_vp, _dp, _dp]),
+    "ffdp_plan_warp_update": (C.c_int, [_vp, C.c_double, _dp, C.c_int, _dp, C.c_int]),
 }
 
 

@@ -369,7 +369,8 @@ struct ffdp_plan_s {
     ffdp_sampler_args ga{};  // sampler args of the global output lattice
     cudaStream_t st = nullptr, cst = nullptr;
     cudaEvent_t ev_u = nullptr, ev_halo = nullptr;
-    DBuf f_h, u_h, g_u, m_own, stage, win, ranges, rng64, red, hist, raw, table, lws, rec, ext, req;
+    DBuf f_h, u_h, u_h2, g_h, m1, m2, m_own, stage, win, ranges, rng64, red, hist, raw, table, lws, rec, ext, req;
+    int64_t adam_step = 0;  // the scale's Adam step counter (adam.hpp:30-50)
     int64_t wz0 = 0, wz1 = 0;  // resident moving planes
     bool loaded = false;
     double* host = nullptr;    // pinned {loss, misses}
@@ -378,6 +379,8 @@ struct ffdp_plan_s {
     int64_t nb() const { return hlo + th() + hhi; }
     ffdp_dims bd() const { return ffdp_dims{global.nx, global.ny, nb()}; }
     ffdp_slab slab(int64_t z0, int64_t z1) const { return ffdp_slab{lo - hlo, nb(), z0, z1, global.nz}; }
+    // g_u lives in the interior of the haloed g buffer (the warp update smooths it in place)
+    float* g_int() const { return g_h.as<float>() + 3 * hlo * plane; }
     ffdp_image_window window() const {
         return ffdp_image_window{win.as<float>(), global, wz0, wz1, 2};
     }
@@ -394,18 +397,20 @@ struct DevGuard {
     ~DevGuard() { cudaSetDevice(prev); }
 };
 
-// exchange `pad` boundary planes of a haloed buffer (channels floats per voxel) with the
-// z neighbours: my first / last interior planes become their halo planes, theirs mine
-int halo_swap(ffdp_plan_s* P, float* buf, int ch, cudaStream_t st) {
+// exchange the w planes next to the interior of a haloed buffer (channels floats per voxel,
+// the plan's hlo / hhi halo planes allocated on each side) with the z neighbours: my first /
+// last w interior planes become their halo planes, theirs mine. w < 0: the whole halo.
+int halo_swap(ffdp_plan_s* P, float* buf, int ch, cudaStream_t st, int64_t w = -1) {
     const int64_t pl = P->plane * ch;
+    const int64_t wl = P->hlo > 0 ? (w < 0 ? P->hlo : w) : 0, wh = P->hhi > 0 ? (w < 0 ? P->hhi : w) : 0;
     std::vector<P2P> ops;
-    if (P->hlo > 0) {
-        ops.push_back({true, buf + P->hlo * pl, sizeof(float) * pl * P->hlo, P->rank - 1});
-        ops.push_back({false, buf, sizeof(float) * pl * P->hlo, P->rank - 1});
+    if (wl > 0) {
+        ops.push_back({true, buf + P->hlo * pl, sizeof(float) * pl * wl, P->rank - 1});
+        ops.push_back({false, buf + (P->hlo - wl) * pl, sizeof(float) * pl * wl, P->rank - 1});
     }
-    if (P->hhi > 0) {
-        ops.push_back({true, buf + (P->hlo + P->th() - P->hhi) * pl, sizeof(float) * pl * P->hhi, P->rank + 1});
-        ops.push_back({false, buf + (P->hlo + P->th()) * pl, sizeof(float) * pl * P->hhi, P->rank + 1});
+    if (wh > 0) {
+        ops.push_back({true, buf + (P->hlo + P->th() - wh) * pl, sizeof(float) * pl * wh, P->rank + 1});
+        ops.push_back({false, buf + (P->hlo + P->th()) * pl, sizeof(float) * pl * wh, P->rank + 1});
     }
     return P->tr->p2p(ops, st);
 }
@@ -516,7 +521,7 @@ int launch_step(ffdp_plan_s* P) {
         const ffdp_dims bd = P->bd();
         auto run = [&](int64_t z0, int64_t z1) {
             return lncc3_step(P->f_h.as<float>(), P->u_h.as<float>(), bd, P->slab(z0, z1), iw, P->ga, P->prm.eps, gi,
-                              P->ranges.as<float>(), P->g_u.as<float>() + 3 * (z0 - P->lo) * P->plane, sum_n, miss,
+                              P->ranges.as<float>(), P->g_int() + 3 * (z0 - P->lo) * P->plane, sum_n, miss,
                               P->lws.p, st);
         };
         if (split) {
@@ -548,10 +553,10 @@ int launch_step(ffdp_plan_s* P) {
     PLAN_TRY(mi_hist_u64_to_raw(h, B, P->scale_exp, P->raw.as<double>(), st));
     PLAN_TRY(ffdp_mi_finalize(P->raw.as<double>(), B, -1.0, P->table.as<double>(), st));
     if (rec)
-        PLAN_TRY(mi_grad_rec(P->f_h.as<float>(), bd, sl, P->prm.kernel, P->table.as<double>(), rec, P->g_u.as<float>(), st));
+        PLAN_TRY(mi_grad_rec(P->f_h.as<float>(), bd, sl, P->prm.kernel, P->table.as<double>(), rec, P->g_int(), st));
     else
         PLAN_TRY(mi_quad_grad(P->f_h.as<float>(), P->u_h.as<float>(), bd, sl, iw, P->ga, P->prm.kernel,
-                              P->table.as<double>(), P->g_u.as<float>(), nullptr, st));
+                              P->table.as<double>(), P->g_int(), nullptr, st));
     k_pack_mi<<<1, 1, 0, st>>>(P->table.as<double>(), B, h, P->red.as<double>());
     FFDP_CHECK_CUDA(cudaMemcpyAsync(P->host, P->red.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     return check_launch("plan step (mi)");
@@ -701,7 +706,10 @@ int ffdp_plan_create(ffdp_group g, ffdp_dims global, const ffdp_plan_params* prm
     P->lncc = prm->loss_kind == 0;
     P->B = P->lncc ? 0 : prm->kernel.bins;
     shard_range(global.nz, P->world, P->rank, P->lo, P->hi);
-    const int pad = P->lncc ? prm->window / 2 : 0;
+    // halo planes of F, u and g_u: the LNCC window radius and the warp update's tap radius
+    if (prm->warp_halo < 0 || prm->warp_halo > 16)
+        return set_error(FFDP_INVALID_ARGUMENT, "plan_create: warp_halo must be in [0, 16]");
+    const int pad = std::max(P->lncc ? prm->window / 2 : 0, (int)prm->warp_halo);
     P->hlo = P->rank > 0 ? pad : 0;
     P->hhi = P->rank < P->world - 1 ? pad : 0;
     // halo_exchange (fabric.hpp:321-326): a neighbour thinner than the halo is an error
@@ -733,7 +741,15 @@ int ffdp_plan_create(ffdp_group g, ffdp_dims global, const ffdp_plan_params* prm
     const int64_t n_in = P->plane * P->th();
     PLAN_TRY(P->f_h.alloc(sizeof(float) * P->plane * P->nb()));
     PLAN_TRY(P->u_h.alloc(sizeof(float) * 3 * P->plane * P->nb()));
-    PLAN_TRY(P->g_u.alloc(sizeof(float) * 3 * n_in));
+    PLAN_TRY(P->g_h.alloc(sizeof(float) * 3 * P->plane * P->nb()));
+    FFDP_CHECK_CUDA(cudaMemset(P->g_h.p, 0, P->g_h.bytes));
+    if (prm->warp_halo > 0) {
+        // the warp update: the smoothed u (ping-pong with u_h) and the Adam moments
+        PLAN_TRY(P->u_h2.alloc(sizeof(float) * 3 * P->plane * P->nb()));
+        FFDP_CHECK_CUDA(cudaMemset(P->u_h2.p, 0, P->u_h2.bytes));
+        PLAN_TRY(P->m1.alloc(sizeof(float) * 3 * n_in));
+        PLAN_TRY(P->m2.alloc(sizeof(float) * 3 * n_in));
+    }
     PLAN_TRY(P->m_own.alloc(sizeof(float) * n_in));
     FFDP_CHECK_CUDA(cudaMemset(P->u_h.p, 0, P->u_h.bytes));
     PLAN_TRY(P->ranges.alloc(4 * sizeof(float)));
@@ -765,7 +781,7 @@ int ffdp_plan_destroy(ffdp_plan p) {
         DevGuard dg(p->dev);
         cudaStreamSynchronize(p->st);
         cudaStreamSynchronize(p->cst);
-        for (DBuf* b : {&p->f_h, &p->u_h, &p->g_u, &p->m_own, &p->stage, &p->win, &p->ranges, &p->rng64, &p->red,
+        for (DBuf* b : {&p->f_h, &p->u_h, &p->u_h2, &p->g_h, &p->m1, &p->m2, &p->m_own, &p->stage, &p->win, &p->ranges, &p->rng64, &p->red,
                         &p->hist, &p->raw, &p->table, &p->lws, &p->rec, &p->ext, &p->req})
             b->release();
         if (p->host) cudaFreeHost(p->host);
@@ -787,7 +803,7 @@ int ffdp_plan_slab(ffdp_plan p, int64_t* lo, int64_t* hi) {
 
 void* ffdp_plan_stream(ffdp_plan p) { return p ? (void*)p->st : nullptr; }
 float* ffdp_plan_u(ffdp_plan p) { return p ? p->u_h.as<float>() + 3 * p->hlo * p->plane : nullptr; }
-float* ffdp_plan_g_u(ffdp_plan p) { return p ? p->g_u.as<float>() : nullptr; }
+float* ffdp_plan_g_u(ffdp_plan p) { return p ? p->g_int() : nullptr; }
 
 int ffdp_plan_window(ffdp_plan p, int64_t* z0, int64_t* z1, int64_t* fetches) {
     if (!p) return set_error(FFDP_INVALID_ARGUMENT, "plan_window: null plan");
@@ -812,6 +828,12 @@ int ffdp_plan_load(ffdp_plan p, const float* f_slab, const float* m_slab) {
         PLAN_TRY(p->tr->allreduce(p->rng64.p, 4, Dt::F64, Op::Min, p->st));
         k_ranges_unpack<<<1, 32, 0, p->st>>>(p->rng64.as<double>(), p->ranges.as<float>());
     }
+    // a new scale: fresh Adam moments (registration.hpp:270-273 builds AdamState per scale)
+    p->adam_step = 0;
+    if (p->m1.p) {
+        FFDP_CHECK_CUDA(cudaMemsetAsync(p->m1.p, 0, p->m1.bytes, p->st));
+        FFDP_CHECK_CUDA(cudaMemsetAsync(p->m2.p, 0, p->m2.bytes, p->st));
+    }
     int64_t a, b;
     affine_z_range(p, a, b);
     p->fetches = 0;
@@ -834,6 +856,39 @@ int ffdp_plan_step(ffdp_plan p, int sync, double* loss) {
         PLAN_TRY(widen(p));  // every rank sees the same summed miss count: all widen together
     }
     return set_error(FFDP_RUNTIME, "plan_step: the moving window kept missing");
+}
+
+int ffdp_plan_warp_update(ffdp_plan p, double lr_norm, const double* taps_grad, int ntaps_grad,
+                          const double* taps_warp, int ntaps_warp) {
+    PLAN_TRY(check_plan(p));
+    if (!p->m1.p) return set_error(FFDP_LOGIC, "plan_warp_update: the plan was created with warp_halo = 0");
+    if (!taps_grad || !taps_warp || ntaps_grad < 1 || ntaps_warp < 1 || ntaps_grad % 2 == 0 || ntaps_warp % 2 == 0)
+        return set_error(FFDP_INVALID_ARGUMENT, "gp_convolve: kernel must be odd");
+    const int rg = ntaps_grad / 2, rw = ntaps_warp / 2;
+    if (rg > p->prm.warp_halo || rw > p->prm.warp_halo)
+        return set_error(FFDP_INVALID_ARGUMENT, "plan_warp_update: taps wider than the plan's warp_halo");
+    DevGuard dg(p->dev);
+    cudaStream_t st = p->st;
+    const int64_t pl3 = 3 * p->plane;
+    // registration.hpp:313: g_s = gp_convolve(g_u, taps_grad, renormalize) with rg halo planes
+    // (halo_exchange, fabric.hpp:315-370), fused with adam_step(u, g_s) (adam.hpp:30-50)
+    PLAN_TRY(halo_swap(p, p->g_h.as<float>(), 3, st, rg));
+    const int64_t glo = p->hlo > 0 ? rg : 0, ghi = p->hhi > 0 ? rg : 0;
+    const ffdp_dims gd{p->global.nx, p->global.ny, glo + p->th() + ghi};
+    const ffdp_slab gs{p->lo - glo, gd.nz, p->lo, p->hi, p->global.nz};
+    float* u_int = p->u_h.as<float>() + p->hlo * pl3;
+    ++p->adam_step;
+    PLAN_TRY(ffdp_sobolev_adam(p->g_h.as<float>() + (p->hlo - glo) * pl3, u_int, p->m1.as<float>(), p->m2.as<float>(),
+                               gd, gs, taps_grad, ntaps_grad, lr_norm, 0.9, 0.999, 1e-8, p->adam_step, st));
+    // registration.hpp:316: u = gp_convolve(u, taps_warp, renormalize) with rw halo planes
+    PLAN_TRY(halo_swap(p, p->u_h.as<float>(), 3, st, rw));
+    const int64_t wlo = p->hlo > 0 ? rw : 0, whi = p->hhi > 0 ? rw : 0;
+    const ffdp_dims wd{p->global.nx, p->global.ny, wlo + p->th() + whi};
+    const ffdp_slab ws{p->lo - wlo, wd.nz, p->lo, p->hi, p->global.nz};
+    PLAN_TRY(ffdp_gp_convolve(p->u_h.as<float>() + (p->hlo - wlo) * pl3, p->u_h2.as<float>() + p->hlo * pl3, wd, ws, 3,
+                              taps_warp, ntaps_warp, 1, st));
+    std::swap(p->u_h, p->u_h2);  // ffdp_plan_u now points at the smoothed field
+    return check_launch("plan_warp_update");
 }
 
 int ffdp_plan_result(ffdp_plan p, double* loss, double* misses) {

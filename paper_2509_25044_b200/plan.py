@@ -76,7 +76,7 @@ class ShardPlan:
     write ``u`` (a torch view of the plan's interior displacement planes) and ``step()``."""
 
     def __init__(self, group: Group, global_shape, params, A=None, t=None, margin_planes: int = 8,
-                 records: bool = True, overlap: bool = True):
+                 records: bool = True, overlap: bool = True, warp_halo: int = 0):
         from .voxreg import ParzenKernel
         self.group = group
         self.global_shape = tuple(int(s) for s in global_shape)
@@ -96,17 +96,23 @@ class ShardPlan:
         p.A[:] = [float(x) for x in A.ravel()]
         p.t[:] = [float(x) for x in t]
         p.margin_planes, p.records, p.overlap = int(margin_planes), int(records), int(overlap)
+        p.warp_halo = int(warp_halo)
         self.params = params
         self.h = C.c_void_p()
         lib.ffdp_plan_create(group.h, Dims(nx, ny, nz), C.byref(p), C.byref(self.h))
         lo, hi = C.c_int64(0), C.c_int64(0)
         lib.ffdp_plan_slab(self.h, C.byref(lo), C.byref(hi))
         self.lo, self.hi = lo.value, hi.value
-        dev = torch.device("cuda", group.device)
-        shape = (self.hi - self.lo, ny, nx, 3)
-        self.u = torch.as_tensor(_DeviceArray(lib.ffdp_plan_u(self.h), shape, self), device=dev)
-        self.g_u = torch.as_tensor(_DeviceArray(lib.ffdp_plan_g_u(self.h), shape, self), device=dev)
-        self.stream = torch.cuda.ExternalStream(lib.ffdp_plan_stream(self.h), device=dev)
+        self._dev = torch.device("cuda", group.device)
+        self._shape = (self.hi - self.lo, ny, nx, 3)
+        self.g_u = torch.as_tensor(_DeviceArray(lib.ffdp_plan_g_u(self.h), self._shape, self), device=self._dev)
+        self.stream = torch.cuda.ExternalStream(lib.ffdp_plan_stream(self.h), device=self._dev)
+
+    @property
+    def u(self) -> torch.Tensor:
+        """The slab's displacement planes (a view of the plan's buffer; the warp update moves
+        it to the other buffer of its ping-pong pair, so take the view after each update)."""
+        return torch.as_tensor(_DeviceArray(lib.ffdp_plan_u(self.h), self._shape, self), device=self._dev)
 
     def load(self, f_slab: torch.Tensor, m_slab: torch.Tensor):
         """Once per scale: this rank's F and M slabs (planes [lo, hi))."""
@@ -126,6 +132,16 @@ class ShardPlan:
         loss = C.c_double(0.0)
         lib.ffdp_plan_step(self.h, 1 if sync else 0, C.byref(loss))
         return loss.value if sync else None
+
+    def warp_update(self, lr_norm: float, sigma_grad: float = 1.0, sigma_warp: float = 0.5):
+        """The iteration's warp update on the slab (registration.hpp:313-317), collective:
+        needs a plan created with warp_halo >= the taps' radius (3 for the default sigmas)."""
+        from .voxreg import gaussian_taps
+        g = np.ascontiguousarray(gaussian_taps(sigma_grad), dtype=np.float64)
+        w = np.ascontiguousarray(gaussian_taps(sigma_warp), dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        lib.ffdp_plan_warp_update(self.h, float(lr_norm), g.ctypes.data_as(dp), int(g.size), w.ctypes.data_as(dp),
+                                  int(w.size))
 
     def result(self):
         """(loss, summed window misses) of the last step (waits for it)."""

@@ -346,3 +346,56 @@ def test_thin_slabs_rotation_and_translation(V, PL, orc, loss):
     print(f"plan {loss} H=5 thin slabs: windows {[r[4] for r in res]}")
     assert abs(res[0][0] - l1) / abs(l1) <= 1e-9
     assert maxrel(gu, g1) <= 1e-6
+
+
+@pytest.mark.parametrize("loss", ["lncc", "mi"])
+def test_plan_iterations_with_warp_update(V, PL, cases, loss):
+    """Three deformable iterations on the plan (step, then ffdp_plan_warp_update: halo'd
+    Sobolev smoothing fused with Adam, halo'd warp smoothing; registration.hpp:277-317) at
+    1-3 ranks against the single-GPU iteration (warp_loss_step + warp_update): the loss trace
+    and the final warp agree bit for bit."""
+    import torch
+    si = cases[loss]
+    shape = si.f.shape
+    lr = V.deformable_lr_norm(shape, 0.5)
+    # single GPU
+    u = dev(si.u)
+    st = V.AdamState.zeros(u)
+    trace1 = []
+    for _ in range(3):
+        r = V.warp_loss_step(dev(si.f), dev(si.m), u, si.A, si.t, params_for(V, loss))
+        trace1.append(r.loss)
+        u = V.warp_update(u, r.g_u, st, lr)
+    u1 = host(u)
+    for world in (1, 2, 3):
+        groups = PL.local_group(world, [0] * world)
+
+        def rank(g):
+            torch.cuda.set_device(0)
+            p = PL.ShardPlan(g, shape, params_for(V, loss), si.A, si.t, warp_halo=3)
+            try:
+                p.load(dev(si.f)[p.lo:p.hi], dev(si.m)[p.lo:p.hi])
+                p.set_u(dev(si.u)[p.lo:p.hi])
+                tr = []
+                for _ in range(3):
+                    tr.append(p.step())
+                    p.warp_update(lr)
+                torch.cuda.synchronize()
+                return tr, host(p.u.clone()), p.lo
+            finally:
+                p.close()
+
+        try:
+            res = run_ranks(groups, rank)
+        finally:
+            for g in groups:
+                g.close()
+        un = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[2])], axis=0)
+        tr = res[0][0]
+        print(f"plan {loss} H={world} 3 iterations: trace {tr} vs {trace1}; "
+              f"warp maxrel {maxrel(un, u1):.2e}")
+        if loss == "mi":
+            assert tr == trace1
+        else:
+            assert max(abs(a - b) for a, b in zip(tr, trace1)) <= 1e-12
+        assert np.array_equal(un, u1)
