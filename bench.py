@@ -274,7 +274,8 @@ class Stepper:
             return
         free, _ = self.torch.cuda.mem_get_info()
         need = 16 * self.n + (4 << 30)
-        self.use_rec = free > need
+        # FFDP_BENCH_NOREC=1 forces the record-free pass 2 (A/B measurements)
+        self.use_rec = free > need and os.environ.get("FFDP_BENCH_NOREC") != "1"
         self.launches_per_step = 2 if self.use_rec else 4
         self.records_note = {"used": self.use_rec, "device_free_bytes": int(free), "needed_bytes": int(need),
                              "torch_reserved_bytes": int(self.torch.cuda.memory_reserved())}

@@ -41,6 +41,10 @@ namespace l3 {
 #ifndef FFDP_L3_ROWS
 #define FFDP_L3_ROWS 1
 #endif
+// FFDP_L3_SPLITFIN = 1: the sampler warps finish half of every plane's outputs
+#ifndef FFDP_L3_SPLITFIN
+#define FFDP_L3_SPLITFIN 0
+#endif
 // FFDP_L3_NB: sampler passes per batch (3 or 6)
 #ifndef FFDP_L3_NB
 #define FFDP_L3_NB 3
@@ -99,6 +103,8 @@ struct __align__(128) Smem {
     unsigned long long fbar[RING];     // F(p) landed (TMA)
     unsigned long long sampled[RING];  // b(p), G(p) written (one arrival per sampler thread)
     unsigned long long consumed[RING]; // moment iteration p finished (one arrival per moment thread)
+    unsigned long long xdone[RING];    // FFDP_L3_SPLITFIN: x stage of iteration p done (moment threads)
+    unsigned long long ydone[RING];    // FFDP_L3_SPLITFIN: the samplers' outputs of iteration p done
     double red[NT / 32];
 };
 
@@ -201,6 +207,93 @@ __device__ __forceinline__ void quant(float a, float b, int32_t (&q)[5]) {
 // in-lattice extent of the window of position g along an axis of n voxels
 __device__ __forceinline__ int win_count(int64_t g, int64_t n) {
     return (int)(min(g + R, n - 1) - max(g - R, (int64_t)0) + 1);
+}
+
+// (only with both row-mapped sides, whose handshake it extends)
+#define L3_SPLIT (FFDP_L3_SPLITFIN && FFDP_L3_ROWS && FFDP_L3_MROWS)
+
+// The y stage and the outputs of plane q for OUTR rows oy.. of column ox (shared by the
+// moment warps and, with FFDP_L3_SPLITFIN, the sampler warps, which finish the lower half
+// of the tile's rows while the moment warps start the next plane's z stage).
+struct FinConst {
+    float sf, kF, smv, kM, ikM, cA, cB, cC, mF, mM, gi2, epsf;
+    int32_t NU;
+    bool poison;
+    __device__ FinConst(const Params& P, float sf_, float kF_, float smv_, float kM_)
+        : sf(sf_), kF(kF_), smv(smv_), kM(kM_) {
+        ikM = 1.0f / kM;
+        const float cAB = (float)(1.0 / (NWIN * NWIN * (double)QSCALE * (double)QSCALE));
+        cA = cAB / (kF * kM);
+        cB = cAB / (kF * kF);
+        cC = cAB / (kM * kM);
+        mF = (float)(1.0 / (NWIN * (double)QSCALE)) / kF;
+        mM = (float)(1.0 / (NWIN * (double)QSCALE)) / kM;
+        NU = (WIN * WIN * WIN) << 21;
+        gi2 = 2.0f * (float)P.gi;
+        epsf = (float)P.eps;
+        poison = !(fabsf(sf) <= 3.0e38f && fabsf(smv) <= 3.0e38f);
+    }
+};
+
+template <int OUTR>
+__device__ __forceinline__ void finalize_rows(const Params& P, const Smem& sm, const FinConst& K, int it, int64_t q,
+                                              int ox, int oy, const bool (&vout)[OUTR], const int (&cxy)[OUTR],
+                                              float* go, int rs, float& nsum) {
+    const int qslot = (it + RING - R) % RING, qg = (it + NG - R) % NG;
+    int32_t S[OUTR][5];
+#pragma unroll
+    for (int ch = 0; ch < 5; ++ch) {
+        int32_t r[OUTR + 2 * R];
+#pragma unroll
+        for (int k = 0; k < OUTR + 2 * R; ++k) r[k] = sm.xb[ch][oy + k][ox];
+        S[0][ch] = r[0] + r[1] + r[2] + r[3] + r[4] + r[5] + r[6];
+#pragma unroll
+        for (int j = 1; j < OUTR; ++j) S[j][ch] = S[j - 1][ch] + r[j + 2 * R] - r[j - 1];
+    }
+    const int cz = win_count(q, P.nz_global);
+#pragma unroll
+    for (int j = 0; j < OUTR; ++j) {
+        if (!vout[j]) continue;
+        const int32_t X = S[j][0], Y = S[j][1];
+        // N^2 U^2 k k' {cov, var F, var M} of the quantised shifted values: exact in int64
+        const int64_t TA = (int64_t)K.NU * S[j][4] - (int64_t)X * Y;
+        const int64_t TB = (int64_t)K.NU * S[j][2] - (int64_t)X * X;
+        const int64_t TC = (int64_t)K.NU * S[j][3] - (int64_t)Y * Y;
+        const int cw = cxy[j] * cz;
+        float a, b, cc, omw;
+        if (cw == WIN * WIN * WIN) {
+            a = (float)TA * K.cA;
+            b = (float)TB * K.cB;
+            cc = (float)TC * K.cC;
+            omw = 0.0f;
+        } else {
+            // zero-padded border: the shift is missing from the N - cw outside positions
+            const double U = (double)QSCALE, iUF = 1.0 / (U * (double)K.kF), iUM = 1.0 / (U * (double)K.kM);
+            const double omc = NWIN - (double)cw, sfd = K.sf, smd = K.smv, cwd = cw, Xd = X, Yd = Y;
+            const double invN2 = 1.0 / (NWIN * NWIN);
+            a = (float)(((double)TA * (iUF * iUM) + omc * (smd * Xd * iUF + sfd * Yd * iUM + sfd * smd * cwd)) * invN2);
+            b = (float)(((double)TB * (iUF * iUF) + omc * (2.0 * sfd * Xd * iUF + sfd * sfd * cwd)) * invN2);
+            cc = (float)(((double)TC * (iUM * iUM) + omc * (2.0 * smd * Yd * iUM + smd * smd * cwd)) * invN2);
+            omw = (float)(omc * (1.0 / NWIN));
+        }
+        const float D = fmaf(b, cc, K.epsf);
+        const float invD = __fdividef(1.0f, D);  // D >= eps > 0
+        nsum += a * a * invD;
+        const float gamma = K.gi2 * a * invD;
+        const float rab = a * b * invD;
+        // F - muF and Mw - muM: (v - s) - (mu - s), mu - s = sum/(N U k) - s (1 - cw/N)
+        const int hy = oy + j + R, hx = ox + R;
+        const float fq = sm.fr[qslot][hy * FW + hx + 1];
+        const float df = (fq - K.sf) - (float)X * K.mF + K.sf * omw;
+        const float dm = sm.br[qslot][hy * HX + hx] * K.ikM - (float)Y * K.mM + K.smv * omw;
+        // dL/dMw (lncc.hpp:262-278, ANTs)
+        const float gmw = K.poison ? __int_as_float(0x7fc00000) : gamma * fmaf(-dm, rab, df);
+        const int ii = (oy + j) * TX + ox;
+        float* o = go + j * rs;
+        o[0] = sm.gr[qg][0][ii] * gmw;
+        o[1] = sm.gr[qg][1][ii] * gmw;
+        o[2] = sm.gr[qg][2][ii] * gmw;
+    }
 }
 
 // ------------------------------------------------------------------ sampler warps
@@ -338,11 +431,33 @@ __device__ __forceinline__ void sampler_warps(const CUtensorMap* umap, const CUt
 constexpr int SROWS = 5;  // main rows per warp (the last one absent on warps 6, 7)
 constexpr int NEDGE = 6 * HY;
 template <bool TMA, bool FULLWIN, bool OFF32>
-__device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUtensorMap* mmap, const Params& P,
-                                             Smem& sm, int st, int64_t pstart, int64_t pend, int64_t zc0,
-                                             int64_t zc1, int x0, int y0, float kM, float nsmk) {
+__device__ __forceinline__ float sampler_rows(const CUtensorMap* umap, const CUtensorMap* mmap, const Params& P,
+                                              Smem& sm, int st, int64_t pstart, int64_t pend, int64_t zc0,
+                                              int64_t zc1, int x0, int y0, float kM, float nsmk, const FinConst& K) {
     const int lane = st & 31, w = st >> 5;
     const int nx = P.nx, ny = P.ny;
+    // FFDP_L3_SPLITFIN: rows 16 + 2 w, 16 + 2 w + 1 of column lane of the moment iteration it
+    // (plane pstart + it - R), after the moment warps' x stage of that iteration
+    constexpr int FOUT = 2;
+    float nsum_s = 0.0f;
+    const int foy = TY / 2 + FOUT * w;
+    bool fvout[FOUT];
+    int fcxy[FOUT];
+#pragma unroll
+    for (int j = 0; j < FOUT; ++j) {
+        fvout[j] = x0 + lane < nx && y0 + foy + j < ny;
+        fcxy[j] = win_count(x0 + lane, nx) * win_count(y0 + foy + j, ny);
+    }
+    // the handshake barriers count output planes k = p - R - zc0 (warm-up iterations have none)
+    auto fin_half = [&](int itm) {
+        const int64_t pm = pstart + itm;
+        const int k = (int)(pm - R - zc0);
+        mbar_wait(&sm.xdone[k % RING], (uint32_t)((k / RING) & 1));
+        float* go = P.g_u + 3 * ((pm - R - P.z_begin) * P.plane +
+                                 (fvout[0] ? (int64_t)(y0 + foy) * nx + x0 + lane : 0));
+        finalize_rows<FOUT>(P, sm, K, itm, pm - R, lane, foy, fvout, fcxy, go, 3 * nx, nsum_s);
+        mbar_arrive(&sm.ydone[k % RING]);
+    };
     // main column of this lane
     const int gxm = x0 + lane;
     const bool vxm = gxm < nx;
@@ -477,9 +592,12 @@ __device__ __forceinline__ void sampler_rows(const CUtensorMap* umap, const CUte
             }
         }
         mbar_arrive(&sm.sampled[slot]);
+        if (L3_SPLIT && p - 1 >= zc0 + R) fin_half(it - 1);
     }
+    if (L3_SPLIT && pend - 1 >= zc0 + R) fin_half((int)(pend - 1 - pstart));
     const unsigned anym = __ballot_sync(0xffffffffu, miss);
     if (anym && P.miss && lane == 0) atomicAdd(P.miss, __popc(anym));
+    return nsum_s;
 }
 
 // ------------------------------------------------------------------ moment warps
@@ -681,7 +799,8 @@ template <bool TMA>
 __device__ __forceinline__ float moment_rows(const CUtensorMap* fmap, const Params& P, Smem& sm, int mt,
                                              int64_t pstart, int64_t pend, int64_t zc0, int x0, int y0, float sf,
                                              float kF, float smv, float kM) {
-    constexpr int NM = 256, OUTR = NIN / NM, MR = SROWS, NJ = MR + 1;
+    // FFDP_L3_SPLITFIN: the moment warps finish rows 0-15 (2 per thread), the sampler warps 16-31
+    constexpr int NM = 256, OUTR = L3_SPLIT ? NIN / NM / 2 : NIN / NM, MR = SROWS, NJ = MR + 1;
     const int lane = mt & 31, w = mt >> 5;
     const float nsfk = -sf * kF, ikM = 1.0f / kM;
     auto issue = [&](int64_t p, int s) {
@@ -710,12 +829,8 @@ __device__ __forceinline__ float moment_rows(const CUtensorMap* fmap, const Para
     const int64_t pl3 = 3 * P.plane;
     float* go = P.g_u + 3 * ((zc0 - P.z_begin) * P.plane + (vout[0] ? (int64_t)(y0 + oy) * nx + gx : 0));
     const int rs = 3 * nx;
-    const float cAB = (float)(1.0 / (NWIN * NWIN * (double)QSCALE * (double)QSCALE));
-    const float cA = cAB / (kF * kM), cB = cAB / (kF * kF), cC = cAB / (kM * kM);
-    const float mF = (float)(1.0 / (NWIN * (double)QSCALE)) / kF, mM = (float)(1.0 / (NWIN * (double)QSCALE)) / kM;
-    const int32_t NU = (WIN * WIN * WIN) << 21;
-    const float gi2 = 2.0f * (float)P.gi, epsf = (float)P.eps;
-    const bool poison = !(fabsf(sf) <= 3.0e38f && fabsf(smv) <= 3.0e38f);
+    const FinConst K(P, sf, kF, smv, kM);
+    const bool poison = K.poison;
 
     int32_t zs[NJ][5];
 #pragma unroll
@@ -773,6 +888,10 @@ __device__ __forceinline__ float moment_rows(const CUtensorMap* fmap, const Para
         }
         moment_sync<NM>();
         if (!warm) {
+            // the sampler warps' half of the previous plane's outputs must have read xb
+            // (output planes k = p - R - zc0 index the handshake barriers)
+            const int k = (int)(p - R - zc0);
+            if (L3_SPLIT && k >= 1) mbar_wait(&sm.ydone[(k - 1) % RING], (uint32_t)(((k - 1) / RING) & 1));
 #pragma unroll
             for (int i = 0; i < (XJOBS + NM - 1) / NM; ++i) {
                 const int j = mt + NM * i;
@@ -787,59 +906,8 @@ __device__ __forceinline__ float moment_rows(const CUtensorMap* fmap, const Para
                 *reinterpret_cast<int4*>(&sm.xb[0][0][0] + rowch * TX + 4 * run) = make_int4(s0, s1, s2, s3);
             }
             moment_sync<NM>();
-            const int64_t q = p - R;
-            const int qslot = (it + RING - R) % RING, qg = (it + NG - R) % NG;
-            int32_t S[OUTR][5];
-#pragma unroll
-            for (int ch = 0; ch < 5; ++ch) {
-                int32_t r[OUTR + 2 * R];
-#pragma unroll
-                for (int k = 0; k < OUTR + 2 * R; ++k) r[k] = sm.xb[ch][oy + k][ox];
-                S[0][ch] = r[0] + r[1] + r[2] + r[3] + r[4] + r[5] + r[6];
-#pragma unroll
-                for (int j = 1; j < OUTR; ++j) S[j][ch] = S[j - 1][ch] + r[j + 2 * R] - r[j - 1];
-            }
-            const int cz = win_count(q, P.nz_global);
-#pragma unroll
-            for (int j = 0; j < OUTR; ++j) {
-                if (!vout[j]) continue;
-                const int32_t X = S[j][0], Y = S[j][1];
-                const int64_t TA = (int64_t)NU * S[j][4] - (int64_t)X * Y;
-                const int64_t TB = (int64_t)NU * S[j][2] - (int64_t)X * X;
-                const int64_t TC = (int64_t)NU * S[j][3] - (int64_t)Y * Y;
-                const int cw = cxy[j] * cz;
-                float a, b, cc, omw;
-                if (cw == WIN * WIN * WIN) {
-                    a = (float)TA * cA;
-                    b = (float)TB * cB;
-                    cc = (float)TC * cC;
-                    omw = 0.0f;
-                } else {
-                    const double U = (double)QSCALE, iUF = 1.0 / (U * (double)kF), iUM = 1.0 / (U * (double)kM);
-                    const double omc = NWIN - (double)cw, sfd = sf, smd = smv, cwd = cw, Xd = X, Yd = Y;
-                    const double invN2 = 1.0 / (NWIN * NWIN);
-                    a = (float)(((double)TA * (iUF * iUM) + omc * (smd * Xd * iUF + sfd * Yd * iUM + sfd * smd * cwd)) *
-                                invN2);
-                    b = (float)(((double)TB * (iUF * iUF) + omc * (2.0 * sfd * Xd * iUF + sfd * sfd * cwd)) * invN2);
-                    cc = (float)(((double)TC * (iUM * iUM) + omc * (2.0 * smd * Yd * iUM + smd * smd * cwd)) * invN2);
-                    omw = (float)(omc * (1.0 / NWIN));
-                }
-                const float D = fmaf(b, cc, epsf);
-                const float invD = __fdividef(1.0f, D);
-                nsum += a * a * invD;
-                const float gamma = gi2 * a * invD;
-                const float rab = a * b * invD;
-                const int hy = oy + j + R, hx = ox + R;
-                const float fq = sm.fr[qslot][hy * FW + hx + 1];
-                const float df = (fq - sf) - (float)X * mF + sf * omw;
-                const float dm = sm.br[qslot][hy * HX + hx] * ikM - (float)Y * mM + smv * omw;
-                const float gmw = poison ? __int_as_float(0x7fc00000) : gamma * fmaf(-dm, rab, df);
-                const int ii = (oy + j) * TX + ox;
-                float* o = go + j * rs;
-                o[0] = sm.gr[qg][0][ii] * gmw;
-                o[1] = sm.gr[qg][1][ii] * gmw;
-                o[2] = sm.gr[qg][2][ii] * gmw;
-            }
+            if (L3_SPLIT) mbar_arrive(&sm.xdone[k % RING]);
+            finalize_rows<OUTR>(P, sm, K, it, p - R, ox, oy, vout, cxy, go, rs, nsum);
             go += pl3;
         }
         mbar_arrive(&sm.consumed[slot]);
@@ -871,6 +939,8 @@ __global__ void __launch_bounds__(NT, 1) k_lncc_fused(const __grid_constant__ CU
             mbar_init(&sm.fbar[s], 1);
             mbar_init(&sm.sampled[s], SP::NS);
             mbar_init(&sm.consumed[s], SP::NM);
+            mbar_init(&sm.xdone[s], SP::NM);
+            mbar_init(&sm.ydone[s], SP::NS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -890,8 +960,8 @@ __global__ void __launch_bounds__(NT, 1) k_lncc_fused(const __grid_constant__ CU
         if (SP::RS != 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SP::RS));
 #if FFDP_L3_ROWS
         if (SP::NS == 256)
-            sampler_rows<TMA, FULLWIN, OFF32>(&umap, &mmap, P, sm, t - SP::NM, pstart, pend, zc0, zc1, x0, y0, kM,
-                                              -smv * kM);
+            nsum = sampler_rows<TMA, FULLWIN, OFF32>(&umap, &mmap, P, sm, t - SP::NM, pstart, pend, zc0, zc1, x0, y0,
+                                                     kM, -smv * kM, FinConst(P, sf, kF, smv, kM));
         else
 #endif
             sampler_warps<NM_, TMA, FULLWIN, OFF32>(&umap, &mmap, P, sm, t - SP::NM, pstart, pend, zc0, zc1, x0, y0,
