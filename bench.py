@@ -820,22 +820,43 @@ class HostStager:
 def run_e2e(args, st, f, u, A, t, loss, world):
     """End to end through the public API: every step copies the step's inputs (F, M, u)
     from host memory to the device, runs the step, and reads the loss back (8 bytes).
-    Inputs up to 8 GiB are pinned whole; larger ones (configs[4]) stay in pageable host
-    memory and go through HostStager's double-buffered pinned chunks."""
+    The host inputs are pinned whole when they take at most 60 % of the host's available
+    RAM (configs[4]: 74 GB of 196 GB; the DMA then runs at the PCIe rate, ~55 GB/s on the
+    B200 boxes, against ~43 GB/s through staging); otherwise they stay in pageable memory
+    and go through HostStager's double-buffered pinned chunks."""
     import torch
     m = st.mimg.interior
     nbytes = 4 * (f.numel() + m.numel() + u.numel())
     steps = max(3, min(args.steps, 20 if nbytes <= (8 << 30) else 3))
-    staged = nbytes > (8 << 30)
-    hf, hu = f.cpu(), u.cpu()
-    # M's host copy from the bordered layout a few planes at a time (a strided view: a whole-
-    # volume device temporary would not fit next to configs[4]'s records)
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 0
+    staged = nbytes > (8 << 30) and (os.environ.get("FFDP_E2E_STAGED") == "1" or nbytes > 0.6 * avail)
+    # host copies made straight from the device (M from its bordered layout a few planes at
+    # a time: a strided view, and a whole-volume device temporary would not fit next to
+    # configs[4]'s records)
+    hf = torch.empty(tuple(f.shape), dtype=torch.float32)
+    hu = torch.empty(tuple(u.shape), dtype=torch.float32)
     hm = torch.empty(tuple(m.shape), dtype=torch.float32)
-    for z0 in range(0, m.shape[0], 16):
-        hm[z0:z0 + 16].copy_(m[z0:z0 + 16])
+    for dst, src in ((hf, f), (hu, u), (hm, m)):
+        for z0 in range(0, src.shape[0], 16):
+            dst[z0:z0 + 16].copy_(src[z0:z0 + 16])
+    registered = []
     if not staged:
-        hf, hm, hu = (x.pin_memory() for x in (hf, hm, hu))
-        cp = lambda dst, src: dst.copy_(src, non_blocking=True)
+        # page-lock the buffers in place (cudaHostRegister; torch's pinned allocator would
+        # round each one up to a power of two: 103 instead of 74 GB at configs[4])
+        rt = torch.cuda.cudart()
+        for x in (hf, hu, hm):
+            if int(rt.cudaHostRegister(x.data_ptr(), x.numel() * 4, 0)) != 0:
+                raise RuntimeError("cudaHostRegister failed")
+            registered.append(x)
+
+        def cp(dst, src):
+            # 32 planes at a time: M's bordered destination is strided, and torch stages a
+            # strided H2D through a contiguous device temporary of the chunk's size
+            for z0 in range(0, src.shape[0], 32):
+                dst[z0:z0 + 32].copy_(src[z0:z0 + 32], non_blocking=True)
     else:
         stager = HostStager()
         cp = stager.copy
@@ -855,9 +876,12 @@ def run_e2e(args, st, f, u, A, t, loss, world):
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / steps * 1e3
     ms = max(e0.elapsed_time(e1) / steps, wall)
+    for x in registered:
+        torch.cuda.cudart().cudaHostUnregister(x.data_ptr())
     return {"value": round(world * f.numel() / (ms * 1e-3) / 1e9, 4), "unit": "Gvoxel/s",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8, "ms_per_step": round(ms, 3), "steps": steps,
             "host_buffers": "pageable, double-buffered pinned staging (256 MB chunks)" if staged else "pinned",
+            "host_available_bytes": int(avail),
             "loss": host_loss}
 
 
