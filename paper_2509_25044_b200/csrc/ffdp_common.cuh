@@ -16,6 +16,10 @@
 #include "../../include/ffdp.h"
 
 #define FFDP_FACE_SNAP 1e-9
+// gather_pad row pointers: 1 = one widened offset + 64-bit stride adds, 0 = four offsets
+#ifndef FFDP_GADDR
+#define FFDP_GADDR 1
+#endif
 
 namespace ffdp {
 
@@ -296,6 +300,32 @@ __device__ __forceinline__ Corners gather_pad(const Geom& g, const Cell& c, int&
     }
     const int32_t sy = (int32_t)g.sy;
     Corners k;
+#if FFDP_GADDR
+    if (OFF == 2) {
+        // one widened offset from the block origin for the first row pointer, the other three
+        // by 64-bit byte-stride adds; the origin is an opaque pointer (otherwise the compiler
+        // folds the border offset into every row pointer: a 64-bit subtract per pointer)
+        const uint32_t o = (uint32_t)(iz - g.wz0 + 2) * (uint32_t)g.sz + (uint32_t)(iy + 2) * (uint32_t)g.sy +
+                           (uint32_t)(ix + 2);
+        uint64_t org;
+        asm("mov.b64 %0, %1;" : "=l"(org) : "l"(g.img - (2 * g.sz + 2 * g.sy + 2)));
+        const char* p0 = reinterpret_cast<const char*>(reinterpret_cast<const float*>(org) + o);
+        const int64_t by = 4 * g.sy, bz = 4 * g.sz;
+        const float* q0 = reinterpret_cast<const float*>(p0);
+        const float* q1 = reinterpret_cast<const float*>(p0 + by);
+        const float* q2 = reinterpret_cast<const float*>(p0 + bz);
+        const float* q3 = reinterpret_cast<const float*>(p0 + bz + by);
+        k.v[0] = __ldg(q0);
+        k.v[1] = __ldg(q0 + 1);
+        k.v[2] = __ldg(q1);
+        k.v[3] = __ldg(q1 + 1);
+        k.v[4] = __ldg(q2);
+        k.v[5] = __ldg(q2 + 1);
+        k.v[6] = __ldg(q3);
+        k.v[7] = __ldg(q3 + 1);
+        return k;
+    }
+#endif
     if (OFF == 1) {
         // the resident window holds < 2^31 elements: 32-bit offsets, one wide add per row
         const int32_t sz = (int32_t)g.sz;
