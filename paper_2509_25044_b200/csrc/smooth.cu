@@ -24,9 +24,19 @@
 // channels); STORE reads and writes one field (24 B). The x/y halo re-reads of a plane
 // come from L2 (neighbouring tiles march the same planes).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstring>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "ffdp_common.cuh"
+
+// FFDP_SMOOTH_TMA = 1: the haloed input planes arrive by TMA (one 3-D tensor box per plane,
+// OOB zero fill = the zero padding) when rows are 16-byte multiples; else per-thread cp.async
+#ifndef FFDP_SMOOTH_TMA
+#define FFDP_SMOOTH_TMA 1
+#endif
 
 namespace ffdp {
 namespace sm {
@@ -61,13 +71,28 @@ __device__ __forceinline__ float wsum(const Params& P, int64_t g, int64_t n) {
 constexpr int NSTAGE = 3;  // input planes in flight (cp.async ring)
 
 template <int R, int CH>
-struct Smem {
+struct __align__(128) Smem {
     // ROW: floats per row, with room for the up-to-3-float shift that 16-byte aligns the
-    // row's first chunk (V16 loads); ROW is a multiple of 4 so every row starts aligned
+    // row's first chunk (V16 loads); ROW is a multiple of 4 so every row starts aligned.
+    // A stage is HY rows of ROW floats (the TMA box), padded to a 128-byte multiple.
     static constexpr int HX = TX + 2 * R, HY = TY + 2 * R, ROW = (CH * HX + 3 + 3) / 4 * 4;
-    float raw[NSTAGE][HY][ROW];  // haloed input planes, filled by cp.async (zero-fill outside)
+    static constexpr int STAGE = (HY * ROW + 31) / 32 * 32;
+    float raw[NSTAGE][STAGE];    // haloed input planes, filled by TMA / cp.async (zero outside)
     float X[HY][TX * CH];        // x-convolved rows (the top barrier of the next plane protects it)
+    unsigned long long bar[NSTAGE];  // TMA: plane landed
 };
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\tselp.u32 %0, 1, "
+            "0, p;\n}"
+            : "=r"(ok)
+            : "r"(saddr(b)), "r"(parity)
+            : "memory");
+}
 
 // 4-byte asynchronous global -> shared copy; src_bytes = 0 writes a zero (no global read).
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
@@ -82,13 +107,16 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// V16: rows of CH * nx floats start 16-byte aligned, so the haloed tile row moves in
-// 16-byte cp.async chunks (the row's first element sits `sh` floats into the stage row;
-// chunks left of the lattice or past its end are zero-filled by src_bytes).
-template <int R, int CH, bool ADAM, bool V16>
-__global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
+// MODE 1 / 2 (V16): rows of CH * nx floats start 16-byte aligned, so the haloed tile row
+// moves in 16-byte cp.async chunks (the row's first element sits `sh` floats into the stage
+// row; chunks left of the lattice or past its end are zero-filled by src_bytes), or (MODE 2)
+// the whole haloed plane is one TMA box issued by thread 0 (OOB zero fill), which leaves the
+// other threads no copy instructions at all. MODE 0: 4-byte cp.async per element.
+template <int R, int CH, bool ADAM, int MODE>
+__global__ void __launch_bounds__(NT, 2) k_smooth(const __grid_constant__ CUtensorMap tmap, const Params P) {
     using S = Smem<R, CH>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool V16 = MODE >= 1, TMA = MODE == 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     S& sm = *reinterpret_cast<S*>(smem_raw);
     const int t = threadIdx.x;
     const int ox = t % TX, oy = t / TX;
@@ -145,11 +173,35 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
             src_bytes[k] = ok ? 4 : 0;
         }
     }
+    if (TMA) {
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < NSTAGE; ++s)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&sm.bar[s])) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     auto issue = [&](int64_t p, int stage) {
+        if (TMA) {
+            // planes outside the volume lie outside the buffer's z extent: zero filled
+            if (t == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the stage
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&sm.bar[stage])),
+                             "r"((uint32_t)(S::HY * S::ROW * 4))
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3, %4}], [%5];" ::"r"(saddr(&sm.raw[stage][0])),
+                    "l"(&tmap), "r"(e0 - sh), "r"(y0 - R), "r"((int)(p - P.buf_z0)), "r"(saddr(&sm.bar[stage]))
+                    : "memory");
+            }
+            return;
+        }
         const bool pin = p >= 0 && p < P.nz_global;
         const float* src = P.in + (pin ? (p - P.buf_z0) * P.plane * CH : 0);
         asm("" : "+l"(src));  // one plane base; each copy is then one wide add of its offset
-        float* dst = &sm.raw[stage][0][0];
+        float* dst = &sm.raw[stage][0];
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
             if (dst_off[k] >= 0) {
@@ -183,7 +235,7 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
 #pragma unroll
     for (int k = 0; k < NSTAGE - 1; ++k) {
         if (pstart + k < pend) issue(pstart + k, k);
-        else cp_async_commit();
+        else if (!TMA) cp_async_commit();
     }
     // Adam operands of the next output voxel, loaded one plane ahead
     float pu[CH], pm1[CH], pm2[CH];
@@ -205,13 +257,16 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
         // barrier after that plane's x taps)
         const int st_next = stage == 0 ? NSTAGE - 1 : stage - 1;
         if (p + NSTAGE - 1 < pend) issue(p + NSTAGE - 1, st_next);
-        else cp_async_commit();
-        cp_async_wait<NSTAGE - 1>();  // this thread's copies of plane p have landed
-        __syncthreads();             // everyone's have; X is free
+        else if (!TMA) cp_async_commit();
+        if (TMA)
+            mbar_wait(&sm.bar[stage], (uint32_t)(((p - pstart) / NSTAGE) & 1));  // plane p has landed
+        else
+            cp_async_wait<NSTAGE - 1>();  // this thread's copies of plane p have landed
+        __syncthreads();                  // everyone's have; X is free
 #pragma unroll
         for (int jj = 0; jj < XJ; ++jj) {
             if (xj_in[jj] < 0) continue;
-            const float* in = &sm.raw[stage][0][0] + xj_in[jj];
+            const float* in = &sm.raw[stage][0] + xj_in[jj];
             float w_[XR + 2 * R];
 #pragma unroll
             for (int i = 0; i < XR + 2 * R; ++i) w_[i] = in[i * CH];
@@ -277,7 +332,7 @@ __global__ void __launch_bounds__(NT, 2) k_smooth(const Params P) {
             for (int c = 0; c < CH; ++c) P.out[o + c] = v[c];
         }
     }
-    cp_async_wait<0>();
+    if (!TMA) cp_async_wait<0>();
 }
 
 // Planes per z chunk: the fewest (waves x planes-with-halo) over chunk counts.
@@ -293,16 +348,31 @@ inline int32_t pick_zchunk(int64_t tiles, int64_t nzs, int64_t capacity, int R) 
     return (int32_t)best;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::atomic<int> state{0};
+    if (state.load() == 0) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        state.store(fn ? 1 : 2);
+    }
+    return fn;
+}
+
 template <int R, int CH, bool ADAM>
 int launch(Params P, cudaStream_t st) {
-    const size_t smem = sizeof(Smem<R, CH>);
+    using S = Smem<R, CH>;
+    const size_t smem = sizeof(S);
     static std::atomic<unsigned long long> attr_mask{0};
     static int per_sm = 1;
     once_per_device(attr_mask, [&] {
-        for (auto fn : {k_smooth<R, CH, ADAM, true>, k_smooth<R, CH, ADAM, false>})
+        for (auto fn : {k_smooth<R, CH, ADAM, 0>, k_smooth<R, CH, ADAM, 1>, k_smooth<R, CH, ADAM, 2>})
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int p = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, k_smooth<R, CH, ADAM, true>, NT, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, k_smooth<R, CH, ADAM, 1>, NT, smem);
         per_sm = std::max(p, 1);
     });
     const bool v16 = ((uintptr_t)P.in & 15) == 0 && (P.nx * CH) % 4 == 0;
@@ -312,10 +382,29 @@ int launch(Params P, cudaStream_t st) {
     const int64_t chunks = (nzs + P.zchunk - 1) / P.zchunk;
     if (ty > 65535 || chunks > 65535) return set_error(FFDP_INVALID_ARGUMENT, "gp_convolve: grid too large");
     const dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)chunks);
-    if (v16)
-        k_smooth<R, CH, ADAM, true><<<grid, NT, smem, st>>>(P);
+    // the input field as a 3-D tensor (CH * nx floats per row, ny rows, the buffer's planes);
+    // the box is one stage: HY rows of ROW floats starting at a 16-byte aligned column
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    bool tma = false;
+    if (FFDP_SMOOTH_TMA && v16 && S::ROW <= 256 && S::HY <= 256) {
+        if (auto enc = tensor_map_encoder()) {
+            const cuuint64_t n0 = (cuuint64_t)P.nx * CH, n1 = (cuuint64_t)P.ny, n2 = (cuuint64_t)(P.buf_z1 - P.buf_z0);
+            const cuuint64_t dims[3] = {n0, n1, n2};
+            const cuuint64_t strides[2] = {n0 * 4, n0 * n1 * 4};
+            const cuuint32_t box[3] = {(cuuint32_t)S::ROW, (cuuint32_t)S::HY, 1};
+            const cuuint32_t es[3] = {1, 1, 1};
+            tma = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(P.in), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+    }
+    if (tma)
+        k_smooth<R, CH, ADAM, 2><<<grid, NT, smem, st>>>(map, P);
+    else if (v16)
+        k_smooth<R, CH, ADAM, 1><<<grid, NT, smem, st>>>(map, P);
     else
-        k_smooth<R, CH, ADAM, false><<<grid, NT, smem, st>>>(P);
+        k_smooth<R, CH, ADAM, 0><<<grid, NT, smem, st>>>(map, P);
     return check_launch(ADAM ? "sobolev_adam" : "gp_convolve");
 }
 
