@@ -771,6 +771,119 @@ __global__ void __launch_bounds__(256, FFDP_GR_MINB) k_step_mi_grad_rec(const fl
     }
 }
 
+// FFDP_GR_TMA = 1: pass 2 from the records as a bulk-copy stream. A persistent CTA takes
+// chunks of GRT_CHUNK voxels: F and the records arrive by 1-D bulk copies
+// (cp.async.bulk, one mbarrier per stage, two stages in flight), the threads compute from
+// shared memory (voxels t + 256 j: conflict-free 16-byte record reads) and write g_u into a
+// shared tile that one bulk store (cp.async.bulk ... bulk_group) moves out. The per-thread
+// load / store instructions of the LDG form go, and the copy engine keeps a CTA's next two
+// chunks (40 KB) in flight. Arithmetic identical to k_step_mi_grad_rec.
+#ifndef FFDP_GR_TMA
+#define FFDP_GR_TMA 1
+#endif
+#ifndef FFDP_GR_STAGES
+#define FFDP_GR_STAGES 2
+#endif
+constexpr int GRT_CHUNK = 1024, GRT_NT = 256, GRT_ST = FFDP_GR_STAGES;  // input stages (chunks in flight + 1)
+struct __align__(128) GrtSmem {
+    float f[GRT_ST][GRT_CHUNK];
+    float4 rec[GRT_ST][GRT_CHUNK];
+    float g[2][3 * GRT_CHUNK];
+    unsigned long long full[GRT_ST];
+};
+
+__device__ __forceinline__ uint32_t grt_saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(GRT_NT, 2) k_step_mi_grad_rec_bulk(const float* __restrict__ f,
+                                                                    const float4* __restrict__ rec,
+                                                                    float* __restrict__ g_u, int64_t nchunks,
+                                                                    const double* table, int B) {
+    extern __shared__ __align__(128) unsigned char grt_raw[];
+    GrtSmem& sm = *reinterpret_cast<GrtSmem*>(grt_raw);
+    float* sg = reinterpret_cast<float*>(grt_raw + sizeof(GrtSmem));
+    const int LD = B + 2 * PAD, CP = (LD + 3) / 4 * 4, CS = LD * CP;
+    const int t = threadIdx.x;
+    auto issue = [&](int64_t c, int s) {
+        const uint32_t bar = grt_saddr(&sm.full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(GRT_CHUNK * 20) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         grt_saddr(&sm.f[s][0])),
+                     "l"(f + c * GRT_CHUNK), "r"(GRT_CHUNK * 4), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         grt_saddr(&sm.rec[s][0])),
+                     "l"(rec + c * GRT_CHUNK), "r"(GRT_CHUNK * 16), "r"(bar)
+                     : "memory");
+    };
+    if (t == 0) {
+        for (int q = 0; q < GRT_ST; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(grt_saddr(&sm.full[q])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int q = 0; q < GRT_ST; ++q)
+            if (blockIdx.x + (int64_t)q * gridDim.x < nchunks) issue(blockIdx.x + (int64_t)q * gridDim.x, q);
+    }
+    {
+        const double* gh = table + B * B + 2 * B;
+        for (int q = t; q < 4 * CS; q += GRT_NT) {
+            const int c = q / CS, r = (q % CS) / CP, k = q % CP;
+            const int m = r - PAD, nn = k + c - PAD;
+            sg[q] = (m >= 0 && m < B && nn >= 0 && nn < B) ? (float)gh[m * B + nn] : 0.0f;
+        }
+        __syncthreads();
+    }
+    auto dl = [&](float fv, float mw) {
+        const BS4 bi = bspline_bins<false>(fv, B);
+        const BS4 bj = bspline_bins<true>(mw, B);
+        const int n0 = bj.m_lo + PAD;
+        const float4* gr = reinterpret_cast<const float4*>(sg + (n0 & 3) * CS + (bi.m_lo + PAD) * CP + (n0 & ~3));
+        float gj = 0.0f;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const float4 g = gr[a * (CP / 4)];
+            float acc = g.x * bj.w[0];
+            acc = fmaf(g.y, bj.w[1], acc);
+            acc = fmaf(g.z, bj.w[2], acc);
+            acc = fmaf(g.w, bj.w[3], acc);
+            gj = fmaf(bi.k[a], acc, gj);
+        }
+        return gj;
+    };
+    int i = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++i) {
+        const int s = i % GRT_ST, go = i & 1;
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\tselp.u32 %0, 1, "
+                "0, p;\n}"
+                : "=r"(ok)
+                : "r"(grt_saddr(&sm.full[s])), "r"((uint32_t)((i / GRT_ST) & 1))
+                : "memory");
+#pragma unroll
+        for (int j = 0; j < GRT_CHUNK / GRT_NT; ++j) {
+            const int v = t + GRT_NT * j;
+            const float4 r = sm.rec[s][v];
+            const float g = dl(sm.f[s][v], r.x);
+            sm.g[go][3 * v] = r.y * g;
+            sm.g[go][3 * v + 1] = r.z * g;
+            sm.g[go][3 * v + 2] = r.w * g;
+        }
+        // the store of two chunks ago (same g tile) has finished reading before anyone rewrites
+        // it: thread 0 waits for every earlier store's read before the barrier
+        if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g_u + 3 * c * GRT_CHUNK),
+                         "r"(grt_saddr(&sm.g[go][0])), "r"(GRT_CHUNK * 12)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (c + GRT_ST * (int64_t)gridDim.x < nchunks) issue(c + GRT_ST * (int64_t)gridDim.x, s);
+        }
+    }
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void k_hist_to_raw(const unsigned long long* h, int n, double inv_scale, double* raw) {
     for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x)
         raw[i] += (double)h[i] * inv_scale;
@@ -957,7 +1070,7 @@ int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ff
         return set_error(FFDP_INVALID_ARGUMENT, "step_mi: records need the B-spline Parzen kernel");
     const int B = k.bins;
     const float* fi = f + (s.z_begin - s.buf_z0) * d.nx * d.ny;  // interior planes
-    const int64_t n = d.nx * d.ny * (s.z_end - s.z_begin);
+    const int64_t n_all = d.nx * d.ny * (s.z_end - s.z_begin);
     const size_t smem = sizeof(float) * grad_tab_floats(B);
     static std::atomic<unsigned long long> attr_mask{0};  // B up to 64: the 4 table copies may exceed 48 KB
     once_per_device(attr_mask, [&] {
@@ -965,6 +1078,27 @@ int mi_grad_rec(const float* f, const ffdp_dims& d, const ffdp_slab& s, const ff
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * grad_tab_floats(64)));
     });
     const bool vec = (((uintptr_t)fi | (uintptr_t)rec | (uintptr_t)g_u) & 15) == 0;
+    int64_t n = n_all;
+    if (FFDP_GR_TMA && vec && n_all >= (int64_t)GRT_CHUNK * num_sms()) {
+        // the chunk-aligned bulk part, then the < GRT_CHUNK tail voxels below
+        const int64_t nch = n_all / GRT_CHUNK;
+        const size_t smem2 = sizeof(GrtSmem) + smem;
+        static std::atomic<unsigned long long> attr2{0};
+        once_per_device(attr2, [&] {
+            cudaFuncSetAttribute(k_step_mi_grad_rec_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(GrtSmem) + sizeof(float) * grad_tab_floats(64)));
+        });
+        const int grid2 = (int)std::min<int64_t>(nch, 2 * (int64_t)num_sms());
+        k_step_mi_grad_rec_bulk<<<grid2, GRT_NT, smem2, st>>>(fi, reinterpret_cast<const float4*>(rec), g_u, nch,
+                                                              table, B);
+        if (int rc = check_launch("step_mi_grad_rec")) return rc;
+        const int64_t done = nch * GRT_CHUNK;
+        n = n_all - done;
+        if (n == 0) return FFDP_OK;
+        fi += done;
+        rec += 4 * done;
+        g_u += 3 * done;
+    }
     const int64_t work = vec ? n / 4 : n;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)FFDP_GR_CTAS * num_sms()));
     if (vec)
